@@ -1,0 +1,195 @@
+// Device-resident semi-naive fixpoint engine (P/src/engine.cpp re-designed
+// for B200).
+//
+// Relation storage in HBM: every version (FULL, DELTA) of a relation is a
+// set of SoA u32 columns kept *sorted lexicographically and distinct*. That
+// one invariant replaces the reference's per-column (raw, sorted_idx,
+// hash) triple for the engine's purposes:
+//   - a join on column 0 probes contiguous runs of the version itself;
+//     other join columns get a cached sorted copy;
+//   - dedup of NEW against FULL and the FULL <- FULL u DELTA merge become a
+//     single merge-path pass over two sorted sequences (no triangle join);
+//   - DELTA comes out of that pass already sorted, ready to be indexed.
+// Rows are compared as packed row keys: W = ceil(arity/2) u64 words, word w
+// = (c[2w] << s) | c[2w+1], with s the bit width of the active domain (no
+// IDB value can exceed the EDB/constant maximum: heads only project body
+// variables).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "column.h"
+#include "fv_common.cuh"
+
+namespace fv {
+
+// ---- plan IR (P/include/colog/compiler.hpp:14-53) --------------------------
+
+struct ColRef {
+    u32 source = 0, col = 0;
+    bool operator==(const ColRef& o) const { return source == o.source && col == o.col; }
+    bool operator<(const ColRef& o) const {
+        return source != o.source ? source < o.source : col < o.col;
+    }
+};
+
+struct PlanSource {
+    std::string relation;
+    u32 arity = 0;
+    std::vector<std::pair<u32, u32>> const_selects;  // (col, value)
+    std::vector<std::pair<u32, u32>> self_eqs;       // (first col, repeated col)
+    bool constrained() const { return !const_selects.empty() || !self_eqs.empty(); }
+};
+
+struct PlanJoin {
+    u32 right_source = 0;
+    ColRef left;
+    u32 right_col = 0;
+    std::vector<std::pair<ColRef, u32>> residual_eq;
+};
+
+struct Plan {
+    std::string head;
+    u32 head_arity = 0;
+    std::vector<PlanSource> sources;
+    std::vector<PlanJoin> joins;
+    std::vector<ColRef> output_cols;
+    std::vector<std::pair<u32, u32>> guard_neq;
+};
+
+struct RelationDecl {
+    std::string name;
+    u32 arity = 0;
+};
+
+struct FactsBlock {
+    std::string relation;
+    u32 arity = 0;
+    u64 n = 0;
+    std::vector<const u32*> cols;  // host SoA
+};
+
+// ---- device relation storage ------------------------------------------------
+
+struct DevVersion {
+    u64 n = 0;
+    std::vector<DBuf<u32>> cols;
+    std::vector<const u32*> ptrs() const {
+        std::vector<const u32*> p;
+        for (auto& c : cols) p.push_back(c.get());
+        return p;
+    }
+};
+
+// Join index over one column of a version: rows grouped by the key column.
+struct JoinIndex {
+    const DevVersion* rows = nullptr;  // rows ordered by the key column
+    DevVersion owned;                  // sorted copy when the key is not column 0
+    u64 n_unique = 0;
+    DBuf<u32> ukeys, ustart, ucount;
+    HashIndex ht;
+};
+
+struct RelState {
+    std::string name;
+    u32 arity = 0;
+    bool idb = false;
+    DevVersion full, delta;
+    // (0 = full, 1 = delta, col) -> index; invalidated when the version changes
+    std::map<std::pair<int, u32>, std::unique_ptr<JoinIndex>> indexes;
+};
+
+struct IterStat {
+    u64 iteration = 0;
+    std::string relation;
+    u64 delta_rows = 0, full_rows = 0, merges = 0;
+    double elapsed_ms = 0.0;
+};
+
+struct EvalState {
+    Ctx* ctx = nullptr;
+    std::map<std::string, std::unique_ptr<RelState>> relations;  // std::map order
+    u64 iterations = 0;
+    std::vector<IterStat> stats;
+    double elapsed_ms = 0.0;
+    u32 key_shift = 32;
+};
+
+std::unique_ptr<EvalState> evaluate(Ctx* c, const std::vector<RelationDecl>& decls,
+                                    const std::vector<Plan>& plans,
+                                    const std::vector<FactsBlock>& facts);
+
+// Validate plan structure against the declarations (throws FV_ERR_PLAN).
+void check_plans(const std::vector<RelationDecl>& decls, const std::vector<Plan>& plans);
+
+// Lexicographically sorted row-major dump of FULL (host).
+std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel);
+u64 fingerprint(const EvalState& s, const std::string& rel);
+
+// ---- kernels (engine_kernels.cu) ---------------------------------------------
+
+constexpr int kMaxSlots = 16;
+constexpr int kMaxFilters = 8;
+
+// One operand column of the materialize / project kernels.
+struct SlotRef {
+    const u32* ptr = nullptr;
+    u32 side = 0;  // 0: probe-side row i, 1: build-side position p
+};
+
+enum FilterOp : u32 { kFilterEq = 0, kFilterNeq = 1, kFilterConst = 2 };
+
+struct Filter {
+    SlotRef a, b;
+    u32 op = kFilterEq;
+    u32 value = 0;  // kFilterConst
+};
+
+struct OutSpec {
+    u32 n_out = 0;  // columns
+    SlotRef col[kMaxSlots];
+    u32 n_filters = 0;
+    Filter f[kMaxFilters];
+    // key mode: write W = ceil(n_out/2) packed u64 words per row
+    u32 key_mode = 0;
+    u32 shift = 32;
+    u64* keys[4] = {nullptr, nullptr, nullptr, nullptr};
+    u32* out_cols[kMaxSlots] = {nullptr};
+    u64* d_count = nullptr;  // compaction counter (n_filters > 0)
+};
+
+struct RowFilter {  // predicate on probe-side rows (source constraints)
+    u32 n = 0;
+    Filter f[kMaxFilters];
+};
+
+// counts[i] = run length of probe[i] in the index (0 on miss or when the
+// probe row fails `pred`); starts[i] = run start.
+void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, const RowFilter& pred,
+                        u32* starts, u32* counts);
+// Ascending ids of rows passing `pred` (side 0); returns the count.
+u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids);
+// Output-partitioned expansion of T join outputs into `spec`.
+void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32* starts,
+                        const OutSpec& spec);
+// Single-source projection of n rows (side 0 only) into `spec`.
+void engine_project(Ctx* c, u64 n, const OutSpec& spec);
+// RLE of a sorted key column into (ukeys, ustart, ucount) + hash table.
+void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx);
+// Pack SoA columns into W key words.
+void engine_pack_keys(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 shift, u64* const* words);
+// Merge sorted distinct A (SoA, arity) with sorted B keys (W words, dups
+// allowed): C = A u B (SoA), D = B \ A distinct (SoA). Returns |D| (device
+// scalar written to *d_new; |C| = n_a + |D|).
+void engine_merge(Ctx* c, const std::vector<const u32*>& a_cols, u64 n_a, u64* const* b_words, u64 n_b,
+                  u32 arity, u32 shift, const std::vector<u32*>& c_cols,
+                  const std::vector<u32*>& d_cols, u64* d_new);
+u64 engine_fingerprint(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 arity);
+// Sort W-word keys in place (LSD over words with a permutation payload).
+void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift);
+
+}  // namespace fv

@@ -1,0 +1,724 @@
+// sm_100a kernels of the fixpoint engine (see engine.h for the data layout).
+//
+//   probe_count   join phase 1 (Algorithm 1, P/src/kernels.cpp:59-92): one
+//                 hash probe per probe row -> (run start, run length)
+//   materialize   join phase 2 (kernels.cpp:104-123) fused with the residual
+//                 equalities (kernels.cpp:137-165), the != guards
+//                 (engine.cpp:128-145) and the head projection
+//                 (engine.cpp:122-125): output-partitioned, each CTA expands
+//                 a fixed tile of join outputs and writes head rows directly
+//                 (as packed row keys for the dedup sort) — no IdPairSet,
+//                 no per-source id arrays, no wide Version.
+//   merge         dedup_rows + deduplicate + difference + merge_delta
+//                 (relation.cpp:71-108, kernels.cpp:210-268) as ONE
+//                 merge-path pass over sorted FULL and sorted candidates.
+#include "engine.h"
+#include "prim.cuh"
+#include "radix_sort.h"
+
+namespace fv {
+
+namespace {
+
+unsigned grid_for(u64 n, int block = 256) {
+    const u64 want = ceil_div(n, block);
+    const u64 cap = u64(kNumSMs) * 16;
+    return static_cast<unsigned>(want == 0 ? 1 : (want < cap ? want : cap));
+}
+
+#define GRID_STRIDE(i, n) \
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); i += u64(gridDim.x) * blockDim.x)
+
+__device__ __forceinline__ u32 slot(const SlotRef& s, u64 i, u64 p) { return s.ptr[s.side ? p : i]; }
+
+__device__ __forceinline__ bool pass_filters(const Filter* f, u32 n, u64 i, u64 p) {
+#pragma unroll
+    for (int k = 0; k < kMaxFilters; ++k) {
+        if (k >= static_cast<int>(n)) break;
+        const u32 a = slot(f[k].a, i, p);
+        if (f[k].op == kFilterConst) {
+            if (a != f[k].value) return false;
+        } else {
+            const u32 b = slot(f[k].b, i, p);
+            if ((a == b) != (f[k].op == kFilterEq)) return false;
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool ht_lookup(const u64* __restrict__ slots, u32 mask, u32 key, u32* idx) {
+    u32 h = hash32(key) & mask;
+    while (true) {
+        const u64 s = __ldg(slots + h);
+        if (s == kEmptySlot) return false;
+        if (static_cast<u32>(s >> 32) == key) {
+            *idx = static_cast<u32>(s);
+            return true;
+        }
+        h = (h + 1) & mask;
+    }
+}
+
+__global__ void probe_count_kernel(const u32* __restrict__ probe, u64 n, const u64* __restrict__ slots,
+                                   u32 mask, const u32* __restrict__ ustart, const u32* __restrict__ ucount,
+                                   RowFilter pred, u32* __restrict__ starts, u32* __restrict__ counts) {
+    GRID_STRIDE(i, n) {
+        u32 s = 0, c = 0, r;
+        if (pass_filters(pred.f, pred.n, i, 0) && ht_lookup(slots, mask, probe[i], &r)) {
+            s = ustart[r];
+            c = ucount[r];
+        }
+        starts[i] = s;
+        counts[i] = c;
+    }
+}
+
+// Write one output row (values computed from slots) at position pos.
+__device__ __forceinline__ void write_row(const OutSpec& spec, u64 pos, u64 i, u64 p) {
+    if (spec.key_mode) {
+        const u32 w = (spec.n_out + 1) / 2;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= static_cast<int>(w)) break;
+            const u64 hi = slot(spec.col[2 * k], i, p);
+            u64 word;
+            if (2 * k + 1 < static_cast<int>(spec.n_out))
+                word = (hi << spec.shift) | slot(spec.col[2 * k + 1], i, p);
+            else
+                word = hi;
+            spec.keys[k][pos] = word;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kMaxSlots; ++k) {
+            if (k >= static_cast<int>(spec.n_out)) break;
+            spec.out_cols[k][pos] = slot(spec.col[k], i, p);
+        }
+    }
+}
+
+constexpr int kMatBlock = 256;
+constexpr int kMatItems = 8;
+constexpr int kMatTile = kMatBlock * kMatItems;
+
+__device__ __forceinline__ u64 upper_bound_u64(const u64* __restrict__ a, u64 len, u64 x) {
+    u64 lo = 0, hi = len;
+    while (lo < hi) {
+        const u64 mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Block-wide exclusive sum of u32 (256 threads); returns prefix, *total.
+__device__ __forceinline__ u32 block_excl_u32(u32 v, u32* s_warp, u32* total) {
+    const u32 lane = lane_id(), warp = threadIdx.x >> 5;
+    u32 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<u32>(o)) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u32 run = 0;
+        for (int w = 0; w < kMatBlock / 32; ++w) {
+            const u32 t = s_warp[w];
+            s_warp[w] = run;
+            run += t;
+        }
+        s_warp[kMatBlock / 32] = run;
+    }
+    __syncthreads();
+    const u32 r = s_warp[warp] + x - v;
+    *total = s_warp[kMatBlock / 32];
+    __syncthreads();
+    return r;
+}
+
+// Output-partitioned join expansion (see lbs_kernel in column_ops.cu).
+template <bool COMPACT>
+__global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __restrict__ offsets, u64 m,
+                                                                 u64 total, const u32* __restrict__ starts,
+                                                                 OutSpec spec) {
+    __shared__ u32 s_owner[kMatTile];
+    __shared__ u64 s_jlo, s_jhi, s_base;
+    __shared__ u32 s_warp[kMatBlock / 32 + 1];
+    const u32 tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    const u64 o0 = u64(blockIdx.x) * kMatTile;
+    const u64 o_end = min(o0 + kMatTile, total);
+    if (tid == 0) {
+        s_jlo = upper_bound_u64(offsets, m + 1, o0) - 1;
+        s_jhi = upper_bound_u64(offsets, m + 1, o_end - 1) - 1;
+    }
+    for (u32 i = tid; i < kMatTile; i += kMatBlock) s_owner[i] = 0;
+    __syncthreads();
+    const u64 jlo = s_jlo, jhi = s_jhi;
+    for (u64 j = jlo + 1 + tid; j <= jhi; j += kMatBlock)
+        atomicMax(&s_owner[offsets[j] - o0], static_cast<u32>(j - jlo));
+    __syncthreads();
+    {
+        u32 v[kMatItems];
+        u32 run = 0;
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k) {
+            run = max(run, s_owner[tid * kMatItems + k]);
+            v[k] = run;
+        }
+        u32 x = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= static_cast<u32>(o)) x = max(x, y);
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        u32 carry = 0;
+        for (u32 w = 0; w < warp; ++w) carry = max(carry, s_warp[w]);
+        const u32 prev = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane > 0) carry = max(carry, prev);
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k) s_owner[tid * kMatItems + k] = max(v[k], carry);
+        __syncthreads();
+    }
+    // Items are strided by the block size so consecutive lanes take
+    // consecutive outputs (coalesced build-side reads and output writes).
+    u64 ii[kMatItems];
+    u32 pp[kMatItems];
+    u32 keep_mask = 0;
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k) {
+        const u32 local = k * kMatBlock + tid;
+        const u64 o = o0 + local;
+        ii[k] = 0;
+        pp[k] = 0;
+        if (o < o_end) {
+            const u64 i = jlo + s_owner[local];
+            const u64 p = starts[i] + (o - offsets[i]);
+            ii[k] = i;
+            pp[k] = static_cast<u32>(p);
+            if (!COMPACT || pass_filters(spec.f, spec.n_filters, i, p)) keep_mask |= 1u << k;
+        }
+    }
+    if (!COMPACT) {
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k)
+            if (keep_mask & (1u << k)) write_row(spec, o0 + k * kMatBlock + tid, ii[k], pp[k]);
+        return;
+    }
+    u32 tot;
+    const u32 excl = block_excl_u32(__popc(keep_mask), s_warp, &tot);
+    if (tid == 0) s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(spec.d_count),
+                                           static_cast<unsigned long long>(tot))
+                               : 0;
+    __syncthreads();
+    u64 pos = s_base + excl;
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k)
+        if (keep_mask & (1u << k)) write_row(spec, pos++, ii[k], pp[k]);
+}
+
+template <bool COMPACT>
+__global__ void __launch_bounds__(kMatBlock) project_kernel(u64 n, OutSpec spec) {
+    __shared__ u32 s_warp[kMatBlock / 32 + 1];
+    __shared__ u64 s_base;
+    const u64 r0 = u64(blockIdx.x) * kMatTile;
+    u32 keep_mask = 0;
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k) {
+        const u64 i = r0 + k * kMatBlock + threadIdx.x;
+        if (i < n && (!COMPACT || pass_filters(spec.f, spec.n_filters, i, 0))) keep_mask |= 1u << k;
+    }
+    if (!COMPACT) {
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k)
+            if (keep_mask & (1u << k)) {
+                const u64 i = r0 + k * kMatBlock + threadIdx.x;
+                write_row(spec, i, i, 0);
+            }
+        return;
+    }
+    u32 tot;
+    const u32 excl = block_excl_u32(__popc(keep_mask), s_warp, &tot);
+    if (threadIdx.x == 0)
+        s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(spec.d_count),
+                                 static_cast<unsigned long long>(tot))
+                     : 0;
+    __syncthreads();
+    u64 pos = s_base + excl;
+#pragma unroll
+    for (int k = 0; k < kMatItems; ++k)
+        if (keep_mask & (1u << k)) {
+            const u64 i = r0 + k * kMatBlock + threadIdx.x;
+            write_row(spec, pos++, i, 0);
+        }
+}
+
+// ---- runs / hash for join indexes ------------------------------------------------
+
+struct RunsOp {
+    const u32* keys;
+    u32* ukeys;
+    u32* ustart;
+    __device__ u64 value(u64 i) const { return (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0; }
+    __device__ void emit(u64 i, u64 p, u64 v) const {
+        if (v) {
+            ukeys[p] = keys[i];
+            ustart[p] = static_cast<u32>(i);
+        }
+    }
+};
+
+__global__ void runs_count_kernel(const u32* __restrict__ ustart, u32* __restrict__ ucount, u64 nu, u64 n) {
+    GRID_STRIDE(i, nu) {
+        const u64 end = i + 1 < nu ? ustart[i + 1] : n;
+        ucount[i] = static_cast<u32>(end - ustart[i]);
+    }
+}
+
+__global__ void hash_build_kernel(const u32* __restrict__ ukeys, u64 nu, unsigned long long* __restrict__ slots,
+                                  u32 mask) {
+    GRID_STRIDE(i, nu) {
+        const u32 key = ukeys[i];
+        const unsigned long long packed = (static_cast<unsigned long long>(key) << 32) | u32(i);
+        u32 h = hash32(key) & mask;
+        while (atomicCAS(slots + h, ~0ull, packed) != ~0ull) h = (h + 1) & mask;
+    }
+}
+
+// ---- keys ------------------------------------------------------------------------------
+
+struct Cols8 {
+    const u32* p[FV_MAX_ARITY];
+};
+struct OutCols8 {
+    u32* p[FV_MAX_ARITY];
+};
+struct Words4 {
+    u64* p[4];
+};
+
+__device__ __forceinline__ u64 pack_word(const Cols8& c, u32 arity, u32 w, u64 row, u32 shift) {
+    const u64 hi = c.p[2 * w][row];
+    if (2 * w + 1 < arity) return (hi << shift) | c.p[2 * w + 1][row];
+    return hi;
+}
+
+__global__ void pack_kernel(Cols8 c, u32 arity, u64 n, u32 shift, Words4 out) {
+    const u32 W = (arity + 1) / 2;
+    GRID_STRIDE(i, n) {
+        for (u32 w = 0; w < W; ++w) out.p[w][i] = pack_word(c, arity, w, i, shift);
+    }
+}
+
+__global__ void gather_u64_kernel(const u64* __restrict__ src, const u32* __restrict__ idx,
+                                  u64* __restrict__ out, u64 n) {
+    GRID_STRIDE(i, n) out[i] = src[idx[i]];
+}
+
+// ---- merge-path unique + difference + merge ---------------------------------------------
+
+template <int W>
+struct Key {
+    u64 w[W];
+};
+
+template <int W>
+__device__ __forceinline__ bool key_le(const Key<W>& a, const Key<W>& b) {
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+        if (a.w[k] != b.w[k]) return a.w[k] < b.w[k];
+    return true;
+}
+template <int W>
+__device__ __forceinline__ bool key_eq(const Key<W>& a, const Key<W>& b) {
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+        if (a.w[k] != b.w[k]) return false;
+    return true;
+}
+
+template <int W>
+__device__ __forceinline__ Key<W> load_a(const Cols8& a, u32 arity, u64 row, u32 shift) {
+    Key<W> k;
+#pragma unroll
+    for (int w = 0; w < W; ++w) k.w[w] = pack_word(a, arity, w, row, shift);
+    return k;
+}
+template <int W>
+__device__ __forceinline__ Key<W> load_b(const Words4& b, u64 row) {
+    Key<W> k;
+#pragma unroll
+    for (int w = 0; w < W; ++w) k.w[w] = b.p[w][row];
+    return k;
+}
+
+template <int W>
+__device__ __forceinline__ void store_row(const OutCols8& out, u32 arity, u32 shift, u64 pos, const Key<W>& k) {
+    const u64 lo_mask = shift >= 64 ? ~u64(0) : ((u64(1) << shift) - 1);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const u32 c0 = 2 * w;
+        if (c0 + 1 < arity) {
+            out.p[c0][pos] = static_cast<u32>(k.w[w] >> shift);
+            out.p[c0 + 1][pos] = static_cast<u32>(k.w[w] & lo_mask);
+        } else if (c0 < arity) {
+            out.p[c0][pos] = static_cast<u32>(k.w[w]);
+        }
+    }
+}
+
+template <int W>
+struct MergeTraits {
+    static constexpr int kItems = W == 1 ? 8 : (W == 2 ? 4 : 2);
+    static constexpr int kBlock = 256;
+    static constexpr int kTile = kItems * kBlock;
+};
+
+template <int W>
+__device__ u64 merge_path_global(const Cols8& a, u32 arity, u32 shift, u64 n_a, const Words4& b, u64 n_b, u64 d) {
+    u64 lo = d > n_b ? d - n_b : 0;
+    u64 hi = d < n_a ? d : n_a;
+    while (lo < hi) {
+        const u64 mid = (lo + hi) >> 1;
+        if (key_le<W>(load_a<W>(a, arity, mid, shift), load_b<W>(b, d - 1 - mid))) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <int W>
+__global__ void __launch_bounds__(MergeTraits<W>::kBlock)
+    merge_kernel(Cols8 a, u64 n_a, Words4 b, u64 n_b, u32 arity, u32 shift, OutCols8 cout, OutCols8 dout,
+                 u64* __restrict__ status, u32 epoch, u32* __restrict__ tile_counter, u64* __restrict__ d_new) {
+    constexpr int ITEMS = MergeTraits<W>::kItems;
+    constexpr int BLOCK = MergeTraits<W>::kBlock;
+    constexpr int TILE = MergeTraits<W>::kTile;
+    __shared__ Key<W> s_keys[TILE];  // inputs: A part then B part; later C outputs
+    __shared__ Key<W> s_dout[TILE];
+    __shared__ u32 s_tile;
+    __shared__ u64 s_a0, s_a1, s_dups_before;
+    __shared__ Key<W> s_prev;
+    __shared__ int s_has_prev;
+    __shared__ u64 s_warp64[BLOCK / 32 + 1];
+
+    const u32 tid = threadIdx.x;
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 total = n_a + n_b;
+    const u64 d0 = u64(tile) * TILE;
+    const u64 d1 = min(d0 + TILE, total);
+    if (tid == 0) {
+        const u64 a0 = merge_path_global<W>(a, arity, shift, n_a, b, n_b, d0);
+        const u64 a1 = merge_path_global<W>(a, arity, shift, n_a, b, n_b, d1);
+        s_a0 = a0;
+        s_a1 = a1;
+        const u64 b0 = d0 - a0;
+        int has = 0;
+        Key<W> pv;
+        if (a0 > 0) {
+            pv = load_a<W>(a, arity, a0 - 1, shift);
+            has = 1;
+        }
+        if (b0 > 0) {
+            const Key<W> pb = load_b<W>(b, b0 - 1);
+            if (!has || key_le<W>(pv, pb)) pv = pb;
+            has = 1;
+        }
+        if (has) s_prev = pv;
+        s_has_prev = has;
+    }
+    __syncthreads();
+    const u64 a0 = s_a0, a1 = s_a1;
+    const u64 b0 = d0 - a0, b1 = d1 - a1;
+    const u32 na = static_cast<u32>(a1 - a0), nb = static_cast<u32>(b1 - b0);
+    Key<W>* sA = s_keys;
+    Key<W>* sB = s_keys + na;
+    for (u32 j = tid; j < na; j += BLOCK) sA[j] = load_a<W>(a, arity, a0 + j, shift);
+    for (u32 j = tid; j < nb; j += BLOCK) sB[j] = load_b<W>(b, b0 + j);
+    __syncthreads();
+
+    // Thread-level merge path inside the tile.
+    const u32 len = na + nb;
+    const u32 t0 = min(tid * ITEMS, len);
+    u32 lo = t0 > nb ? t0 - nb : 0, hi = min(t0, na);
+    while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (key_le<W>(sA[mid], sB[t0 - 1 - mid])) lo = mid + 1;
+        else hi = mid;
+    }
+    u32 ai = lo, bi = t0 - lo;
+    Key<W> prev;
+    bool has_prev;
+    if (t0 == 0) {
+        has_prev = s_has_prev != 0;
+        if (has_prev) prev = s_prev;
+    } else {
+        has_prev = true;
+        if (ai > 0 && bi > 0) prev = key_le<W>(sA[ai - 1], sB[bi - 1]) ? sB[bi - 1] : sA[ai - 1];
+        else if (ai > 0) prev = sA[ai - 1];
+        else prev = sB[bi - 1];
+    }
+    Key<W> item[ITEMS];
+    u32 valid = 0, from_b = 0, dup = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        if (t0 + k < len) {
+            const bool take_a = bi >= nb || (ai < na && key_le<W>(sA[ai], sB[bi]));
+            const Key<W> key = take_a ? sA[ai] : sB[bi];
+            if (take_a) ++ai;
+            else ++bi;
+            valid |= 1u << k;
+            if (!take_a) {
+                from_b |= 1u << k;
+                if (has_prev && key_eq<W>(key, prev)) dup |= 1u << k;
+            }
+            item[k] = key;
+            prev = key;
+            has_prev = true;
+        }
+    }
+    const u32 nondup = __popc(valid & ~dup);
+    const u32 nondup_b = __popc(from_b & ~dup);
+    // One block scan over both counts packed in a u64.
+    u64 agg;
+    const u64 excl = block_exclusive_scan<BLOCK>((u64(nondup_b) << 32) | nondup, s_warp64, &agg);
+    const u32 tile_nondup = static_cast<u32>(agg), tile_nondup_b = static_cast<u32>(agg >> 32);
+    const u64 tile_dups = u64(len) - tile_nondup;
+
+    if (tid < 32) {
+        u64 before = 0;
+        if (tile == 0) {
+            if (tid == 0) st_relaxed_u64(status, lb_pack(epoch, kLbFlagInclusive, tile_dups));
+        } else {
+            if (tid == 0) st_relaxed_u64(status + tile, lb_pack(epoch, kLbFlagAggregate, tile_dups));
+            before = lookback_warp(status, tile, epoch);
+            if (tid == 0) st_relaxed_u64(status + tile, lb_pack(epoch, kLbFlagInclusive, before + tile_dups));
+        }
+        if (tid == 0) s_dups_before = before;
+    }
+    __syncthreads();  // also: all reads of sA/sB done before reuse below
+    const u64 dups_before = s_dups_before;
+    u32 cpos = static_cast<u32>(excl);
+    u32 dpos = static_cast<u32>(excl >> 32);
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u32 bit = 1u << k;
+        if ((valid & bit) && !(dup & bit)) {
+            s_keys[cpos++] = item[k];
+            if (from_b & bit) s_dout[dpos++] = item[k];
+        }
+    }
+    __syncthreads();
+    const u64 c_base = d0 - dups_before;
+    const u64 d_base = b0 - dups_before;
+    for (u32 j = tid; j < tile_nondup; j += BLOCK) store_row<W>(cout, arity, shift, c_base + j, s_keys[j]);
+    for (u32 j = tid; j < tile_nondup_b; j += BLOCK) store_row<W>(dout, arity, shift, d_base + j, s_dout[j]);
+    if (tid == 0 && d1 == total) *d_new = d_base + tile_nondup_b;
+}
+
+// ---- fingerprint ------------------------------------------------------------------------
+
+__global__ void fingerprint_kernel(Cols8 c, u32 arity, u64 n, unsigned long long* out) {
+    unsigned long long acc = 0;
+    GRID_STRIDE(i, n) {
+        u64 h = 0x2545F4914F6CDD1Dull;
+        for (u32 j = 0; j < arity; ++j) h = mix64(h ^ c.p[j][i]);
+        acc += h;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane_id() == 0) atomicAdd(out, acc);
+}
+
+}  // namespace
+
+namespace {
+struct SelectRowsOp {
+    RowFilter pred;
+    u32* ids;
+    __device__ u64 value(u64 i) const { return pass_filters(pred.f, pred.n, i, 0) ? 1 : 0; }
+    __device__ void emit(u64 i, u64 p, u64 v) const {
+        if (v) ids[p] = static_cast<u32>(i);
+    }
+};
+}  // namespace
+
+// ---- host launchers -------------------------------------------------------------------------
+
+u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids) {
+    if (!n) return 0;
+    u64* d = c->d_scalars + 18;
+    tile_scan(c, SelectRowsOp{pred, ids}, n, d);
+    u64 k = 0;
+    c->read_scalars(d, &k, 1);
+    return k;
+}
+
+void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, const RowFilter& pred,
+                        u32* starts, u32* counts) {
+    if (!n) return;
+    probe_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(probe, n, idx.ht.slots.get(), idx.ht.mask,
+                                                            idx.ustart.get(), idx.ucount.get(), pred,
+                                                            starts, counts);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32* starts,
+                        const OutSpec& spec) {
+    if (!total) return;
+    const u64 tiles = ceil_div(total, kMatTile);
+    if (spec.n_filters)
+        materialize_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(offsets, m, total,
+                                                                                           starts, spec);
+    else
+        materialize_kernel<false><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(offsets, m, total,
+                                                                                            starts, spec);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void engine_project(Ctx* c, u64 n, const OutSpec& spec) {
+    if (!n) return;
+    const u64 tiles = ceil_div(n, kMatTile);
+    if (spec.n_filters)
+        project_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(n, spec);
+    else
+        project_kernel<false><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(n, spec);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx) {
+    idx.n_unique = 0;
+    if (n == 0) return;
+    DBuf<u32> uk(c, n), us(c, n);
+    u64* d = c->d_scalars + 16;
+    tile_scan(c, RunsOp{sorted_keys, uk.get(), us.get()}, n, d);
+    c->read_scalars(d, &idx.n_unique, 1);
+    const u64 nu = idx.n_unique;
+    idx.ukeys = DBuf<u32>(c, nu);
+    idx.ustart = DBuf<u32>(c, nu);
+    idx.ucount = DBuf<u32>(c, nu);
+    FV_CUDA(cudaMemcpyAsync(idx.ukeys.get(), uk.get(), 4 * nu, cudaMemcpyDeviceToDevice, c->stream));
+    FV_CUDA(cudaMemcpyAsync(idx.ustart.get(), us.get(), 4 * nu, cudaMemcpyDeviceToDevice, c->stream));
+    runs_count_kernel<<<grid_for(nu), 256, 0, c->stream>>>(idx.ustart.get(), idx.ucount.get(), nu, n);
+    u64 cap = 64;
+    while (cap < 2 * nu) cap <<= 1;
+    idx.ht.slots = DBuf<u64>(c, cap);
+    idx.ht.mask = static_cast<u32>(cap - 1);
+    FV_CUDA(cudaMemsetAsync(idx.ht.slots.get(), 0xff, 8 * cap, c->stream));
+    hash_build_kernel<<<grid_for(nu), 256, 0, c->stream>>>(
+        idx.ukeys.get(), nu, reinterpret_cast<unsigned long long*>(idx.ht.slots.get()), idx.ht.mask);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch(2);
+}
+
+static Cols8 cols8(const std::vector<const u32*>& cols) {
+    Cols8 c{};
+    for (size_t j = 0; j < cols.size() && j < FV_MAX_ARITY; ++j) c.p[j] = cols[j];
+    return c;
+}
+
+void engine_pack_keys(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 shift, u64* const* words) {
+    if (!n) return;
+    const u32 arity = static_cast<u32>(cols.size());
+    Words4 w{};
+    for (u32 k = 0; k < (arity + 1) / 2; ++k) w.p[k] = words[k];
+    pack_kernel<<<grid_for(n), 256, 0, c->stream>>>(cols8(cols), arity, n, shift, w);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+template <int W>
+static void merge_launch(Ctx* c, const Cols8& a, u64 n_a, const Words4& b, u64 n_b, u32 arity, u32 shift,
+                         const OutCols8& co, const OutCols8& dout, u64* d_new) {
+    const u64 tiles = ceil_div(n_a + n_b, MergeTraits<W>::kTile);
+    u32* counter = nullptr;
+    const u32 epoch = c->lookback_epoch(tiles, &counter);
+    merge_kernel<W><<<static_cast<unsigned>(tiles), MergeTraits<W>::kBlock, 0, c->stream>>>(
+        a, n_a, b, n_b, arity, shift, co, dout, c->lb.status, epoch, counter, d_new);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void engine_merge(Ctx* c, const std::vector<const u32*>& a_cols, u64 n_a, u64* const* b_words, u64 n_b,
+                  u32 arity, u32 shift, const std::vector<u32*>& c_cols, const std::vector<u32*>& d_cols,
+                  u64* d_new) {
+    if (n_a + n_b == 0 || n_b == 0) {
+        // Nothing new: C = A (caller copies), D empty.
+        FV_CUDA(cudaMemsetAsync(d_new, 0, sizeof(u64), c->stream));
+        if (n_a) {
+            for (u32 j = 0; j < arity; ++j)
+                FV_CUDA(cudaMemcpyAsync(c_cols[j], a_cols[j], 4 * n_a, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        return;
+    }
+    const Cols8 a = cols8(a_cols);
+    Words4 b{};
+    const u32 W = (arity + 1) / 2;
+    for (u32 k = 0; k < W; ++k) b.p[k] = b_words[k];
+    OutCols8 co{}, dout{};
+    for (u32 j = 0; j < arity; ++j) {
+        co.p[j] = c_cols[j];
+        dout.p[j] = d_cols[j];
+    }
+    switch (W) {
+        case 1: merge_launch<1>(c, a, n_a, b, n_b, arity, shift, co, dout, d_new); break;
+        case 2: merge_launch<2>(c, a, n_a, b, n_b, arity, shift, co, dout, d_new); break;
+        case 3: merge_launch<3>(c, a, n_a, b, n_b, arity, shift, co, dout, d_new); break;
+        case 4: merge_launch<4>(c, a, n_a, b, n_b, arity, shift, co, dout, d_new); break;
+        default: fail(FV_ERR_ARITY, "arity exceeds FV_MAX_ARITY");
+    }
+}
+
+u64 engine_fingerprint(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 arity) {
+    u64* d = c->d_scalars + 17;
+    FV_CUDA(cudaMemsetAsync(d, 0, sizeof(u64), c->stream));
+    if (n) {
+        fingerprint_kernel<<<grid_for(n), 256, 0, c->stream>>>(cols8(cols), arity, n,
+                                                                reinterpret_cast<unsigned long long*>(d));
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+    }
+    u64 h = 0;
+    c->read_scalars(d, &h, 1);
+    return h;
+}
+
+void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift) {
+    if (n <= 1) return;
+    const u32 W = static_cast<u32>(words.size());
+    auto word_bits = [&](u32 w) -> u32 {
+        return (2 * w + 1 < arity) ? 2 * shift : shift;  // (hi << shift) | lo
+    };
+    if (W == 1) {
+        const u32 bits = arity >= 2 ? 2 * shift : shift;
+        DBuf<u64> alt(c, n);
+        if (radix_sort_keys_u64(c, words[0].get(), alt.get(), n, 0, bits > 64 ? 64 : bits)) words[0].swap(alt);
+        return;
+    }
+    DBuf<u32> perm(c, n), perm_alt(c, n);
+    DBuf<u64> tmp(c, n), tmp_alt(c, n);
+    iota_u32(c, perm.get(), n);
+    for (int w = static_cast<int>(W) - 1; w >= 0; --w) {
+        gather_u64_kernel<<<grid_for(n), 256, 0, c->stream>>>(words[w].get(), perm.get(), tmp.get(), n);
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+        u32 bits = word_bits(static_cast<u32>(w));
+        if (bits > 64) bits = 64;
+        if (radix_sort_pairs_u64(c, tmp.get(), tmp_alt.get(), perm.get(), perm_alt.get(), n, 0, bits))
+            perm.swap(perm_alt);
+    }
+    for (u32 w = 0; w < W; ++w) {
+        gather_u64_kernel<<<grid_for(n), 256, 0, c->stream>>>(words[w].get(), perm.get(), tmp.get(), n);
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+        words[w].swap(tmp);
+    }
+}
+
+}  // namespace fv

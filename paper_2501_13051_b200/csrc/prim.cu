@@ -1,0 +1,66 @@
+// Small device helpers shared by the operator kernels.
+#include "prim.cuh"
+
+namespace fv {
+
+namespace {
+
+__global__ void iota_kernel(u32* out, u64 n) {
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        out[i] = static_cast<u32>(i);
+}
+
+__global__ void gather_kernel(const u32* __restrict__ src, const u32* __restrict__ idx,
+                              u32* __restrict__ out, u64 n) {
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        out[i] = src[idx[i]];
+}
+
+__global__ void reduce_max_kernel(const u32* __restrict__ in, u64 n, unsigned long long* out) {
+    u32 m = 0;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        m = max(m, in[i]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane_id() == 0) atomicMax(out, static_cast<unsigned long long>(m));
+}
+
+unsigned grid_for(u64 n, int block = 256) {
+    const u64 want = ceil_div(n, block);
+    const u64 cap = u64(kNumSMs) * 16;
+    return static_cast<unsigned>(want == 0 ? 1 : (want < cap ? want : cap));
+}
+
+}  // namespace
+
+void exclusive_scan_counts(Ctx* c, const u32* counts, u64* offsets, u64 n) {
+    if (n == 0) {
+        FV_CUDA(cudaMemsetAsync(offsets, 0, sizeof(u64), c->stream));
+        return;
+    }
+    tile_scan(c, ScanCountsOp{counts, offsets, n}, n, nullptr);
+}
+
+void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out) {
+    FV_CUDA(cudaMemsetAsync(d_out, 0, sizeof(u64), c->stream));
+    if (n == 0) return;
+    reduce_max_kernel<<<grid_for(n), 256, 0, c->stream>>>(in, n,
+                                                         reinterpret_cast<unsigned long long*>(d_out));
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void iota_u32(Ctx* c, u32* out, u64 n) {
+    if (!n) return;
+    iota_kernel<<<grid_for(n), 256, 0, c->stream>>>(out, n);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void gather_u32(Ctx* c, const u32* src, const u32* idx, u32* out, u64 n) {
+    if (!n) return;
+    gather_kernel<<<grid_for(n), 256, 0, c->stream>>>(src, idx, out, n);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+}  // namespace fv

@@ -1,0 +1,154 @@
+// Single-pass scan / stream-compaction primitive for sm_100a.
+//
+// The reference's order-preserving compactions (compact_positions,
+// P/src/kernels.cpp:15-34: count per fixed block -> sequential scan ->
+// write) and its serial exclusive scan (join_offsets, :94-102) become one
+// kernel: each CTA reduces a tile, publishes its aggregate, and resolves its
+// global prefix by decoupled look-back over its predecessors, so the input
+// is read once and the output written once (HBM roofline: n*(in+out) bytes).
+#pragma once
+
+#include "fv_common.cuh"
+
+namespace fv {
+
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+// Block-wide exclusive scan of one u64 per thread; returns the thread's
+// exclusive prefix and writes the block total to *total (all threads).
+template <int BLOCK>
+__device__ __forceinline__ u64 block_exclusive_scan(u64 v, u64* s_warp, u64* total) {
+    constexpr int W = BLOCK / 32;
+    const u32 lane = lane_id(), warp = threadIdx.x >> 5;
+    u64 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<u32>(o)) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        u64 w = lane < W ? s_warp[lane] : 0;
+        u64 incl = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= static_cast<u32>(o)) incl += y;
+        }
+        if (lane < W) s_warp[lane] = incl - w;
+        if (lane == W - 1) s_warp[W] = incl;
+    }
+    __syncthreads();
+    u64 excl = s_warp[warp] + x - v;
+    *total = s_warp[W];
+    __syncthreads();
+    return excl;
+}
+
+// Op contract:
+//   __device__ u64  value(u64 i) const;            // item weight (0/1 for select)
+//   __device__ void emit(u64 i, u64 prefix, u64 v) const;  // called for every i < n
+// The last tile stores the grand total to *d_total.
+template <int BLOCK, int ITEMS, class Op>
+__global__ void __launch_bounds__(BLOCK) tile_scan_kernel(Op op, u64 n, u64* status, u32 epoch,
+                                                          u32* tile_counter, u64* d_total) {
+    __shared__ u32 s_tile;
+    __shared__ u64 s_warp[BLOCK / 32 + 1];
+    __shared__ u64 s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 base = u64(tile) * (BLOCK * ITEMS) + u64(threadIdx.x) * ITEMS;
+
+    u64 v[ITEMS];
+    u64 sum = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 i = base + k;
+        v[k] = i < n ? op.value(i) : 0;
+        sum += v[k];
+    }
+    u64 agg;
+    const u64 excl = block_exclusive_scan<BLOCK>(sum, s_warp, &agg);
+
+    if (threadIdx.x < 32) {
+        u64 prefix = 0;
+        if (tile == 0) {
+            if (threadIdx.x == 0) st_relaxed_u64(status, lb_pack(epoch, kLbFlagInclusive, agg));
+        } else {
+            if (threadIdx.x == 0) st_relaxed_u64(status + tile, lb_pack(epoch, kLbFlagAggregate, agg));
+            prefix = lookback_warp(status, tile, epoch);
+            if (threadIdx.x == 0)
+                st_relaxed_u64(status + tile, lb_pack(epoch, kLbFlagInclusive, prefix + agg));
+        }
+        if (threadIdx.x == 0) {
+            s_prefix = prefix;
+            const u64 tiles = ceil_div(n, BLOCK * ITEMS);
+            if (tile == tiles - 1 && d_total) *d_total = prefix + agg;
+        }
+    }
+    __syncthreads();
+    u64 run = s_prefix + excl;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 i = base + k;
+        if (i < n) op.emit(i, run, v[k]);
+        run += v[k];
+    }
+}
+
+// Launch helper. d_total may be null. n == 0 writes *d_total = 0.
+template <class Op>
+void tile_scan(Ctx* c, const Op& op, u64 n, u64* d_total) {
+    if (n == 0) {
+        if (d_total) FV_CUDA(cudaMemsetAsync(d_total, 0, sizeof(u64), c->stream));
+        return;
+    }
+    const u64 tiles = ceil_div(n, kScanTile);
+    u32* counter = nullptr;
+    const u32 epoch = c->lookback_epoch(tiles, &counter);
+    tile_scan_kernel<kScanBlock, kScanItems, Op>
+        <<<static_cast<unsigned>(tiles), kScanBlock, 0, c->stream>>>(op, n, c->lb.status, epoch,
+                                                                      counter, d_total);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+// ---- common ops ------------------------------------------------------------
+
+// Exclusive scan of u32 counts into u64 offsets[n + 1] (offsets[n] = total).
+struct ScanCountsOp {
+    const u32* counts;
+    u64* offsets;
+    u64 n;
+    __device__ u64 value(u64 i) const { return counts[i]; }
+    __device__ void emit(u64 i, u64 prefix, u64 v) const {
+        offsets[i] = prefix;
+        if (i == n - 1) offsets[n] = prefix + v;
+    }
+};
+
+// Order-preserving compaction of positions i with flag[i] != 0 into ids.
+struct SelectFlagsOp {
+    const u8* flags;
+    u8 want;  // keep when (flags[i] != 0) == want
+    u32* out;
+    __device__ u64 value(u64 i) const { return (flags[i] != 0) == (want != 0) ? 1 : 0; }
+    __device__ void emit(u64 i, u64 prefix, u64 v) const {
+        if (v) out[prefix] = static_cast<u32>(i);
+    }
+};
+
+void exclusive_scan_counts(Ctx* c, const u32* counts, u64* offsets, u64 n);
+
+// Device reductions returning to a device scalar.
+void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out);
+
+// Fill / iota helpers.
+void iota_u32(Ctx* c, u32* out, u64 n);
+void gather_u32(Ctx* c, const u32* src, const u32* idx, u32* out, u64 n);
+
+}  // namespace fv

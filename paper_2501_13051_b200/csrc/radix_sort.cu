@@ -1,0 +1,302 @@
+// Onesweep LSD radix sort for sm_100a (keys u32/u64, optional u32 payload).
+//
+// Replaces the comparator sorts of the reference:
+//   build_index   (P/src/column.cpp:25-30): std::sort of ids by (value, id)
+//   dedup_rows    (P/src/relation.cpp:71-80): sort of ids by (row, id)
+// A stable LSD sort of (key, id) pairs started from iota yields exactly the
+// reference's strict (value, id) order, so sorted_idx is bit-identical.
+//
+// Per sort: one histogram kernel computes all digit histograms in a single
+// read of the keys (warp-aggregated shared atomics via __match_any_sync), a
+// tiny kernel turns them into per-digit global bases, then one onesweep
+// kernel per 8-bit digit reads each key once and writes it once:
+//   - tile of BLOCK*ITEMS keys in a warp-striped arrangement (coalesced
+//     128-bit-friendly loads; lane order == input order so ranking is stable)
+//   - per-warp digit ranks with __match_any_sync, per-warp shared histograms
+//   - decoupled look-back across tiles per digit (status words carry an epoch
+//     so no clearing between passes)
+//   - shared-memory exchange so global stores are runs of one digit.
+// HBM roofline per pass: n * 2 * (sizeof(K) + sizeof(payload)) bytes.
+#include "radix_sort.h"
+
+namespace fv {
+
+namespace {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortBlock = 256;
+constexpr int kSortWarps = kSortBlock / 32;
+
+template <typename K>
+struct SortTraits;
+template <>
+struct SortTraits<u32> {
+    static constexpr int kItems = 16;
+};
+template <>
+struct SortTraits<u64> {
+    static constexpr int kItems = 12;
+};
+
+template <typename K>
+__device__ __forceinline__ u32 digit_of(K key, u32 shift, u32 mask) {
+    return static_cast<u32>(key >> shift) & mask;
+}
+
+// ---- histogram over all passes -------------------------------------------
+
+template <typename K>
+__global__ void __launch_bounds__(256) radix_hist_kernel(const K* __restrict__ keys, u64 n,
+                                                         u32 begin_bit, u32 end_bit, u32 npass,
+                                                         unsigned long long* __restrict__ hist) {
+    __shared__ u32 s_hist[8][kRadix];
+    for (u32 i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
+    const u32 lane = lane_id();
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    // Whole warps iterate together so __match_any_sync sees full masks.
+    const u64 n_round = ceil_div(n, 32) * 32;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        const bool valid = i < n;
+        const K key = valid ? keys[i] : K(0);
+        for (u32 p = 0; p < npass; ++p) {
+            const u32 shift = begin_bit + p * kRadixBits;
+            const u32 bits = min(u32(kRadixBits), end_bit - shift);
+            const u32 d = valid ? digit_of(key, shift, (1u << bits) - 1) : 0xffffu;
+            const u32 peers = __match_any_sync(0xffffffffu, d);
+            if (valid && lane == static_cast<u32>(__ffs(peers) - 1))
+                atomicAdd(&s_hist[p][d], static_cast<u32>(__popc(peers)));
+        }
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < npass * kRadix; i += blockDim.x) {
+        const u32 v = (&s_hist[0][0])[i];
+        if (v) atomicAdd(hist + i, static_cast<unsigned long long>(v));
+    }
+}
+
+// hist[p][d] -> exclusive bases[p][d]; trivial[p] = 1 when one digit holds
+// every key (the pass would be the identity permutation and is skipped).
+__global__ void radix_bins_kernel(const unsigned long long* __restrict__ hist, u64* __restrict__ bins,
+                                  u64 n, u64* __restrict__ trivial) {
+    __shared__ u64 s_warp[kSortWarps + 1];
+    const u32 p = blockIdx.x;
+    const u64 v = hist[p * kRadix + threadIdx.x];
+    // inline block scan (256 threads)
+    const u32 lane = lane_id(), warp = threadIdx.x >> 5;
+    u64 x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        u64 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<u32>(o)) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 run = 0;
+        for (int w = 0; w < kSortWarps; ++w) {
+            u64 t = s_warp[w];
+            s_warp[w] = run;
+            run += t;
+        }
+        s_warp[kSortWarps] = run;
+    }
+    __syncthreads();
+    bins[p * kRadix + threadIdx.x] = s_warp[warp] + x - v;
+    const int is_trivial = __syncthreads_or(v == n);
+    if (threadIdx.x == 0) trivial[p] = is_trivial ? 1 : 0;
+}
+
+// ---- onesweep pass ------------------------------------------------------------
+
+template <typename K, bool HAS_VAL>
+__global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
+    const K* __restrict__ keys_in, K* __restrict__ keys_out, const u32* __restrict__ vals_in,
+    u32* __restrict__ vals_out, u64 n, u32 shift, u32 mask, const u64* __restrict__ bins,
+    u64* __restrict__ status, u32 epoch, u32* __restrict__ tile_counter) {
+    constexpr int ITEMS = SortTraits<K>::kItems;
+    constexpr int TILE = kSortBlock * ITEMS;
+    constexpr int WARP_TILE = 32 * ITEMS;
+
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    K* s_keys = reinterpret_cast<K*>(s_raw);
+    u32* s_vals = reinterpret_cast<u32*>(s_raw + sizeof(K) * TILE);
+    __shared__ u32 s_whist[kSortWarps][kRadix];
+    __shared__ u32 s_block_excl[kRadix];
+    __shared__ u64 s_global[kRadix];
+    __shared__ u32 s_tile;
+    __shared__ u32 s_warp_sums[kSortWarps];
+
+    const u32 tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    for (u32 i = tid; i < kSortWarps * kRadix; i += kSortBlock) (&s_whist[0][0])[i] = 0;
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 tile_base = u64(tile) * TILE;
+    const u64 warp_base = tile_base + u64(warp) * WARP_TILE;
+
+    K key[ITEMS];
+    u32 val[ITEMS];
+    u32 rank[ITEMS];
+    u32 dig[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 i = warp_base + u64(k) * 32 + lane;
+        const bool valid = i < n;
+        key[k] = valid ? keys_in[i] : K(0);
+        if (HAS_VAL) val[k] = valid ? vals_in[i] : 0u;
+        dig[k] = valid ? digit_of(key[k], shift, mask) : 0xffffu;
+    }
+    // Warp-level stable ranking, item-major (k outer, lane inner) = input order.
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u32 d = dig[k];
+        const u32 peers = __match_any_sync(0xffffffffu, d);
+        const u32 leader = __ffs(peers) - 1;
+        u32 b = 0;
+        if (d != 0xffffu && lane == leader) {
+            b = s_whist[warp][d];
+            s_whist[warp][d] = b + __popc(peers);
+        }
+        b = __shfl_sync(0xffffffffu, b, leader);
+        rank[k] = b + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+
+    // Thread d owns digit d: exclusive scan across warps, tile count.
+    const u32 d = tid;
+    u32 count = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+        const u32 t = s_whist[w][d];
+        s_whist[w][d] = count;
+        count += t;
+    }
+    // Publish early so successors are not held up by our own look-back.
+    u64* my_status = status + u64(tile) * kRadix + d;
+    if (tile == 0) {
+        st_relaxed_u64(my_status, lb_pack(epoch, kLbFlagInclusive, count));
+    } else {
+        st_relaxed_u64(my_status, lb_pack(epoch, kLbFlagAggregate, count));
+    }
+    // Block exclusive scan of counts across digits (for the smem exchange).
+    {
+        u32 x = count;
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= static_cast<u32>(o)) x += y;
+        }
+        if (lane == 31) s_warp_sums[warp] = x;
+        __syncthreads();
+        if (tid == 0) {
+            u32 run = 0;
+            for (int w = 0; w < kSortWarps; ++w) {
+                u32 t = s_warp_sums[w];
+                s_warp_sums[w] = run;
+                run += t;
+            }
+        }
+        __syncthreads();
+        s_block_excl[d] = s_warp_sums[warp] + x - count;
+    }
+    u64 excl = 0;
+    if (tile > 0) {
+        excl = lookback_thread(status, tile, kRadix, d, epoch);
+        st_relaxed_u64(my_status, lb_pack(epoch, kLbFlagInclusive, excl + count));
+    }
+    s_global[d] = bins[d] + excl;
+    __syncthreads();
+
+    // Exchange into digit order within the tile.
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        if (dig[k] != 0xffffu) {
+            const u32 lp = s_block_excl[dig[k]] + s_whist[warp][dig[k]] + rank[k];
+            s_keys[lp] = key[k];
+            if (HAS_VAL) s_vals[lp] = val[k];
+        }
+    }
+    __syncthreads();
+    const u64 remaining = n - tile_base;
+    const u32 valid_count = remaining < u64(TILE) ? static_cast<u32>(remaining) : u32(TILE);
+    for (u32 i = tid; i < valid_count; i += kSortBlock) {
+        const K kk = s_keys[i];
+        const u32 dd = digit_of(kk, shift, mask);
+        const u64 pos = s_global[dd] + (i - s_block_excl[dd]);
+        keys_out[pos] = kk;
+        if (HAS_VAL) vals_out[pos] = s_vals[i];
+    }
+}
+
+template <typename K, bool HAS_VAL>
+void onesweep_pass(Ctx* c, const K* kin, K* kout, const u32* vin, u32* vout, u64 n, u32 shift,
+                   u32 mask, const u64* bins) {
+    constexpr int TILE = kSortBlock * SortTraits<K>::kItems;
+    const u64 tiles = ceil_div(n, TILE);
+    u32* counter = nullptr;
+    const u32 epoch = c->lookback_epoch(tiles * kRadix, &counter);
+    const size_t smem = sizeof(K) * TILE + (HAS_VAL ? sizeof(u32) * TILE : 0);
+    onesweep_kernel<K, HAS_VAL><<<static_cast<unsigned>(tiles), kSortBlock, smem, c->stream>>>(
+        kin, kout, vin, vout, n, shift, mask, bins, c->lb.status, epoch, counter);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+template <typename K, bool HAS_VAL>
+bool radix_sort_impl(Ctx* c, K* keys, K* keys_alt, u32* vals, u32* vals_alt, u64 n,
+                     u32 begin_bit, u32 end_bit) {
+    if (n <= 1 || end_bit <= begin_bit) return false;
+    const u32 npass = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
+    // hist (u64 x npass x 256) | bins (same) | trivial flags (npass)
+    DBuf<u64> scratch(c, u64(npass) * kRadix * 2 + 8);
+    unsigned long long* hist = reinterpret_cast<unsigned long long*>(scratch.get());
+    u64* bins = scratch.get() + u64(npass) * kRadix;
+    u64* trivial = bins + u64(npass) * kRadix;
+    FV_CUDA(cudaMemsetAsync(hist, 0, sizeof(u64) * npass * kRadix, c->stream));
+    {
+        const u64 want = ceil_div(n, 256 * 8);
+        const unsigned grid = static_cast<unsigned>(want < u64(kNumSMs) * 8 ? (want ? want : 1)
+                                                                             : u64(kNumSMs) * 8);
+        radix_hist_kernel<K><<<grid, 256, 0, c->stream>>>(keys, n, begin_bit, end_bit, npass, hist);
+        FV_CUDA(cudaGetLastError());
+        radix_bins_kernel<<<npass, kRadix, 0, c->stream>>>(hist, bins, n, trivial);
+        FV_CUDA(cudaGetLastError());
+        c->count_launch(2);
+    }
+    u64 triv[8] = {0};
+    c->read_scalars(trivial, triv, static_cast<int>(npass));
+
+    bool in_alt = false;
+    for (u32 p = 0; p < npass; ++p) {
+        if (triv[p]) continue;
+        const u32 shift = begin_bit + p * kRadixBits;
+        const u32 bits = (end_bit - shift) < u32(kRadixBits) ? (end_bit - shift) : u32(kRadixBits);
+        const u32 mask = (1u << bits) - 1;
+        K* kin = in_alt ? keys_alt : keys;
+        K* kout = in_alt ? keys : keys_alt;
+        u32* vin = in_alt ? vals_alt : vals;
+        u32* vout = in_alt ? vals : vals_alt;
+        onesweep_pass<K, HAS_VAL>(c, kin, kout, vin, vout, n, shift, mask, bins + u64(p) * kRadix);
+        in_alt = !in_alt;
+    }
+    return in_alt;
+}
+
+}  // namespace
+
+bool radix_sort_pairs_u32(Ctx* c, u32* keys, u32* keys_alt, u32* vals, u32* vals_alt, u64 n,
+                          u32 begin_bit, u32 end_bit) {
+    return radix_sort_impl<u32, true>(c, keys, keys_alt, vals, vals_alt, n, begin_bit, end_bit);
+}
+bool radix_sort_keys_u32(Ctx* c, u32* keys, u32* keys_alt, u64 n, u32 begin_bit, u32 end_bit) {
+    return radix_sort_impl<u32, false>(c, keys, keys_alt, nullptr, nullptr, n, begin_bit, end_bit);
+}
+bool radix_sort_pairs_u64(Ctx* c, u64* keys, u64* keys_alt, u32* vals, u32* vals_alt, u64 n,
+                          u32 begin_bit, u32 end_bit) {
+    return radix_sort_impl<u64, true>(c, keys, keys_alt, vals, vals_alt, n, begin_bit, end_bit);
+}
+bool radix_sort_keys_u64(Ctx* c, u64* keys, u64* keys_alt, u64 n, u32 begin_bit, u32 end_bit) {
+    return radix_sort_impl<u64, false>(c, keys, keys_alt, nullptr, nullptr, n, begin_bit, end_bit);
+}
+
+}  // namespace fv
