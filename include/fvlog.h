@@ -71,6 +71,14 @@ const char* fv_last_error(const fv_ctx* ctx);
 fv_status fv_ctx_synchronize(fv_ctx* ctx);
 /* Number of kernels this context has launched so far (profiling evidence). */
 uint64_t fv_ctx_kernel_launches(const fv_ctx* ctx);
+/* Per-kernel-class timing with CUDA events recorded on the context stream
+ * around every launch (enable = 1 clears previous entries). Each entry:
+ * launches, summed device milliseconds, summed algorithmic bytes (inputs
+ * read once + outputs written once). */
+fv_status fv_ctx_profile(fv_ctx* ctx, int enable);
+uint32_t fv_ctx_profile_count(const fv_ctx* ctx);
+fv_status fv_ctx_profile_entry(const fv_ctx* ctx, uint32_t i, const char** name, uint64_t* launches,
+                               double* ms, double* bytes);
 /* Process-wide count of values materialized by gathers
  * (P/src/column.cpp:10-15 gather_volume / reset_gather_volume). */
 uint64_t fv_gather_volume(void);
@@ -281,6 +289,14 @@ fv_status fv_evaluate(fv_ctx* ctx, const fv_relation_decl* decls, uint32_t n_dec
 /* evaluate a parsed program: program facts plus the given blocks. */
 fv_status fv_evaluate_program(fv_ctx* ctx, const fv_program* p, const fv_facts* facts,
                               uint32_t n_facts, fv_state** out);
+/* EDB resident in HBM: upload once (unsorted, duplicates allowed; seed
+ * dedups), evaluate many times without host->device traffic. */
+typedef struct fv_edb fv_edb;
+fv_status fv_edb_upload(fv_ctx* ctx, const fv_relation_decl* decls, uint32_t n_decls,
+                        const fv_facts* facts, uint32_t n_facts, fv_edb** out);
+void fv_edb_free(fv_edb* e);
+fv_status fv_evaluate_program_edb(fv_ctx* ctx, const fv_program* p, const fv_edb* edb,
+                                  fv_state** out);
 void fv_state_free(fv_state* s);
 /* EvaluationState::iterations (includes the final empty iteration). */
 uint64_t fv_state_iterations(const fv_state* s);

@@ -100,6 +100,35 @@ fv_status fv_ctx_synchronize(fv_ctx* ctx) {
 }
 
 uint64_t fv_ctx_kernel_launches(const fv_ctx* ctx) { return ctx ? ctx->c->launches : 0; }
+
+fv_status fv_ctx_profile(fv_ctx* ctx, int enable) {
+    FV_API_BEGIN(ctx)
+    FV_REQUIRE(ctx, FV_ERR_INVALID, "fv_ctx_profile: null ctx");
+    ctx->c->sync();
+    if (enable) ctx->c->prof_agg.clear();
+    ctx->c->prof = enable != 0;
+    FV_API_END
+}
+
+uint32_t fv_ctx_profile_count(const fv_ctx* ctx) {
+    if (!ctx) return 0;
+    ctx->c->sync();
+    return static_cast<uint32_t>(ctx->c->prof_agg.size());
+}
+
+fv_status fv_ctx_profile_entry(const fv_ctx* ctx, uint32_t i, const char** name, uint64_t* launches, double* ms,
+                               double* bytes) {
+    FV_API_BEGIN(const_cast<fv_ctx*>(ctx))
+    FV_REQUIRE(ctx, FV_ERR_INVALID, "fv_ctx_profile_entry: null ctx");
+    ctx->c->sync();
+    if (i >= ctx->c->prof_agg.size()) fv::fail(FV_ERR_RANGE, "profile entry out of range");
+    const auto& [n, a] = ctx->c->prof_agg[i];
+    if (name) *name = n.c_str();
+    if (launches) *launches = a.launches;
+    if (ms) *ms = a.ms;
+    if (bytes) *bytes = a.bytes;
+    FV_API_END
+}
 uint64_t fv_gather_volume(void) { return fv::gather_volume(); }
 void fv_reset_gather_volume(void) { fv::reset_gather_volume(); }
 

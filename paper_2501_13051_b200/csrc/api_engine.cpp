@@ -30,6 +30,11 @@ struct fv_program {
     std::vector<std::unique_ptr<PlanPod>> pods;
 };
 
+struct fv_edb {
+    fv_ctx* ctx = nullptr;
+    fv::DeviceEdb edb;
+};
+
 struct fv_state {
     fv_ctx* ctx = nullptr;
     std::unique_ptr<fv::EvalState> st;
@@ -294,6 +299,56 @@ fv_status fv_evaluate_program(fv_ctx* ctx, const fv_program* p, const fv_facts* 
     }
     for (auto& b : blocks_from(facts, n_facts)) blocks.push_back(std::move(b));
     *out = wrap_state(ctx, fv::evaluate(ctx->c, fv::fe::declarations(mp->prog), mp->plans, blocks));
+    FV_API_END
+}
+
+fv_status fv_edb_upload(fv_ctx* ctx, const fv_relation_decl* decls, uint32_t n_decls, const fv_facts* facts,
+                        uint32_t n_facts, fv_edb** out) {
+    FV_API_BEGIN(ctx)
+    FV_REQUIRE(ctx && out && (decls || !n_decls) && (facts || !n_facts), FV_ERR_INVALID, "fv_edb_upload: null argument");
+    std::vector<fv::RelationDecl> d;
+    for (uint32_t i = 0; i < n_decls; ++i) d.push_back({decls[i].name, decls[i].arity});
+    auto* e = new fv_edb();
+    e->ctx = ctx;
+    e->edb = fv::upload_facts(ctx->c, d, blocks_from(facts, n_facts));
+    ctx->c->sync();
+    *out = e;
+    FV_API_END
+}
+
+void fv_edb_free(fv_edb* e) {
+    if (!e) return;
+    e->ctx->c->activate();
+    delete e;
+}
+
+fv_status fv_evaluate_program_edb(fv_ctx* ctx, const fv_program* p, const fv_edb* edb, fv_state** out) {
+    FV_API_BEGIN(ctx)
+    FV_REQUIRE(ctx && p && edb && out, FV_ERR_INVALID, "fv_evaluate_program_edb: null argument");
+    auto* mp = const_cast<fv_program*>(p);
+    ensure_compiled(mp);
+    auto decls = fv::fe::declarations(mp->prog);
+    // Program-text facts are tiny; upload them next to the resident EDB.
+    auto pf = fv::fe::program_facts(mp->prog);
+    std::vector<std::vector<u32>> storage;
+    std::vector<fv::FactsBlock> blocks;
+    std::map<std::string, u32> arity;
+    for (auto& r : mp->prog.relations) arity[r.name] = r.arity;
+    for (auto& [rel, rows] : pf) {
+        const u32 a = arity[rel];
+        const u64 n = rows.size() / a;
+        fv::FactsBlock b{rel, a, n, {}};
+        for (u32 j = 0; j < a; ++j) {
+            storage.emplace_back(n);
+            for (u64 i = 0; i < n; ++i) storage.back()[i] = rows[i * a + j];
+        }
+        blocks.push_back(std::move(b));
+    }
+    size_t si = 0;
+    for (auto& b : blocks)
+        for (u32 j = 0; j < b.arity; ++j) b.cols.push_back(storage[si++].data());
+    fv::DeviceEdb text_edb = fv::upload_facts(ctx->c, decls, blocks);
+    *out = wrap_state(ctx, fv::evaluate_device(ctx->c, decls, mp->plans, {&text_edb, &edb->edb}));
     FV_API_END
 }
 

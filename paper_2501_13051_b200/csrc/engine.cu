@@ -294,6 +294,7 @@ public:
         engine_merge(c_, r.full.ptrs(), r.full.n, bw.data(), cand.n, arity, st_.key_shift, cc, dc, d_new);
         u64 nd = 0;
         c_->read_scalars(d_new, &nd, 1);
+        c_->prof_add_bytes("merge_dedup", 8.0 * double(nd) * arity);
         C.n = r.full.n + nd;
         D.n = nd;
         r.full = std::move(C);
@@ -348,8 +349,50 @@ void check_plans(const std::vector<RelationDecl>& decls, const std::vector<Plan>
     }
 }
 
+DeviceEdb upload_facts(Ctx* c, const std::vector<RelationDecl>& decls, const std::vector<FactsBlock>& facts) {
+    std::map<std::string, u32> arity;
+    for (auto& d : decls) arity[d.name] = d.arity;
+    std::map<std::string, std::vector<const FactsBlock*>> by_rel;
+    for (auto& f : facts) {
+        auto it = arity.find(f.relation);
+        if (it == arity.end()) continue;  // facts for undeclared relations are ignored
+        if (f.arity != it->second) fail(FV_ERR_ARITY, "facts for '" + f.relation + "' have the wrong arity");
+        by_rel[f.relation].push_back(&f);
+    }
+    DeviceEdb edb;
+    for (auto& [name, blocks] : by_rel) {
+        u64 n = 0;
+        for (auto* b : blocks) n += b->n;
+        if (n == 0) continue;
+        DevVersion v;
+        v.n = n;
+        for (u32 j = 0; j < arity[name]; ++j) {
+            DBuf<u32> col(c, n);
+            u64 off = 0;
+            for (auto* b : blocks) {
+                col.upload(b->cols[j], b->n, off);
+                off += b->n;
+            }
+            v.cols.push_back(std::move(col));
+        }
+        edb.rels.emplace(name, std::move(v));
+    }
+    return edb;
+}
+
 std::unique_ptr<EvalState> evaluate(Ctx* c, const std::vector<RelationDecl>& decls,
                                     const std::vector<Plan>& plans, const std::vector<FactsBlock>& facts) {
+    check_plans(decls, plans);
+    const auto t0 = Clock::now();
+    DeviceEdb edb = upload_facts(c, decls, facts);
+    auto st = evaluate_device(c, decls, plans, {&edb});
+    st->elapsed_ms = ms_since(t0);
+    return st;
+}
+
+std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDecl>& decls,
+                                           const std::vector<Plan>& plans,
+                                           const std::vector<const DeviceEdb*>& edbs) {
     check_plans(decls, plans);
     const auto t0 = Clock::now();
     auto st = std::make_unique<EvalState>();
@@ -366,51 +409,58 @@ std::unique_ptr<EvalState> evaluate(Ctx* c, const std::vector<RelationDecl>& dec
         st->relations[d.name] = std::move(r);
     }
 
-    // ---- upload EDB, choose the key shift from the active domain ----------
-    std::map<std::string, std::vector<const FactsBlock*>> by_rel;
-    for (auto& f : facts) {
-        auto it = st->relations.find(f.relation);
-        if (it == st->relations.end()) continue;  // facts for undeclared relations are ignored
-        if (f.arity != it->second->arity) fail(FV_ERR_ARITY, "facts for '" + f.relation + "' have the wrong arity");
-        by_rel[f.relation].push_back(&f);
+    // ---- gather the resident EDB blocks, key shift from the active domain ----
+    std::map<std::string, std::vector<const DevVersion*>> by_rel;
+    for (const DeviceEdb* e : edbs)
+        for (auto& [name, v] : e->rels) {
+            auto it = st->relations.find(name);
+            if (it == st->relations.end() || v.n == 0) continue;
+            if (v.cols.size() != it->second->arity) fail(FV_ERR_ARITY, "facts for '" + name + "' have the wrong arity");
+            by_rel[name].push_back(&v);
+        }
+    std::map<std::string, DevVersion> concat;  // only for relations with several blocks
+    std::map<std::string, const DevVersion*> raw;
+    for (auto& [name, blocks] : by_rel) {
+        if (blocks.size() == 1) {
+            raw[name] = blocks[0];
+            continue;
+        }
+        u64 n = 0;
+        for (auto* b : blocks) n += b->n;
+        DevVersion v;
+        v.n = n;
+        for (u32 j = 0; j < st->relations[name]->arity; ++j) {
+            DBuf<u32> col(c, n);
+            u64 off = 0;
+            for (auto* b : blocks) {
+                FV_CUDA(cudaMemcpyAsync(col.get() + off, b->cols[j].get(), 4 * b->n, cudaMemcpyDeviceToDevice,
+                                        c->stream));
+                off += b->n;
+            }
+            v.cols.push_back(std::move(col));
+        }
+        raw[name] = &concat.emplace(name, std::move(v)).first->second;
     }
-    std::map<std::string, DevVersion> raw;
     u64 vmax = 0;
     for (auto& p : plans)
         for (auto& s : p.sources)
             for (auto& cs : s.const_selects) vmax = std::max<u64>(vmax, cs.second);
     u64* dmax = c->d_scalars + 22;
-    std::vector<u64> col_max;
-    for (auto& [name, blocks] : by_rel) {
-        u64 n = 0;
-        for (auto* b : blocks) n += b->n;
-        if (n == 0) continue;
-        DevVersion v;
-        v.n = n;
-        const u32 arity = st->relations[name]->arity;
-        for (u32 j = 0; j < arity; ++j) {
-            DBuf<u32> col(c, n);
-            u64 off = 0;
-            for (auto* b : blocks) {
-                col.upload(b->cols[j], b->n, off);
-                off += b->n;
-            }
-            v.cols.push_back(std::move(col));
-        }
-        raw.emplace(name, std::move(v));
-    }
-    for (auto& [name, v] : raw)
+    for (auto& [name, vp] : raw) {
+        const DevVersion& v = *vp;
         for (auto& col : v.cols) {
             reduce_max_u32(c, col.get(), v.n, dmax);
             u64 m = 0;
             c->read_scalars(dmax, &m, 1);
             vmax = std::max(vmax, m);
         }
+    }
     st->key_shift = std::max<u32>(1, bit_width_u64(vmax));
 
     Engine eng(c, *st);
     // ---- seed: FULL = DELTA = dedup(EDB) (engine.cpp:148-161) ---------------
-    for (auto& [name, v] : raw) {
+    for (auto& [name, vp] : raw) {
+        const DevVersion& v = *vp;
         RelState& r = *st->relations[name];
         CandPool pool;
         pool.arity = r.arity;
@@ -423,6 +473,7 @@ std::unique_ptr<EvalState> evaluate(Ctx* c, const std::vector<RelationDecl>& dec
         // DELTA must equal FULL; the merge produced two identical copies.
     }
     raw.clear();
+    concat.clear();
 
     // ---- variants (delta_rewrite, engine.cpp:57-64) --------------------------
     struct Variant {

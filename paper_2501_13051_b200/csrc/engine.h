@@ -119,9 +119,22 @@ struct EvalState {
     u32 key_shift = 32;
 };
 
+// EDB resident in HBM (unsorted, possibly duplicated rows, per relation).
+struct DeviceEdb {
+    std::map<std::string, DevVersion> rels;
+};
+
+DeviceEdb upload_facts(Ctx* c, const std::vector<RelationDecl>& decls, const std::vector<FactsBlock>& facts);
+
+// Host facts: upload + seed + fixpoint (elapsed_ms spans all three, the
+// reference's evaluate() boundary, P/src/runner.cpp:58-61).
 std::unique_ptr<EvalState> evaluate(Ctx* c, const std::vector<RelationDecl>& decls,
                                     const std::vector<Plan>& plans,
                                     const std::vector<FactsBlock>& facts);
+// EDB already resident: seed + fixpoint.
+std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDecl>& decls,
+                                           const std::vector<Plan>& plans,
+                                           const std::vector<const DeviceEdb*>& edbs);
 
 // Validate plan structure against the declarations (throws FV_ERR_PLAN).
 void check_plans(const std::vector<RelationDecl>& decls, const std::vector<Plan>& plans);

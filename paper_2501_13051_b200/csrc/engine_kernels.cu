@@ -560,6 +560,7 @@ u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids) {
 void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, const RowFilter& pred,
                         u32* starts, u32* counts) {
     if (!n) return;
+    ProfScope prof(c, "join_probe_count", double(n) * 20.0);
     probe_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(probe, n, idx.ht.slots.get(), idx.ht.mask,
                                                             idx.ustart.get(), idx.ucount.get(), pred,
                                                             starts, counts);
@@ -571,6 +572,16 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
                         const OutSpec& spec) {
     if (!total) return;
     const u64 tiles = ceil_div(total, kMatTile);
+    // Algorithmic bytes: per probe row its offset and run start; per output
+    // its build-side operands and the written row.
+    double side1 = 0, side0 = 0;
+    for (u32 k = 0; k < spec.n_out; ++k) (spec.col[k].side ? side1 : side0) += 4;
+    for (u32 k = 0; k < spec.n_filters; ++k) {
+        (spec.f[k].a.side ? side1 : side0) += 4;
+        if (spec.f[k].op != kFilterConst) (spec.f[k].b.side ? side1 : side0) += 4;
+    }
+    const double out_bytes = spec.key_mode ? 8.0 * ((spec.n_out + 1) / 2) : 4.0 * spec.n_out;
+    ProfScope prof(c, "join_materialize", double(m) * (12.0 + side0) + double(total) * (side1 + out_bytes));
     if (spec.n_filters)
         materialize_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(offsets, m, total,
                                                                                            starts, spec);
@@ -584,6 +595,8 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
 void engine_project(Ctx* c, u64 n, const OutSpec& spec) {
     if (!n) return;
     const u64 tiles = ceil_div(n, kMatTile);
+    ProfScope prof(c, "project", double(n) * (4.0 * (spec.n_out + 2 * spec.n_filters) +
+                                               8.0 * ((spec.n_out + 1) / 2)));
     if (spec.n_filters)
         project_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(n, spec);
     else
@@ -628,6 +641,7 @@ void engine_pack_keys(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 sh
     const u32 arity = static_cast<u32>(cols.size());
     Words4 w{};
     for (u32 k = 0; k < (arity + 1) / 2; ++k) w.p[k] = words[k];
+    ProfScope prof(c, "pack_keys", double(n) * (4.0 * arity + 8.0 * ((arity + 1) / 2)));
     pack_kernel<<<grid_for(n), 256, 0, c->stream>>>(cols8(cols), arity, n, shift, w);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
@@ -639,6 +653,9 @@ static void merge_launch(Ctx* c, const Cols8& a, u64 n_a, const Words4& b, u64 n
     const u64 tiles = ceil_div(n_a + n_b, MergeTraits<W>::kTile);
     u32* counter = nullptr;
     const u32 epoch = c->lookback_epoch(tiles, &counter);
+    // Reads FULL and the candidates once, rewrites FULL; the 2 x |DELTA| row
+    // writes are added by the caller once |DELTA| is known (prof_add_bytes).
+    ProfScope prof(c, "merge_dedup", 8.0 * double(n_a) * arity + 8.0 * W * double(n_b));
     merge_kernel<W><<<static_cast<unsigned>(tiles), MergeTraits<W>::kBlock, 0, c->stream>>>(
         a, n_a, b, n_b, arity, shift, co, dout, c->lb.status, epoch, counter, d_new);
     FV_CUDA(cudaGetLastError());

@@ -56,8 +56,34 @@ struct LookbackPool {
     u32 epoch = 0;
 };
 
+// Per-kernel-class timing with CUDA events on the launching stream (enabled
+// by fv_ctx_profile; used by bench.py for the live roofline numbers).
+struct ProfAgg {
+    u64 launches = 0;
+    double ms = 0.0;
+    double bytes = 0.0;  // algorithmic bytes (implementation-independent)
+};
+
 struct Ctx {
     int device = 0;
+    bool prof = false;
+    struct ProfRec {
+        const char* name;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    std::vector<ProfRec> prof_pending;
+    std::vector<cudaEvent_t> prof_events;
+    std::vector<std::pair<std::string, ProfAgg>> prof_agg;
+    cudaEvent_t prof_begin();
+    void prof_end(const char* name, cudaEvent_t a, double bytes);
+    void prof_flush();  // after a stream sync
+    void prof_add_bytes(const char* name, double bytes) {
+        if (!prof) return;
+        prof_flush();
+        for (auto& [n, a] : prof_agg)
+            if (n == name) a.bytes += bytes;
+    }
     cudaStream_t stream = nullptr;
     cudaMemPool_t pool = nullptr;
     std::string last_error;
@@ -81,6 +107,25 @@ struct Ctx {
 
 Ctx* ctx_new(int device);
 void ctx_delete(Ctx* c);
+
+// RAII timing of one kernel launch (no-op unless profiling is enabled).
+class ProfScope {
+public:
+    ProfScope(Ctx* c, const char* name, double bytes) : c_(c), name_(name), bytes_(bytes) {
+        if (c_->prof) a_ = c_->prof_begin();
+    }
+    ~ProfScope() {
+        if (c_->prof && a_) c_->prof_end(name_, a_, bytes_);
+    }
+    ProfScope(const ProfScope&) = delete;
+    ProfScope& operator=(const ProfScope&) = delete;
+
+private:
+    Ctx* c_;
+    const char* name_;
+    double bytes_;
+    cudaEvent_t a_ = nullptr;
+};
 
 // ---- device buffers ------------------------------------------------------
 

@@ -46,7 +46,55 @@ void Ctx::release(void* p) {
     if (p) cudaFreeAsync(p, stream);
 }
 
-void Ctx::sync() { FV_CUDA(cudaStreamSynchronize(stream)); }
+void Ctx::sync() {
+    FV_CUDA(cudaStreamSynchronize(stream));
+    if (!prof_pending.empty()) prof_flush();
+}
+
+cudaEvent_t Ctx::prof_begin() {
+    cudaEvent_t e;
+    if (prof_events.empty()) {
+        FV_CUDA(cudaEventCreate(&e));
+    } else {
+        e = prof_events.back();
+        prof_events.pop_back();
+    }
+    FV_CUDA(cudaEventRecord(e, stream));
+    return e;
+}
+
+void Ctx::prof_end(const char* name, cudaEvent_t a, double bytes) {
+    cudaEvent_t b;
+    if (prof_events.empty()) {
+        FV_CUDA(cudaEventCreate(&b));
+    } else {
+        b = prof_events.back();
+        prof_events.pop_back();
+    }
+    FV_CUDA(cudaEventRecord(b, stream));
+    prof_pending.push_back({name, a, b, bytes});
+}
+
+void Ctx::prof_flush() {
+    for (auto& r : prof_pending) {
+        float ms = 0.f;
+        FV_CUDA(cudaEventSynchronize(r.b));
+        FV_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        ProfAgg* agg = nullptr;
+        for (auto& [n, a] : prof_agg)
+            if (n == r.name) agg = &a;
+        if (!agg) {
+            prof_agg.emplace_back(r.name, ProfAgg{});
+            agg = &prof_agg.back().second;
+        }
+        agg->launches += 1;
+        agg->ms += ms;
+        agg->bytes += r.bytes;
+        prof_events.push_back(r.a);
+        prof_events.push_back(r.b);
+    }
+    prof_pending.clear();
+}
 
 u32 Ctx::lookback_epoch(u64 words, u32** tile_counter) {
     if (words > lb.capacity) {
@@ -74,6 +122,7 @@ void Ctx::read_scalars(const u64* d, u64* h, int n) {
     FV_CUDA(cudaMemcpyAsync(pinned, d, sizeof(u64) * n, cudaMemcpyDeviceToHost, stream));
     FV_CUDA(cudaStreamSynchronize(stream));
     std::memcpy(h, pinned, sizeof(u64) * n);
+    if (!prof_pending.empty()) prof_flush();
 }
 
 Ctx* ctx_new(int device) {
@@ -121,6 +170,11 @@ void ctx_delete(Ctx* c) {
         cudaStreamDestroy(c->stream);
     }
     if (c->pinned) cudaFreeHost(c->pinned);
+    for (auto& r : c->prof_pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->prof_events) cudaEventDestroy(e);
     delete c;
 }
 

@@ -37,6 +37,7 @@ void exclusive_scan_counts(Ctx* c, const u32* counts, u64* offsets, u64 n) {
         FV_CUDA(cudaMemsetAsync(offsets, 0, sizeof(u64), c->stream));
         return;
     }
+    ProfScope prof(c, "scan_offsets", double(n) * 12.0);
     tile_scan(c, ScanCountsOp{counts, offsets, n}, n, nullptr);
 }
 
@@ -58,6 +59,7 @@ void iota_u32(Ctx* c, u32* out, u64 n) {
 
 void gather_u32(Ctx* c, const u32* src, const u32* idx, u32* out, u64 n) {
     if (!n) return;
+    ProfScope prof(c, "gather", double(n) * 12.0);
     gather_kernel<<<grid_for(n), 256, 0, c->stream>>>(src, idx, out, n);
     FV_CUDA(cudaGetLastError());
     c->count_launch();

@@ -236,6 +236,9 @@ void onesweep_pass(Ctx* c, const K* kin, K* kout, const u32* vin, u32* vout, u64
     u32* counter = nullptr;
     const u32 epoch = c->lookback_epoch(tiles * kRadix, &counter);
     const size_t smem = sizeof(K) * TILE + (HAS_VAL ? sizeof(u32) * TILE : 0);
+    ProfScope prof(c, sizeof(K) == 8 ? (HAS_VAL ? "radix_onesweep_u64_kv" : "radix_onesweep_u64")
+                                     : (HAS_VAL ? "radix_onesweep_u32_kv" : "radix_onesweep_u32"),
+                   2.0 * double(n) * (sizeof(K) + (HAS_VAL ? 4 : 0)));
     onesweep_kernel<K, HAS_VAL><<<static_cast<unsigned>(tiles), kSortBlock, smem, c->stream>>>(
         kin, kout, vin, vout, n, shift, mask, bins, c->lb.status, epoch, counter);
     FV_CUDA(cudaGetLastError());
@@ -257,6 +260,7 @@ bool radix_sort_impl(Ctx* c, K* keys, K* keys_alt, u32* vals, u32* vals_alt, u64
         const u64 want = ceil_div(n, 256 * 8);
         const unsigned grid = static_cast<unsigned>(want < u64(kNumSMs) * 8 ? (want ? want : 1)
                                                                              : u64(kNumSMs) * 8);
+        ProfScope prof(c, "radix_histogram", double(n) * sizeof(K));
         radix_hist_kernel<K><<<grid, 256, 0, c->stream>>>(keys, n, begin_bit, end_bit, npass, hist);
         FV_CUDA(cudaGetLastError());
         radix_bins_kernel<<<npass, kRadix, 0, c->stream>>>(hist, bins, n, trivial);

@@ -1,0 +1,208 @@
+"""GPU parity of the fixpoint engine (through the C ABI): identical sorted
+tuple sets, per-iteration delta counts and iteration counts as the
+reference (tests/golden/engine.json), the oracle restatement and the naive
+evaluator; the reference's run()/CLI surface (P/tests/io_test.cpp:148-229,
+P/tests/CMakeLists.txt:25-35); full-size checks at BASELINE sizes."""
+import json
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+import golden_cases
+from conftest import GOLDEN, ROOT, load_golden, matches
+from oracle import naive
+from paper_2501_13051_b200 import _lib
+from paper_2501_13051_b200 import engine as E
+from paper_2501_13051_b200 import workloads as W
+from progen import Rng, random_edb, random_program
+
+pytestmark = pytest.mark.gpu
+
+
+def _rows_set(a):
+    return {tuple(r) for r in np.asarray(a).tolist()}
+
+
+def test_engine_golden_cases(ctx):
+    for case in load_golden("engine.json"):
+        text, facts = golden_cases.program_and_facts(case)
+        st = E.evaluate_program(text, facts, ctx=ctx)
+        assert st.iterations == case["iterations"], case["name"]
+        got_stats = [(s.index, s.relation, s.delta_rows, s.full_rows, s.merges) for s in st.stats()]
+        assert got_stats == [tuple(s) for s in case["stats"]], case["name"]
+        rels = st.relations()
+        assert set(rels) == set(case["relations"]), case["name"]
+        for rel, exp in case["relations"].items():
+            assert rels[rel][1] == exp["rows"], (case["name"], rel)
+            assert matches(st.dump(rel).reshape(-1), exp["dump"]), (case["name"], rel)
+
+
+def test_engine_vs_oracle_and_naive_random_programs(ctx, oracle):
+    g = Rng(56)
+    compared = 0
+    for _ in range(60):
+        text, arities = random_program(g)
+        prog = E.compile_program(text)
+        if prog.validate():
+            continue
+        facts = random_edb(g, arities, 40)
+        st = E.evaluate_program(prog, facts, ctx=ctx)
+        it, rels, deltas = oracle.evaluate(*prog.oracle_args(facts))
+        exp = naive.naive_evaluate(text, {k: [tuple(r) for r in v] for k, v in facts.items()})
+        names = [r for r, _ in prog.relations()]
+        assert st.iterations == it, text
+        for k, name in enumerate(names):
+            got = st.dump(name)
+            assert np.array_equal(got, rels[k]), (text, name)
+            assert _rows_set(got) == exp.get(name, set()), (text, name)
+        dc = st.delta_counts()
+        for rel, seq in dc.items():
+            assert seq == [deltas[i][names.index(rel)] for i in range(it)], (text, rel)
+        compared += 1
+    assert compared > 15
+
+
+def test_residual_equalities_follow_the_naive_semantics(ctx):
+    # Multi-variable joins: the reference's filter_pairs_eq (P/src/kernels.cpp:155)
+    # indexes the left values by pair position; the engine implements the
+    # intended semantics and is checked against the naive evaluator.
+    text = ("t(x, y) :- a(x, y), b(x, y).\n"
+            "u(x, z) :- a(x, y), b(y, x), c(x, y, z).\n"
+            "p(x) :- a(x, x).\n")
+    g = Rng(9)
+    for r in range(6):
+        facts = {"a": W.random_rows(100 + r, 80, 2, 6), "b": W.random_rows(200 + r, 80, 2, 6),
+                 "c": W.random_rows(300 + r, 60, 3, 6)}
+        st = E.evaluate_program(text, facts, ctx=ctx)
+        exp = naive.naive_evaluate(text, {k: [tuple(x) for x in v] for k, v in facts.items()})
+        for rel in ("t", "u", "p"):
+            assert _rows_set(st.dump(rel)) == exp[rel], rel
+
+
+def test_explicit_plan_boundary(ctx):
+    prog = E.compile_program(W.SG_PROGRAM)
+    facts = {"edge": W.binary_tree(6)}
+    a = E.evaluate_program(prog, facts, ctx=ctx)
+    b = E.evaluate(prog.relations(), prog.plans(), facts, ctx=ctx)
+    assert np.array_equal(a.dump("sg"), b.dump("sg"))
+    assert a.delta_counts() == b.delta_counts()
+    bad = prog.plans()
+    bad[1].joins[0].right_col = 7
+    with pytest.raises(_lib.DiagnosticError):
+        E.evaluate(prog.relations(), bad, facts, ctx=ctx)
+
+
+def test_invalid_programs_raise_diagnostics(ctx):
+    with pytest.raises(_lib.DiagnosticError, match="head variable 'z'"):
+        E.evaluate_program("reach(x, z) :- edge(x, y).", {}, ctx=ctx)
+    with pytest.raises(_lib.DiagnosticError, match="cross products"):
+        E.evaluate_program("a(x, y) :- b(x), c(y).", {}, ctx=ctx)
+
+
+def test_fingerprint_matches_host_restatement(ctx):
+    st = E.evaluate_program(W.TC_PROGRAM, {"edge": W.tc_uniform(500, 2500, 3)}, ctx=ctx)
+    assert st.fingerprint("reach") == E.fingerprint_rows(st.dump("reach"))
+
+
+def test_seed_deduplicates_and_counts(ctx):
+    st = E.evaluate_program(W.TC_PROGRAM, {"edge": np.array([[1, 2], [1, 2], [2, 3]], np.uint32)}, ctx=ctx)
+    assert st.rows("edge") == 2
+    assert _rows_set(st.dump("reach")) == {(1, 2), (2, 3), (1, 3)}
+    s = E.evaluate_program("reach(x, y) :- edge(x, y).\n", {"edge": np.array([[1, 2]], np.uint32)}, ctx=ctx)
+    assert s.iterations == 2
+
+
+def test_delta_sum_equals_full(ctx):
+    st = E.evaluate_program(W.TC_PROGRAM, {"edge": W.path_graph(15)}, ctx=ctx)
+    assert sum(st.delta_counts()["reach"]) == st.rows("reach") == 105
+
+
+def test_max_u32_values_and_arity4(ctx):
+    big = np.array([[4294967295, 0], [0, 4294967294], [4294967294, 4294967295]], np.uint32)
+    st = E.evaluate_program(W.TC_PROGRAM, {"edge": big}, ctx=ctx)
+    exp = naive.naive_evaluate(W.TC_PROGRAM, {"edge": [tuple(map(int, r)) for r in big]})
+    assert _rows_set(st.dump("reach")) == exp["reach"]
+    text = "q(a, b, c, d) :- r(a, b, c, d).\nq(a, b, c, e) :- q(a, b, c, d), r(d, x, y, e), a != e.\n"
+    facts = {"r": W.random_rows(5, 200, 4, 9)}
+    st = E.evaluate_program(text, facts, ctx=ctx)
+    exp = naive.naive_evaluate(text, {"r": [tuple(map(int, r)) for r in facts["r"]]})
+    assert _rows_set(st.dump("q")) == exp["q"]
+
+
+# ---- runner / CLI (P/tests/io_test.cpp:161-229, P/tests/CMakeLists.txt:25-35) ----------------
+
+
+def test_run_path10_end_to_end():
+    with tempfile.TemporaryDirectory() as d:
+        prog = os.path.join(d, "tc.dl")
+        open(prog, "w").write(W.TC_PROGRAM)
+        W.write_tsv_dir(os.path.join(d, "facts"), {"edge": W.path_graph(10)})
+        rc, out, err = E.run(prog, os.path.join(d, "facts"), os.path.join(d, "out"), stats=True, dump=["reach"])
+        assert rc == 0 and err == ""
+        assert "rel=reach rows=45" in out and "iter=0 rel=reach delta=9" in out
+        assert open(os.path.join(d, "out", "reach.tsv")).readline().strip() == "0\t1"
+
+
+def test_run_rejects_invalid_program():
+    with tempfile.TemporaryDirectory() as d:
+        prog = os.path.join(d, "bad.dl")
+        open(prog, "w").write("reach(x, z) :- edge(x, y).\n")
+        os.makedirs(os.path.join(d, "facts"))
+        rc, out, err = E.run(prog, os.path.join(d, "facts"), os.path.join(d, "out"))
+        assert rc != 0 and "head variable 'z'" in err
+
+
+def test_run_resolves_string_constants():
+    with tempfile.TemporaryDirectory() as d:
+        prog = os.path.join(d, "family.dl")
+        open(prog, "w").write('parentof("Larry", "Alice").\nparentof("Alice", "Bob").\n'
+                              "ancestor(x, y) :- parentof(x, y).\n"
+                              "ancestor(x, z) :- parentof(x, y), ancestor(y, z).\n")
+        os.makedirs(os.path.join(d, "facts"))
+        rc, out, err = E.run(prog, os.path.join(d, "facts"), os.path.join(d, "out"), dump=["ancestor"])
+        assert rc == 0 and "rel=ancestor rows=3" in out
+        assert "Larry\tBob" in open(os.path.join(d, "out", "ancestor.tsv")).read()
+
+
+def test_cli_binary_matches_reference_ctests():
+    cli = os.path.join(ROOT, "paper_2501_13051_b200", "fvlog")
+    data = os.path.join(ROOT, "tests", "data")
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run([cli, "run", os.path.join(data, "tc.dl"), "--facts", os.path.join(data, "path10"),
+                            "--out", d, "--dump", "reach"], capture_output=True, text=True)
+        assert r.returncode == 0 and "rel=reach rows=45" in r.stdout
+        r = subprocess.run([cli, "run", os.path.join(data, "invalid_unbound.dl"), "--facts",
+                            os.path.join(data, "path10"), "--out", d], capture_output=True, text=True)
+        assert r.returncode != 0
+
+
+# ---- full BASELINE sizes: size-independent checks --------------------------------------------
+
+
+def _large():
+    p = os.path.join(GOLDEN, "large.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+def test_sg_c3_full_size_closed_form(ctx):
+    st = E.evaluate_program(W.SG_PROGRAM, {"edge": W.sg_forest(244, 10)}, ctx=ctx)
+    assert st.rows("sg") == W.sg_count(244, 10) == 340_637_176
+    assert st.iterations == 11
+    # SG of a forest of identical trees: every tree contributes the same rows.
+    assert sum(st.delta_counts()["sg"]) == 340_637_176
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_tc_full_size_against_large_goldens(ctx, cfg):
+    g = _large().get(cfg)
+    if not g:
+        pytest.skip(f"{cfg} golden not generated (tests/golden/make_golden_large.py)")
+    edges = W.tc_uniform(10_000, 50_000, 1) if cfg == "C1" else W.tc_powerlaw(1000, 1000, 5000, 1)
+    st = E.evaluate_program(W.TC_PROGRAM, {"edge": edges}, ctx=ctx)
+    assert st.rows("reach") == g["rows"]
+    assert st.delta_counts()["reach"] == g["deltas"]
+    assert st.iterations == g["iterations"]
+    assert str(st.fingerprint("reach")) == g["fingerprint"]

@@ -76,3 +76,48 @@ def test_oracle_against_built_reference(oracle):
             assert np.array_equal(x, y)
         rows = W.random_rows(seed, 700, 3, 5)
         assert np.array_equal(oracle.dedup_rows(rows, 3), ref.dedup_rows(rows, 3))
+
+
+# ---- engine: oracle restatement vs reference goldens and the naive oracle ----
+
+import json
+import os
+
+from paper_2501_13051_b200 import engine as E
+from oracle import naive
+from progen import Rng, random_edb, random_program
+import golden_cases
+
+
+def test_oracle_engine_golden(oracle):
+    for case in load_golden("engine.json"):
+        text, facts = golden_cases.program_and_facts(case)
+        if case["name"] == "SG tree depth 10":
+            continue  # 1.4M rows: covered on the GPU; too slow for the C oracle here
+        prog = E.compile_program(text)
+        it, rels, deltas = oracle.evaluate(*prog.oracle_args(facts))
+        assert it == case["iterations"], case["name"]
+        names = [r for r, _ in prog.relations()]
+        for rel, exp in case["relations"].items():
+            got = rels[names.index(rel)]
+            assert got.shape[0] == exp["rows"], (case["name"], rel)
+            assert matches(got.reshape(-1), exp["dump"]), (case["name"], rel)
+        for (i, rel, d, _full, _m) in case["stats"]:
+            assert deltas[i][names.index(rel)] == d, (case["name"], i, rel)
+
+
+def test_oracle_engine_vs_naive_random_programs(oracle):
+    g = Rng(56)
+    compared = 0
+    for _ in range(40):
+        text, arities = random_program(g)
+        prog = E.compile_program(text)
+        if prog.validate():
+            continue
+        facts = random_edb(g, arities, 40)
+        it, rels, _ = oracle.evaluate(*prog.oracle_args(facts))
+        exp = naive.naive_evaluate(text, {k: [tuple(r) for r in v] for k, v in facts.items()})
+        for k, (name, _a) in enumerate(prog.relations()):
+            assert {tuple(r) for r in rels[k].tolist()} == exp.get(name, set()), (text, name)
+        compared += 1
+    assert compared > 10
