@@ -4,6 +4,9 @@
 #include <cstring>
 
 #include "api_internal.h"
+#include "transport.h"
+
+fv_ctx::~fv_ctx() = default;
 
 using fv::DBuf;
 using fv::u32;
@@ -85,8 +88,27 @@ fv_status fv_ctx_create(int device, fv_ctx** out) {
 
 void fv_ctx_destroy(fv_ctx* ctx) {
     if (!ctx) return;
+    if (ctx->c) ctx->c->tx = nullptr;
+    ctx->tx.reset();
     fv::ctx_delete(ctx->c);
     delete ctx;
+}
+
+fv_status fv_nccl_unique_id(void* out128) {
+    FV_API_BEGIN(nullptr)
+    FV_REQUIRE(out128, FV_ERR_INVALID, "fv_nccl_unique_id: null out");
+    fv::nccl_unique_id(out128);
+    FV_API_END
+}
+
+fv_status fv_ctx_set_nccl(fv_ctx* ctx, int rank, int world, const void* id128) {
+    FV_API_BEGIN(ctx)
+    FV_REQUIRE(ctx && id128 && world >= 1 && rank >= 0 && rank < world, FV_ERR_INVALID,
+               "fv_ctx_set_nccl: bad argument");
+    ctx->c->tx = nullptr;
+    ctx->tx = fv::make_nccl_transport(ctx->c, rank, world, id128);
+    ctx->c->tx = ctx->tx.get();
+    FV_API_END
 }
 
 const char* fv_last_error(const fv_ctx* ctx) {

@@ -3,9 +3,12 @@
 #include <cstring>
 #include <sstream>
 
+#include <set>
+
 #include "api_internal.h"
 #include "frontend.h"
 #include "runner.h"
+#include "transport.h"
 
 using fv::u32;
 using fv::u64;
@@ -349,6 +352,95 @@ fv_status fv_evaluate_program_edb(fv_ctx* ctx, const fv_program* p, const fv_edb
         for (u32 j = 0; j < b.arity; ++j) b.cols.push_back(storage[si++].data());
     fv::DeviceEdb text_edb = fv::upload_facts(ctx->c, decls, blocks);
     *out = wrap_state(ctx, fv::evaluate_device(ctx->c, decls, mp->plans, {&text_edb, &edb->edb}));
+    FV_API_END
+}
+
+fv_status fv_evaluate_program_sharded(fv_ctx* ctx, const fv_program* p, const fv_facts* facts, uint32_t n_facts,
+                                      uint32_t world, fv_state** states_out) {
+    FV_API_BEGIN(ctx)
+    FV_REQUIRE(ctx && p && states_out && (facts || !n_facts), FV_ERR_INVALID,
+               "fv_evaluate_program_sharded: null argument");
+    auto* mp = const_cast<fv_program*>(p);
+    ensure_compiled(mp);
+    auto pf = fv::fe::program_facts(mp->prog);
+    std::map<std::string, u32> arity;
+    for (auto& r : mp->prog.relations) arity[r.name] = r.arity;
+    std::vector<std::vector<u32>> storage;
+    for (auto& [rel, rows] : pf) {
+        const u32 a = arity[rel];
+        const u64 n = rows.size() / a;
+        for (u32 j = 0; j < a; ++j) {
+            storage.emplace_back(n);
+            for (u64 i = 0; i < n; ++i) storage.back()[i] = rows[i * a + j];
+        }
+    }
+    std::vector<fv::FactsBlock> blocks;
+    size_t si = 0;
+    for (auto& [rel, rows] : pf) {
+        const u32 a = arity[rel];
+        fv::FactsBlock b{rel, a, rows.size() / a, {}};
+        for (u32 j = 0; j < a; ++j) b.cols.push_back(storage[si++].data());
+        blocks.push_back(std::move(b));
+    }
+    for (auto& b : blocks_from(facts, n_facts)) blocks.push_back(std::move(b));
+    auto states = fv::evaluate_sharded(ctx->c, world, fv::fe::declarations(mp->prog), mp->plans, blocks);
+    for (uint32_t r = 0; r < world; ++r) states_out[r] = wrap_state(ctx, std::move(states[r]));
+    FV_API_END
+}
+
+fv_status fv_program_partition_plan(const fv_program* p, char* buf, size_t cap, size_t* len) {
+    FV_API_BEGIN(nullptr)
+    FV_REQUIRE(p, FV_ERR_INVALID, "fv_program_partition_plan: null program");
+    auto* mp = const_cast<fv_program*>(p);
+    ensure_compiled(mp);
+    std::set<std::string> idb;
+    for (auto& plan : mp->plans) idb.insert(plan.head);
+    std::map<std::string, std::set<u32>> keyset;
+    std::ostringstream rules;
+    rules << "[";
+    for (size_t i = 0; i < mp->plans.size(); ++i) {
+        const auto dp = fv::dist_plan(mp->plans[i], idb);
+        for (size_t s = 0; s < dp.src_copy.size(); ++s) {
+            const std::string& rel = mp->plans[i].sources[s].relation;
+            if (idb.count(rel)) keyset[rel].insert(dp.src_copy[s]);
+        }
+        rules << (i ? "," : "") << "{\"src_copy\":[";
+        for (size_t s = 0; s < dp.src_copy.size(); ++s) rules << (s ? "," : "") << dp.src_copy[s];
+        rules << "],\"shuffle\":[";
+        for (size_t k = 0; k < dp.shuffle.size(); ++k) rules << (k ? "," : "") << int(dp.shuffle[k]);
+        rules << "],\"replicated_out\":" << (dp.replicated_out ? "true" : "false") << "}";
+    }
+    rules << "]";
+    std::ostringstream os;
+    os << "{\"relations\":{";
+    bool first = true;
+    for (auto& r : mp->prog.relations) {
+        const bool is_idb = idb.count(r.name) > 0;
+        std::set<u32> ks = keyset[r.name];
+        if (is_idb) ks.insert(0);
+        os << (first ? "" : ",") << "\"" << r.name << "\":{\"idb\":" << (is_idb ? "true" : "false") << ",\"keyset\":[";
+        bool f2 = true;
+        for (u32 k : ks) {
+            os << (f2 ? "" : ",") << k;
+            f2 = false;
+        }
+        os << "]}";
+        first = false;
+    }
+    os << "},\"rules\":" << rules.str() << "}";
+    const std::string s = os.str();
+    copy_out(s, buf, cap);
+    if (len) *len = s.size();
+    FV_API_END
+}
+
+uint32_t fv_owner(uint32_t v, uint32_t world) { return fv::owner_of(v, world); }
+
+fv_status fv_state_partition(const fv_state* s, int* rank, int* world) {
+    FV_API_BEGIN(nullptr)
+    FV_REQUIRE(s, FV_ERR_INVALID, "fv_state_partition: null state");
+    if (rank) *rank = s->st->rank;
+    if (world) *world = s->st->world;
     FV_API_END
 }
 

@@ -10,8 +10,14 @@
 #include "column.h"
 #include "fvlog.h"
 
+namespace fv {
+class Transport;
+}
+
 struct fv_ctx {
     fv::Ctx* c = nullptr;
+    std::unique_ptr<fv::Transport> tx;  // partitioned evaluation (NCCL)
+    ~fv_ctx();
 };
 
 struct fv_column {

@@ -15,13 +15,33 @@
 // radix sort plus one merge-path pass. The host reads back one scalar per
 // join step (its output size, to allocate) and one per head relation per
 // iteration (|DELTA|, the fixpoint test).
+//
+// Partitioned evaluation (Ctx::tx != null, world > 1):
+//   - EDB-only relations are replicated on every rank;
+//   - every IDB relation is hash-partitioned: the home copy holds the rows
+//     with owner(hash(col 0)) == rank; a relation probed on column c (as a
+//     join's right atom, or as a rule's first atom joined on c) also keeps a
+//     copy partitioned on c (keyset, derived statically from the plans);
+//   - a join step whose right atom is partitioned needs its probe rows on the
+//     owner of the probe value: intermediates that are replicated (all EDB so
+//     far) or already partitioned on the probe column join locally, others
+//     are shuffled by the probe value first;
+//   - head rows of a replicated derivation are owner-filtered; all others are
+//     routed to owner(head col 0) by ONE all-to-all per head per iteration;
+//   - after the local dedup/merge, the new Δ rows are forwarded to the other
+//     partition copies; |Δ| and |FULL| are all-reduced (termination + stats).
+// Every collective depends only on plan structure, so all ranks issue the
+// same sequence (no data-dependent early exits in partitioned mode).
 #include <algorithm>
 #include <chrono>
+#include <exception>
 #include <set>
+#include <thread>
 
 #include "engine.h"
 #include "prim.cuh"
 #include "radix_sort.h"
+#include "transport.h"
 
 namespace fv {
 
@@ -59,20 +79,64 @@ struct Inter {
     std::vector<DBuf<u32>> owned;
 };
 
+// Partition column of plan source s (the copy it is read from when its
+// relation is partitioned): the probe column of the first join for source 0,
+// the hash column of its join for the others.
+u32 copy_for_source(const Plan& p, u32 s) {
+    if (s == 0) return p.joins.empty() ? 0 : p.joins[0].left.col;
+    return p.joins[s - 1].right_col;
+}
+
+}  // namespace
+
+DistPlan dist_plan(const Plan& p, const std::set<std::string>& idb) {
+    DistPlan d;
+    for (u32 s = 0; s < p.sources.size(); ++s)
+        d.src_copy.push_back(idb.count(p.sources[s].relation) ? copy_for_source(p, s) : 0);
+    bool repl = !idb.count(p.sources[0].relation);
+    ColRef dkey{0, copy_for_source(p, 0)};
+    for (size_t k = 0; k < p.joins.size(); ++k) {
+        const PlanJoin& jn = p.joins[k];
+        const bool rpart = idb.count(p.sources[jn.right_source].relation) > 0;
+        const bool sh = rpart && !repl && !(dkey == jn.left);
+        d.shuffle.push_back(sh ? 1 : 0);
+        if (sh || (rpart && repl)) {
+            dkey = jn.left;
+            repl = false;
+        }
+    }
+    d.replicated_out = repl;
+    return d;
+}
+
+namespace {
+
 class Engine {
 public:
-    Engine(Ctx* c, EvalState& st) : c_(c), st_(st) {}
+    Engine(Ctx* c, EvalState& st) : c_(c), st_(st) {
+        if (c->tx) {
+            world_ = static_cast<u32>(c->tx->world());
+            rank_ = static_cast<u32>(c->tx->rank());
+        }
+    }
 
+    bool dist() const { return world_ > 1; }
+    bool partitioned(const RelState& r) const { return dist() && r.idb; }
     RelState& rel(const std::string& name) { return *st_.relations.at(name); }
 
-    JoinIndex& index(RelState& r, bool delta, u32 col) {
+    DevVersion& vfull(RelState& r, u32 kc) { return kc ? r.copies.at(kc)->full : r.full; }
+    DevVersion& vdelta(RelState& r, u32 kc) { return kc ? r.copies.at(kc)->delta : r.delta; }
+    IndexMap& vindexes(RelState& r, u32 kc) { return kc ? r.copies.at(kc)->indexes : r.indexes; }
+
+    JoinIndex& index(RelState& r, u32 kc, bool delta, u32 col) {
+        IndexMap& m = vindexes(r, kc);
         auto key = std::make_pair(delta ? 1 : 0, col);
-        auto it = r.indexes.find(key);
-        if (it != r.indexes.end()) return *it->second;
+        auto it = m.find(key);
+        if (it != m.end()) return *it->second;
         auto idx = std::make_unique<JoinIndex>();
-        build_index_on(delta ? r.delta : r.full, col, *idx, nullptr);
+        build_index_on(delta ? vdelta(r, kc) : vfull(r, kc), col, *idx, nullptr);
         JoinIndex& ref = *idx;
-        r.indexes.emplace(key, std::move(idx));
+        m.emplace(key, std::move(idx));
         return ref;
     }
 
@@ -106,7 +170,7 @@ public:
             std::vector<const u32*> order_cols{base->cols[col].get()};
             for (u32 j = 0; j < arity; ++j)
                 if (j != col) order_cols.push_back(base->cols[j].get());
-            DBuf<u32> perm = lexicographic_order(c_, order_cols.data(), arity, base->n);
+            DBuf<u32> perm = base->n ? lexicographic_order(c_, order_cols.data(), arity, base->n) : DBuf<u32>();
             DevVersion sorted;
             sorted.n = base->n;
             for (u32 j = 0; j < arity; ++j) {
@@ -136,16 +200,96 @@ public:
         if (s.n_filters >= static_cast<u32>(kMaxFilters)) fail(FV_ERR_PLAN, "rule needs more than 8 filters");
         s.f[s.n_filters++] = x;
     }
+    Filter owner_filter(const SlotRef& s) const {
+        Filter f{s, {}, kFilterOwner, rank_};
+        f.world = world_;
+        return f;
+    }
 
-    // execute_plan (P/src/engine.cpp:72-146) for one variant, appending the
-    // head rows as packed keys to `out`.
-    void exec_variant(const Plan& plan, long delta_source, CandPool& out) {
+    // ---- exchange helpers (partitioned mode) -------------------------------------
+
+    // All-to-all of routed rows. `route` has filled send buffers grouped by
+    // destination with cnt/off; returns the received row count and fills
+    // `recv` buffers (allocated here) for each column.
+    template <typename T>
+    u64 exchange(const std::vector<DBuf<T>>& send, const std::vector<u64>& cnt, const std::vector<u64>& off,
+                 std::vector<DBuf<T>>& recv) {
+        std::vector<u64> rcnt(world_), roff(world_);
+        c_->tx->exchange_counts(c_, cnt.data(), rcnt.data());
+        u64 total = 0;
+        for (u32 p = 0; p < world_; ++p) {
+            roff[p] = total;
+            total += rcnt[p];
+        }
+        recv.clear();
+        std::vector<ExchangeCol> cols;
+        for (size_t j = 0; j < send.size(); ++j) {
+            recv.emplace_back(c_, total);
+            cols.push_back(ExchangeCol{send[j].get(), recv.back().get(), static_cast<u32>(sizeof(T))});
+        }
+        c_->tx->exchange_rows(c_, cols, cnt.data(), off.data(), rcnt.data(), roff.data());
+        return total;
+    }
+
+    // Shuffle an intermediate so every row sits on owner(row[key]).
+    Inter shuffle(const Inter& cur, const ColRef& key) {
+        std::vector<const u32*> in;
+        std::vector<ColRef> refs;
+        for (auto& [r, p] : cur.cols) {
+            refs.push_back(r);
+            in.push_back(p);
+        }
+        std::vector<DBuf<u32>> send;
+        std::vector<u32*> outp;
+        for (size_t j = 0; j < in.size(); ++j) {
+            send.emplace_back(c_, cur.n);
+            outp.push_back(send.back().get());
+        }
+        std::vector<u64> cnt(world_), off(world_);
+        RouteKey rk;
+        rk.col = cur.cols.at(key);
+        engine_route(c_, cur.n, rk, world_, in, outp, {}, {}, cnt.data(), off.data());
+        Inter next;
+        next.n = exchange(send, cnt, off, next.owned);
+        for (size_t j = 0; j < refs.size(); ++j) next.cols[refs[j]] = next.owned[j].get();
+        return next;
+    }
+
+    // Route a candidate pool to owner(head col 0).
+    void route_pool(CandPool& pool) {
+        const u32 W = (pool.arity + 1) / 2;
+        if (pool.words.empty()) pool.words.resize(W);
+        std::vector<const u64*> in;
+        std::vector<DBuf<u64>> send;
+        std::vector<u64*> outp;
+        for (u32 w = 0; w < W; ++w) {
+            in.push_back(pool.words[w].get());
+            send.emplace_back(c_, pool.n);
+            outp.push_back(send.back().get());
+        }
+        RouteKey rk;
+        rk.word = pool.words[0].get();
+        rk.shift = st_.key_shift;
+        rk.hi = pool.arity >= 2 ? 1 : 0;
+        std::vector<u64> cnt(world_), off(world_);
+        engine_route(c_, pool.n, rk, world_, {}, {}, in, outp, cnt.data(), off.data());
+        std::vector<DBuf<u64>> recv;
+        pool.n = exchange(send, cnt, off, recv);
+        pool.words = std::move(recv);
+        pool.cap = pool.n;
+    }
+
+    // ---- execute_plan (P/src/engine.cpp:72-146) for one variant ------------------
+
+    void exec_variant(const Plan& plan, const DistPlan& dp, long delta_source, CandPool& out) {
         const u32 ns = static_cast<u32>(plan.sources.size());
+        const bool D = dist();
         std::vector<const DevVersion*> ver(ns);
         for (u32 s = 0; s < ns; ++s) {
             RelState& r = rel(plan.sources[s].relation);
-            ver[s] = (static_cast<long>(s) == delta_source) ? &r.delta : &r.full;
-            if (ver[s]->n == 0) return;  // engine.cpp:76-78
+            const u32 kc = partitioned(r) ? dp.src_copy[s] : 0;
+            ver[s] = (static_cast<long>(s) == delta_source) ? &vdelta(r, kc) : &vfull(r, kc);
+            if (!D && ver[s]->n == 0) return;  // engine.cpp:76-78
         }
         Inter cur;
         cur.n = ver[0]->n;
@@ -169,6 +313,8 @@ public:
             const PlanJoin& jn = plan.joins[k];
             const u32 R = jn.right_source;
             RelState& rr = rel(plan.sources[R].relation);
+            const bool rpart = partitioned(rr);
+            if (D && dp.shuffle[k]) cur = shuffle(cur, jn.left);
             std::unique_ptr<JoinIndex> tmp;
             JoinIndex* idx;
             if (plan.sources[R].constrained()) {
@@ -176,9 +322,9 @@ public:
                 build_index_on(*ver[R], jn.right_col, *tmp, &plan.sources[R]);
                 idx = tmp.get();
             } else {
-                idx = &index(rr, static_cast<long>(R) == delta_source, jn.right_col);
+                idx = &index(rr, rpart ? jn.right_col : 0, static_cast<long>(R) == delta_source, jn.right_col);
             }
-            if (idx->rows->n == 0) return;
+            if (!D && idx->rows->n == 0) return;
             const u64 n = cur.n;
             DBuf<u32> starts(c_, n), counts(c_, n);
             RowFilter pred;
@@ -186,12 +332,11 @@ public:
             engine_probe_count(c_, cur.cols.at(jn.left), n, *idx, pred, starts.get(), counts.get());
             DBuf<u64> offsets(c_, n + 1);
             exclusive_scan_counts(c_, counts.get(), offsets.get(), n);
-            u64 T = 0;
             FV_CUDA(cudaMemcpyAsync(c_->pinned, offsets.get() + n, 8, cudaMemcpyDeviceToHost, c_->stream));
             c_->sync();
-            T = c_->pinned[0];
+            const u64 T = c_->pinned[0];
             counts.reset();
-            if (T == 0) return;
+            if (!D && T == 0) return;
 
             const bool last = k + 1 == nj;
             auto slot_of = [&](const ColRef& r) -> SlotRef {
@@ -208,6 +353,7 @@ public:
             if (last) {
                 for (auto& [ga, gb] : plan.guard_neq)
                     push(spec, Filter{slot_of(plan.output_cols[ga]), slot_of(plan.output_cols[gb]), kFilterNeq, 0});
+                if (D && dp.replicated_out) push(spec, owner_filter(slot_of(plan.output_cols[0])));
                 spec.key_mode = 1;
                 spec.n_out = plan.head_arity;
                 for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot_of(plan.output_cols[h]);
@@ -240,7 +386,7 @@ public:
             }
             next.n = produced;
             cur = std::move(next);
-            if (cur.n == 0) return;
+            if (!D && cur.n == 0) return;
         }
         // No joins: a single-atom rule (copy / projection / selection).
         OutSpec spec;
@@ -252,6 +398,7 @@ public:
         auto slot0 = [&](const ColRef& r) { return SlotRef{ver[0]->cols[r.col].get(), 0}; };
         for (auto& [ga, gb] : plan.guard_neq)
             push(spec, Filter{slot0(plan.output_cols[ga]), slot0(plan.output_cols[gb]), kFilterNeq, 0});
+        if (D && dp.replicated_out) push(spec, owner_filter(slot0(plan.output_cols[0])));
         spec.key_mode = 1;
         spec.n_out = plan.head_arity;
         for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot0(plan.output_cols[h]);
@@ -267,45 +414,113 @@ public:
         out.n += produced;
     }
 
-    // Sort candidates and fold them into FULL; returns |DELTA|.
-    u64 dedup_merge(RelState& r, CandPool& cand) {
-        const u32 arity = r.arity;
+    // Sort candidates and fold them into (full, delta); returns |DELTA|.
+    u64 dedup_merge(DevVersion& full, DevVersion& delta, IndexMap& indexes, u32 arity, CandPool& cand) {
         if (cand.n == 0) {
-            r.delta = DevVersion();
-            r.delta.n = 0;
-            r.delta.cols.resize(arity);
-            r.indexes.clear();
+            delta = DevVersion();
+            delta.n = 0;
+            delta.cols.resize(arity);
+            indexes.clear();
             return 0;
         }
         engine_sort_keys(c_, cand.words, cand.n, arity, st_.key_shift);
-        DevVersion C, D;
+        DevVersion C, Dv;
         for (u32 j = 0; j < arity; ++j) {
-            C.cols.emplace_back(c_, r.full.n + cand.n);
-            D.cols.emplace_back(c_, cand.n);
+            C.cols.emplace_back(c_, full.n + cand.n);
+            Dv.cols.emplace_back(c_, cand.n);
         }
         std::vector<u64*> bw;
         for (auto& w : cand.words) bw.push_back(w.get());
         std::vector<u32*> cc, dc;
         for (u32 j = 0; j < arity; ++j) {
             cc.push_back(C.cols[j].get());
-            dc.push_back(D.cols[j].get());
+            dc.push_back(Dv.cols[j].get());
         }
         u64* d_new = c_->d_scalars + 21;
-        engine_merge(c_, r.full.ptrs(), r.full.n, bw.data(), cand.n, arity, st_.key_shift, cc, dc, d_new);
+        engine_merge(c_, full.ptrs(), full.n, bw.data(), cand.n, arity, st_.key_shift, cc, dc, d_new);
         u64 nd = 0;
         c_->read_scalars(d_new, &nd, 1);
         c_->prof_add_bytes("merge_dedup", 8.0 * double(nd) * arity);
-        C.n = r.full.n + nd;
-        D.n = nd;
-        r.full = std::move(C);
-        r.delta = std::move(D);
-        r.indexes.clear();
+        C.n = full.n + nd;
+        Dv.n = nd;
+        full = std::move(C);
+        delta = std::move(Dv);
+        indexes.clear();
         return nd;
     }
+
+    u64 dedup_merge_home(RelState& r, CandPool& cand) { return dedup_merge(r.full, r.delta, r.indexes, r.arity, cand); }
+
+    // Seed one copy of a relation from raw EDB rows (owner-filtered on kc
+    // when partitioned).
+    void seed_copy(RelState& r, const DevVersion& v, u32 kc) {
+        CandPool pool;
+        pool.arity = r.arity;
+        pool.reserve(c_, v.n);
+        const u32 W = (r.arity + 1) / 2;
+        if (!partitioned(r)) {
+            std::vector<u64*> wp;
+            for (auto& w : pool.words) wp.push_back(w.get());
+            engine_pack_keys(c_, v.ptrs(), v.n, st_.key_shift, wp.data());
+            pool.n = v.n;
+        } else {
+            OutSpec spec;
+            spec.shift = st_.key_shift;
+            spec.key_mode = 1;
+            spec.n_out = r.arity;
+            for (u32 j = 0; j < r.arity; ++j) spec.col[j] = SlotRef{v.cols[j].get(), 0};
+            push(spec, owner_filter(SlotRef{v.cols[kc].get(), 0}));
+            for (u32 w = 0; w < W; ++w) spec.keys[w] = pool.words[w].get();
+            spec.d_count = c_->d_scalars + 20;
+            FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
+            engine_project(c_, v.n, spec);
+            c_->read_scalars(spec.d_count, &pool.n, 1);
+        }
+        dedup_merge(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool);
+    }
+
+    // Forward the new home Δ rows to the relation's other partition copies.
+    void forward_delta(RelState& r) {
+        for (u32 kc : r.keyset) {
+            if (kc == 0) continue;
+            std::vector<const u32*> in;
+            std::vector<DBuf<u32>> send;
+            std::vector<u32*> outp;
+            for (u32 j = 0; j < r.arity; ++j) {
+                in.push_back(r.delta.cols[j].get());
+                send.emplace_back(c_, r.delta.n);
+                outp.push_back(send.back().get());
+            }
+            RouteKey rk;
+            rk.col = r.delta.cols[kc].get();
+            std::vector<u64> cnt(world_), off(world_);
+            engine_route(c_, r.delta.n, rk, world_, in, outp, {}, {}, cnt.data(), off.data());
+            std::vector<DBuf<u32>> recv;
+            const u64 n = exchange(send, cnt, off, recv);
+            CandPool pool;
+            pool.arity = r.arity;
+            pool.reserve(c_, n);
+            std::vector<const u32*> rp;
+            for (auto& b : recv) rp.push_back(b.get());
+            std::vector<u64*> wp;
+            for (auto& w : pool.words) wp.push_back(w.get());
+            engine_pack_keys(c_, rp, n, st_.key_shift, wp.data());
+            pool.n = n;
+            RelCopy& cp = *r.copies.at(kc);
+            dedup_merge(cp.full, cp.delta, cp.indexes, r.arity, pool);
+        }
+    }
+
+    void allreduce(std::vector<u64>& v) {
+        if (dist() && !v.empty()) c_->tx->allreduce_sum(c_, v.data(), static_cast<int>(v.size()));
+    }
+    u32 world() const { return world_; }
+    u32 rank() const { return rank_; }
 
 private:
     Ctx* c_;
     EvalState& st_;
+    u32 world_ = 1, rank_ = 0;
 };
 
 }  // namespace
@@ -408,6 +623,29 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         r->delta.cols.resize(d.arity);
         st->relations[d.name] = std::move(r);
     }
+    Engine eng(c, *st);
+    st->rank = static_cast<int>(eng.rank());
+    st->world = static_cast<int>(eng.world());
+    // Partition copies each IDB relation needs (static in the plans).
+    if (eng.dist()) {
+        for (auto& [name, r] : st->relations)
+            if (r->idb) r->keyset.insert(0);
+        for (auto& p : plans) {
+            const DistPlan dp = dist_plan(p, idb);
+            for (u32 s = 0; s < p.sources.size(); ++s) {
+                RelState& r = *st->relations.at(p.sources[s].relation);
+                if (r.idb) r.keyset.insert(dp.src_copy[s]);
+            }
+        }
+        for (auto& [name, r] : st->relations)
+            for (u32 kc : r->keyset)
+                if (kc != 0) {
+                    auto cp = std::make_unique<RelCopy>();
+                    cp->full.cols.resize(r->arity);
+                    cp->delta.cols.resize(r->arity);
+                    r->copies.emplace(kc, std::move(cp));
+                }
+    }
 
     // ---- gather the resident EDB blocks, key shift from the active domain ----
     std::map<std::string, std::vector<const DevVersion*>> by_rel;
@@ -455,22 +693,23 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
             vmax = std::max(vmax, m);
         }
     }
+    if (eng.dist()) {  // every rank must pack keys with the same shift
+        std::vector<u64> bits(64, 0);
+        bits[bit_width_u64(vmax)] = 1;
+        eng.allreduce(bits);
+        for (u32 b = 0; b < 64; ++b)
+            if (bits[b]) vmax = std::max<u64>(vmax, b ? (u64(1) << (b - 1)) : 0);
+    }
     st->key_shift = std::max<u32>(1, bit_width_u64(vmax));
 
-    Engine eng(c, *st);
     // ---- seed: FULL = DELTA = dedup(EDB) (engine.cpp:148-161) ---------------
     for (auto& [name, vp] : raw) {
-        const DevVersion& v = *vp;
         RelState& r = *st->relations[name];
-        CandPool pool;
-        pool.arity = r.arity;
-        pool.reserve(c, v.n);
-        std::vector<u64*> wp;
-        for (auto& w : pool.words) wp.push_back(w.get());
-        engine_pack_keys(c, v.ptrs(), v.n, st->key_shift, wp.data());
-        pool.n = v.n;
-        eng.dedup_merge(r, pool);  // FULL empty: C = D = distinct rows
-        // DELTA must equal FULL; the merge produced two identical copies.
+        if (eng.partitioned(r)) {
+            for (u32 kc : r.keyset) eng.seed_copy(r, *vp, kc);
+        } else {
+            eng.seed_copy(r, *vp, 0);  // FULL empty: C = D = distinct rows
+        }
     }
     raw.clear();
     concat.clear();
@@ -479,16 +718,20 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     struct Variant {
         const Plan* plan;
         long delta_source;
+        size_t plan_index;
     };
+    std::vector<DistPlan> dplans;
+    for (auto& p : plans) dplans.push_back(dist_plan(p, idb));
     std::vector<Variant> variants;
-    for (auto& p : plans) {
+    for (size_t i = 0; i < plans.size(); ++i) {
+        const Plan& p = plans[i];
         bool any = false;
         for (size_t s = 0; s < p.sources.size(); ++s)
             if (idb.count(p.sources[s].relation)) {
-                variants.push_back({&p, static_cast<long>(s)});
+                variants.push_back({&p, static_cast<long>(s), i});
                 any = true;
             }
-        if (!any) variants.push_back({&p, -1});
+        if (!any) variants.push_back({&p, -1, i});
     }
 
     // ---- fixpoint (engine.cpp:163-239) ---------------------------------------
@@ -499,15 +742,26 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         for (auto& v : variants) pooled[v.plan->head].arity = v.plan->head_arity;
         for (auto& v : variants) {
             if (v.delta_source < 0 && iteration != 0) continue;
-            eng.exec_variant(*v.plan, v.delta_source, pooled[v.plan->head]);
+            eng.exec_variant(*v.plan, dplans[v.plan_index], v.delta_source, pooled[v.plan->head]);
         }
-        bool any_delta = false;
-        std::vector<IterStat> its;
+        std::vector<u64> counts;  // per head: |Δ|, |FULL| (local, then global)
         for (auto& [name, pool] : pooled) {
             RelState& r = *st->relations.at(name);
-            const u64 nd = eng.dedup_merge(r, pool);
+            if (eng.dist()) eng.route_pool(pool);
+            const u64 nd = eng.dedup_merge_home(r, pool);
+            if (eng.dist()) eng.forward_delta(r);
+            counts.push_back(nd);
+            counts.push_back(r.full.n);
+        }
+        eng.allreduce(counts);
+        bool any_delta = false;
+        std::vector<IterStat> its;
+        size_t k = 0;
+        for (auto& [name, pool] : pooled) {
+            const u64 nd = counts[2 * k], nf = counts[2 * k + 1];
+            ++k;
             if (nd) any_delta = true;
-            its.push_back({iteration, name, nd, r.full.n, 1, 0.0});
+            its.push_back({iteration, name, nd, nf, 1, 0.0});
         }
         const double ms = ms_since(ti);
         for (auto& s : its) {
@@ -521,6 +775,49 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     c->sync();
     st->elapsed_ms = ms_since(t0);
     return st;
+}
+
+std::vector<std::unique_ptr<EvalState>> evaluate_sharded(Ctx* base, u32 world, const std::vector<RelationDecl>& decls,
+                                                         const std::vector<Plan>& plans,
+                                                         const std::vector<FactsBlock>& facts) {
+    if (world == 0 || world > 64) fail(FV_ERR_INVALID, "evaluate_sharded: world must be in [1, 64]");
+    check_plans(decls, plans);
+    auto group = make_local_group(static_cast<int>(world));
+    std::vector<Ctx*> ctxs(world, nullptr);
+    std::vector<std::unique_ptr<EvalState>> out(world);
+    std::vector<std::exception_ptr> errs(world);
+    try {
+        for (u32 r = 0; r < world; ++r) {
+            ctxs[r] = ctx_new(base->device);
+            ctxs[r]->tx = group[r].get();
+        }
+        std::vector<std::thread> threads;
+        for (u32 r = 0; r < world; ++r)
+            threads.emplace_back([&, r] {
+                try {
+                    ctxs[r]->activate();
+                    out[r] = evaluate(ctxs[r], decls, plans, facts);
+                } catch (...) {
+                    errs[r] = std::current_exception();
+                }
+            });
+        for (auto& t : threads) t.join();
+    } catch (...) {
+        for (auto* c : ctxs)
+            if (c) ctx_delete(c);
+        throw;
+    }
+    for (u32 r = 0; r < world; ++r) {
+        ctxs[r]->tx = nullptr;
+        if (out[r]) {
+            out[r]->owned_ctx = ctxs[r];
+        } else {
+            ctx_delete(ctxs[r]);
+        }
+    }
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    return out;
 }
 
 std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel) {

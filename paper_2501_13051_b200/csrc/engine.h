@@ -18,6 +18,7 @@
 
 #include <map>
 #include <memory>
+#include <set>
 #include <string>
 #include <utility>
 #include <vector>
@@ -94,13 +95,26 @@ struct JoinIndex {
     HashIndex ht;
 };
 
+using IndexMap = std::map<std::pair<int, u32>, std::unique_ptr<JoinIndex>>;
+
+// A partition copy of a relation keyed on a column other than 0 (partitioned
+// evaluation only): the rows whose owner(hash(row[col])) is this rank.
+struct RelCopy {
+    DevVersion full, delta;
+    IndexMap indexes;
+};
+
 struct RelState {
     std::string name;
     u32 arity = 0;
     bool idb = false;
+    // Home copy: all rows (single GPU) or the rows owned by hash(col 0).
     DevVersion full, delta;
     // (0 = full, 1 = delta, col) -> index; invalidated when the version changes
-    std::map<std::pair<int, u32>, std::unique_ptr<JoinIndex>> indexes;
+    IndexMap indexes;
+    // Partitioned evaluation: extra copies keyed on other probed columns.
+    std::map<u32, std::unique_ptr<RelCopy>> copies;
+    std::set<u32> keyset;  // partition columns this relation is needed on
 };
 
 struct IterStat {
@@ -114,9 +128,15 @@ struct EvalState {
     Ctx* ctx = nullptr;
     std::map<std::string, std::unique_ptr<RelState>> relations;  // std::map order
     u64 iterations = 0;
-    std::vector<IterStat> stats;
+    std::vector<IterStat> stats;  // global (all-reduced) counts in a partitioned run
     double elapsed_ms = 0.0;
     u32 key_shift = 32;
+    int rank = 0, world = 1;  // this state's partition
+    Ctx* owned_ctx = nullptr;  // virtual-rank context owned by the state
+    ~EvalState() {
+        relations.clear();
+        if (owned_ctx) ctx_delete(owned_ctx);
+    }
 };
 
 // EDB resident in HBM (unsorted, possibly duplicated rows, per relation).
@@ -136,6 +156,25 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
                                            const std::vector<Plan>& plans,
                                            const std::vector<const DeviceEdb*>& edbs);
 
+// Partitioned evaluation with `world` virtual ranks on c's device (threads,
+// in-process transport): the distributed code path on one GPU. Returns one
+// state per rank (home partitions; stats are global).
+std::vector<std::unique_ptr<EvalState>> evaluate_sharded(Ctx* c, u32 world, const std::vector<RelationDecl>& decls,
+                                                         const std::vector<Plan>& plans,
+                                                         const std::vector<FactsBlock>& facts);
+
+// Static partitioning decisions for one rule plan (partitioned evaluation):
+//   src_copy[s]      partition column source s is read from (IDB sources)
+//   shuffle[k]       shuffle the intermediate by joins[k].left before step k
+//   replicated_out   the derivation only touches replicated (EDB) relations:
+//                    its head rows are owner-filtered instead of routed
+struct DistPlan {
+    std::vector<u32> src_copy;
+    std::vector<u8> shuffle;
+    bool replicated_out = false;
+};
+DistPlan dist_plan(const Plan& p, const std::set<std::string>& idb);
+
 // Validate plan structure against the declarations (throws FV_ERR_PLAN).
 void check_plans(const std::vector<RelationDecl>& decls, const std::vector<Plan>& plans);
 
@@ -154,12 +193,13 @@ struct SlotRef {
     u32 side = 0;  // 0: probe-side row i, 1: build-side position p
 };
 
-enum FilterOp : u32 { kFilterEq = 0, kFilterNeq = 1, kFilterConst = 2 };
+enum FilterOp : u32 { kFilterEq = 0, kFilterNeq = 1, kFilterConst = 2, kFilterOwner = 3 };
 
 struct Filter {
     SlotRef a, b;
     u32 op = kFilterEq;
-    u32 value = 0;  // kFilterConst
+    u32 value = 0;  // kFilterConst: the constant; kFilterOwner: this rank
+    u32 world = 1;  // kFilterOwner: owner(a) = floor(hash32(a) * world / 2^32) must equal value
 };
 
 struct OutSpec {
@@ -202,6 +242,21 @@ void engine_merge(Ctx* c, const std::vector<const u32*>& a_cols, u64 n_a, u64* c
                   u32 arity, u32 shift, const std::vector<u32*>& c_cols,
                   const std::vector<u32*>& d_cols, u64* d_new);
 u64 engine_fingerprint(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 arity);
+
+// Destination rank of a row: owner(hash32(v)) where v is a u32 column value
+// or the high/low half of a packed key word.
+struct RouteKey {
+    const u32* col = nullptr;   // u32 column, or
+    const u64* word = nullptr;  // packed key word: v = hi ? word >> shift : word
+    u32 shift = 0;
+    u32 hi = 0;
+};
+// Group n rows by destination rank: u32 columns `c32` and u64 columns `c64`
+// are scattered into the matching *_out buffers (capacity n) so that rows for
+// rank p occupy [off[p], off[p] + cnt[p]) (order inside a bucket unspecified).
+void engine_route(Ctx* c, u64 n, const RouteKey& key, u32 world, const std::vector<const u32*>& c32,
+                  const std::vector<u32*>& c32_out, const std::vector<const u64*>& c64,
+                  const std::vector<u64*>& c64_out, u64* cnt, u64* off);
 // Sort W-word keys in place (LSD over words with a permutation payload).
 void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift);
 

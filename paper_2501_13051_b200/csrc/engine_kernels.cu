@@ -38,6 +38,8 @@ __device__ __forceinline__ bool pass_filters(const Filter* f, u32 n, u64 i, u64 
         const u32 a = slot(f[k].a, i, p);
         if (f[k].op == kFilterConst) {
             if (a != f[k].value) return false;
+        } else if (f[k].op == kFilterOwner) {
+            if (static_cast<u32>((static_cast<u64>(hash32(a)) * f[k].world) >> 32) != f[k].value) return false;
         } else {
             const u32 b = slot(f[k].b, i, p);
             if ((a == b) != (f[k].op == kFilterEq)) return false;
@@ -138,24 +140,33 @@ __device__ __forceinline__ u32 block_excl_u32(u32 v, u32* s_warp, u32* total) {
     return r;
 }
 
+// First and last source row of every output tile (parallel binary searches).
+__global__ void tile_rows_kernel(const u64* __restrict__ offsets, u64 m, u64 total, u64 tiles,
+                                 u64* __restrict__ jlo, u64* __restrict__ jhi) {
+    GRID_STRIDE(b, tiles) {
+        const u64 o0 = b * kMatTile;
+        const u64 o_end = min(o0 + kMatTile, total);
+        jlo[b] = upper_bound_u64(offsets, m + 1, o0) - 1;
+        jhi[b] = upper_bound_u64(offsets, m + 1, o_end - 1) - 1;
+    }
+}
+
 // Output-partitioned join expansion (see lbs_kernel in column_ops.cu).
 template <bool COMPACT>
 __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __restrict__ offsets, u64 m,
                                                                  u64 total, const u32* __restrict__ starts,
+                                                                 const u64* __restrict__ tile_jlo,
+                                                                 const u64* __restrict__ tile_jhi,
                                                                  OutSpec spec) {
     __shared__ u32 s_owner[kMatTile];
-    __shared__ u64 s_jlo, s_jhi, s_base;
+    __shared__ u64 s_base;
     __shared__ u32 s_warp[kMatBlock / 32 + 1];
     const u32 tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const u64 o0 = u64(blockIdx.x) * kMatTile;
     const u64 o_end = min(o0 + kMatTile, total);
-    if (tid == 0) {
-        s_jlo = upper_bound_u64(offsets, m + 1, o0) - 1;
-        s_jhi = upper_bound_u64(offsets, m + 1, o_end - 1) - 1;
-    }
     for (u32 i = tid; i < kMatTile; i += kMatBlock) s_owner[i] = 0;
     __syncthreads();
-    const u64 jlo = s_jlo, jhi = s_jhi;
+    const u64 jlo = tile_jlo[blockIdx.x], jhi = tile_jhi[blockIdx.x];
     for (u64 j = jlo + 1 + tid; j <= jhi; j += kMatBlock)
         atomicMax(&s_owner[offsets[j] - o0], static_cast<u32>(j - jlo));
     __syncthreads();
@@ -389,15 +400,33 @@ __device__ u64 merge_path_global(const Cols8& a, u32 arity, u32 shift, u64 n_a, 
     return lo;
 }
 
+// Merge-path split of every tile boundary, one thread per boundary (all
+// binary searches in parallel instead of serially inside each merge CTA).
+template <int W>
+__global__ void merge_partition_kernel(Cols8 a, u64 n_a, Words4 b, u64 n_b, u32 arity, u32 shift, u64 tiles,
+                                       u64* __restrict__ splits) {
+    constexpr int TILE = MergeTraits<W>::kTile;
+    GRID_STRIDE(t, tiles + 1) {
+        const u64 d = min(u64(t) * TILE, n_a + n_b);
+        splits[t] = merge_path_global<W>(a, arity, shift, n_a, b, n_b, d);
+    }
+}
+
 template <int W>
 __global__ void __launch_bounds__(MergeTraits<W>::kBlock)
     merge_kernel(Cols8 a, u64 n_a, Words4 b, u64 n_b, u32 arity, u32 shift, OutCols8 cout, OutCols8 dout,
-                 u64* __restrict__ status, u32 epoch, u32* __restrict__ tile_counter, u64* __restrict__ d_new) {
+                 const u64* __restrict__ splits, u64* __restrict__ status, u32 epoch, u32* __restrict__ tile_counter,
+                 u64* __restrict__ d_new) {
     constexpr int ITEMS = MergeTraits<W>::kItems;
     constexpr int BLOCK = MergeTraits<W>::kBlock;
     constexpr int TILE = MergeTraits<W>::kTile;
-    __shared__ Key<W> s_keys[TILE];  // inputs: A part then B part; later C outputs
-    __shared__ Key<W> s_dout[TILE];
+    // Padded tiles (one slot per 16): each thread walks its own stretch of
+    // the merge, so lanes access keys ~ITEMS apart; without padding those
+    // strided u64 accesses hit the same banks (16-way conflicts).
+    constexpr int PADDED = TILE + TILE / 16;
+    __shared__ Key<W> s_keys[PADDED];  // inputs: A part then B part; later C outputs
+    __shared__ Key<W> s_dout[PADDED];
+    auto pad = [](u32 i) { return i + (i >> 4); };
     __shared__ u32 s_tile;
     __shared__ u64 s_a0, s_a1, s_dups_before;
     __shared__ Key<W> s_prev;
@@ -412,8 +441,8 @@ __global__ void __launch_bounds__(MergeTraits<W>::kBlock)
     const u64 d0 = u64(tile) * TILE;
     const u64 d1 = min(d0 + TILE, total);
     if (tid == 0) {
-        const u64 a0 = merge_path_global<W>(a, arity, shift, n_a, b, n_b, d0);
-        const u64 a1 = merge_path_global<W>(a, arity, shift, n_a, b, n_b, d1);
+        const u64 a0 = splits[tile];
+        const u64 a1 = splits[tile + 1];
         s_a0 = a0;
         s_a1 = a1;
         const u64 b0 = d0 - a0;
@@ -435,10 +464,10 @@ __global__ void __launch_bounds__(MergeTraits<W>::kBlock)
     const u64 a0 = s_a0, a1 = s_a1;
     const u64 b0 = d0 - a0, b1 = d1 - a1;
     const u32 na = static_cast<u32>(a1 - a0), nb = static_cast<u32>(b1 - b0);
-    Key<W>* sA = s_keys;
-    Key<W>* sB = s_keys + na;
-    for (u32 j = tid; j < na; j += BLOCK) sA[j] = load_a<W>(a, arity, a0 + j, shift);
-    for (u32 j = tid; j < nb; j += BLOCK) sB[j] = load_b<W>(b, b0 + j);
+#define SA(i) s_keys[pad(i)]
+#define SB(j) s_keys[pad(na + (j))]
+    for (u32 j = tid; j < na; j += BLOCK) SA(j) = load_a<W>(a, arity, a0 + j, shift);
+    for (u32 j = tid; j < nb; j += BLOCK) SB(j) = load_b<W>(b, b0 + j);
     __syncthreads();
 
     // Thread-level merge path inside the tile.
@@ -447,7 +476,7 @@ __global__ void __launch_bounds__(MergeTraits<W>::kBlock)
     u32 lo = t0 > nb ? t0 - nb : 0, hi = min(t0, na);
     while (lo < hi) {
         const u32 mid = (lo + hi) >> 1;
-        if (key_le<W>(sA[mid], sB[t0 - 1 - mid])) lo = mid + 1;
+        if (key_le<W>(SA(mid), SB(t0 - 1 - mid))) lo = mid + 1;
         else hi = mid;
     }
     u32 ai = lo, bi = t0 - lo;
@@ -458,17 +487,17 @@ __global__ void __launch_bounds__(MergeTraits<W>::kBlock)
         if (has_prev) prev = s_prev;
     } else {
         has_prev = true;
-        if (ai > 0 && bi > 0) prev = key_le<W>(sA[ai - 1], sB[bi - 1]) ? sB[bi - 1] : sA[ai - 1];
-        else if (ai > 0) prev = sA[ai - 1];
-        else prev = sB[bi - 1];
+        if (ai > 0 && bi > 0) prev = key_le<W>(SA(ai - 1), SB(bi - 1)) ? SB(bi - 1) : SA(ai - 1);
+        else if (ai > 0) prev = SA(ai - 1);
+        else prev = SB(bi - 1);
     }
     Key<W> item[ITEMS];
     u32 valid = 0, from_b = 0, dup = 0;
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         if (t0 + k < len) {
-            const bool take_a = bi >= nb || (ai < na && key_le<W>(sA[ai], sB[bi]));
-            const Key<W> key = take_a ? sA[ai] : sB[bi];
+            const bool take_a = bi >= nb || (ai < na && key_le<W>(SA(ai), SB(bi)));
+            const Key<W> key = take_a ? SA(ai) : SB(bi);
             if (take_a) ++ai;
             else ++bi;
             valid |= 1u << k;
@@ -508,15 +537,18 @@ __global__ void __launch_bounds__(MergeTraits<W>::kBlock)
     for (int k = 0; k < ITEMS; ++k) {
         const u32 bit = 1u << k;
         if ((valid & bit) && !(dup & bit)) {
-            s_keys[cpos++] = item[k];
-            if (from_b & bit) s_dout[dpos++] = item[k];
+            s_keys[pad(cpos++)] = item[k];
+            if (from_b & bit) s_dout[pad(dpos++)] = item[k];
         }
     }
     __syncthreads();
+#undef SA
+#undef SB
     const u64 c_base = d0 - dups_before;
     const u64 d_base = b0 - dups_before;
-    for (u32 j = tid; j < tile_nondup; j += BLOCK) store_row<W>(cout, arity, shift, c_base + j, s_keys[j]);
-    for (u32 j = tid; j < tile_nondup_b; j += BLOCK) store_row<W>(dout, arity, shift, d_base + j, s_dout[j]);
+    for (u32 j = tid; j < tile_nondup; j += BLOCK) store_row<W>(cout, arity, shift, c_base + j, s_keys[pad(j)]);
+    for (u32 j = tid; j < tile_nondup_b; j += BLOCK)
+        store_row<W>(dout, arity, shift, d_base + j, s_dout[pad(j)]);
     if (tid == 0 && d1 == total) *d_new = d_base + tile_nondup_b;
 }
 
@@ -536,6 +568,55 @@ __global__ void fingerprint_kernel(Cols8 c, u32 arity, u64 n, unsigned long long
 }  // namespace
 
 namespace {
+
+constexpr int kMaxRanks = 64;
+
+__device__ __forceinline__ u32 route_dest(const RouteKey& k, u64 i, u32 world) {
+    u32 v;
+    if (k.col) v = k.col[i];
+    else v = static_cast<u32>(k.hi ? (k.word[i] >> k.shift) : k.word[i]);
+    return static_cast<u32>((static_cast<u64>(hash32(v)) * world) >> 32);
+}
+
+__global__ void route_count_kernel(RouteKey key, u64 n, u32 world, unsigned long long* counts) {
+    __shared__ u32 s_cnt[kMaxRanks];
+    for (u32 p = threadIdx.x; p < world; p += blockDim.x) s_cnt[p] = 0;
+    __syncthreads();
+    GRID_STRIDE(i, n) atomicAdd(&s_cnt[route_dest(key, i, world)], 1u);
+    __syncthreads();
+    for (u32 p = threadIdx.x; p < world; p += blockDim.x)
+        if (s_cnt[p]) atomicAdd(counts + p, static_cast<unsigned long long>(s_cnt[p]));
+}
+
+__global__ void route_scatter_kernel(RouteKey key, u64 n, u32 world, unsigned long long* cursor, Cols8 in32,
+                                     OutCols8 out32, u32 n32, Words4 in64, Words4 out64, u32 n64) {
+    __shared__ u32 s_cnt[kMaxRanks];
+    __shared__ u64 s_base[kMaxRanks];
+    constexpr int ITEMS = 8;
+    const u64 r0 = u64(blockIdx.x) * blockDim.x * ITEMS;
+    for (u32 p = threadIdx.x; p < world; p += blockDim.x) s_cnt[p] = 0;
+    __syncthreads();
+    u32 dest[ITEMS], rank[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 i = r0 + u64(k) * blockDim.x + threadIdx.x;
+        dest[k] = i < n ? route_dest(key, i, world) : 0;
+        rank[k] = i < n ? atomicAdd(&s_cnt[dest[k]], 1u) : 0;
+    }
+    __syncthreads();
+    for (u32 p = threadIdx.x; p < world; p += blockDim.x)
+        s_base[p] = s_cnt[p] ? atomicAdd(cursor + p, static_cast<unsigned long long>(s_cnt[p])) : 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 i = r0 + u64(k) * blockDim.x + threadIdx.x;
+        if (i >= n) continue;
+        const u64 pos = s_base[dest[k]] + rank[k];
+        for (u32 j = 0; j < n32; ++j) out32.p[j][pos] = in32.p[j][i];
+        for (u32 j = 0; j < n64; ++j) out64.p[j][pos] = in64.p[j][i];
+    }
+}
+
 struct SelectRowsOp {
     RowFilter pred;
     u32* ids;
@@ -560,6 +641,11 @@ u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids) {
 void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, const RowFilter& pred,
                         u32* starts, u32* counts) {
     if (!n) return;
+    if (idx.n_unique == 0) {  // empty build side: every probe misses
+        FV_CUDA(cudaMemsetAsync(counts, 0, 4 * n, c->stream));
+        FV_CUDA(cudaMemsetAsync(starts, 0, 4 * n, c->stream));
+        return;
+    }
     ProfScope prof(c, "join_probe_count", double(n) * 20.0);
     probe_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(probe, n, idx.ht.slots.get(), idx.ht.mask,
                                                             idx.ustart.get(), idx.ucount.get(), pred,
@@ -581,15 +667,19 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
         if (spec.f[k].op != kFilterConst) (spec.f[k].b.side ? side1 : side0) += 4;
     }
     const double out_bytes = spec.key_mode ? 8.0 * ((spec.n_out + 1) / 2) : 4.0 * spec.n_out;
+    DBuf<u64> rows(c, 2 * tiles);
+    tile_rows_kernel<<<grid_for(tiles), 256, 0, c->stream>>>(offsets, m, total, tiles, rows.get(),
+                                                             rows.get() + tiles);
+    FV_CUDA(cudaGetLastError());
     ProfScope prof(c, "join_materialize", double(m) * (12.0 + side0) + double(total) * (side1 + out_bytes));
     if (spec.n_filters)
-        materialize_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(offsets, m, total,
-                                                                                           starts, spec);
+        materialize_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(
+            offsets, m, total, starts, rows.get(), rows.get() + tiles, spec);
     else
-        materialize_kernel<false><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(offsets, m, total,
-                                                                                            starts, spec);
+        materialize_kernel<false><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(
+            offsets, m, total, starts, rows.get(), rows.get() + tiles, spec);
     FV_CUDA(cudaGetLastError());
-    c->count_launch();
+    c->count_launch(2);
 }
 
 void engine_project(Ctx* c, u64 n, const OutSpec& spec) {
@@ -655,11 +745,18 @@ static void merge_launch(Ctx* c, const Cols8& a, u64 n_a, const Words4& b, u64 n
     const u32 epoch = c->lookback_epoch(tiles, &counter);
     // Reads FULL and the candidates once, rewrites FULL; the 2 x |DELTA| row
     // writes are added by the caller once |DELTA| is known (prof_add_bytes).
+    DBuf<u64> splits(c, tiles + 1);
+    {
+        ProfScope prof(c, "merge_partition", double(tiles + 1) * 8.0);
+        merge_partition_kernel<W><<<grid_for(tiles + 1), 256, 0, c->stream>>>(a, n_a, b, n_b, arity, shift, tiles,
+                                                                              splits.get());
+        FV_CUDA(cudaGetLastError());
+    }
     ProfScope prof(c, "merge_dedup", 8.0 * double(n_a) * arity + 8.0 * W * double(n_b));
     merge_kernel<W><<<static_cast<unsigned>(tiles), MergeTraits<W>::kBlock, 0, c->stream>>>(
-        a, n_a, b, n_b, arity, shift, co, dout, c->lb.status, epoch, counter, d_new);
+        a, n_a, b, n_b, arity, shift, co, dout, splits.get(), c->lb.status, epoch, counter, d_new);
     FV_CUDA(cudaGetLastError());
-    c->count_launch();
+    c->count_launch(2);
 }
 
 void engine_merge(Ctx* c, const std::vector<const u32*>& a_cols, u64 n_a, u64* const* b_words, u64 n_b,
@@ -690,6 +787,47 @@ void engine_merge(Ctx* c, const std::vector<const u32*>& a_cols, u64 n_a, u64* c
         case 4: merge_launch<4>(c, a, n_a, b, n_b, arity, shift, co, dout, d_new); break;
         default: fail(FV_ERR_ARITY, "arity exceeds FV_MAX_ARITY");
     }
+}
+
+void engine_route(Ctx* c, u64 n, const RouteKey& key, u32 world, const std::vector<const u32*>& c32,
+                  const std::vector<u32*>& c32_out, const std::vector<const u64*>& c64,
+                  const std::vector<u64*>& c64_out, u64* cnt, u64* off) {
+    if (world > static_cast<u32>(kMaxRanks)) fail(FV_ERR_INVALID, "more than 64 ranks");
+    if (c32.size() > FV_MAX_ARITY || c64.size() > 4) fail(FV_ERR_INVALID, "route: too many columns");
+    DBuf<u64> d(c, 2 * world);
+    FV_CUDA(cudaMemsetAsync(d.get(), 0, 16 * world, c->stream));
+    if (n) {
+        ProfScope prof(c, "route_count", double(n) * 4.0);
+        route_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(key, n, world,
+                                                                reinterpret_cast<unsigned long long*>(d.get()));
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+    }
+    d.download(cnt, world);
+    u64 run = 0;
+    for (u32 p = 0; p < world; ++p) {
+        off[p] = run;
+        run += cnt[p];
+    }
+    if (!n) return;
+    d.upload(off, world, world);  // cursors start at the bucket offsets
+    Cols8 i32{};
+    OutCols8 o32{};
+    Words4 i64{}, o64{};
+    for (size_t j = 0; j < c32.size(); ++j) {
+        i32.p[j] = c32[j];
+        o32.p[j] = c32_out[j];
+    }
+    for (size_t j = 0; j < c64.size(); ++j) {
+        i64.p[j] = const_cast<u64*>(c64[j]);
+        o64.p[j] = c64_out[j];
+    }
+    ProfScope prof(c, "route_scatter", double(n) * 2.0 * (4.0 * c32.size() + 8.0 * c64.size()));
+    route_scatter_kernel<<<static_cast<unsigned>(ceil_div(n, 256 * 8)), 256, 0, c->stream>>>(
+        key, n, world, reinterpret_cast<unsigned long long*>(d.get() + world), i32, o32,
+        static_cast<u32>(c32.size()), i64, o64, static_cast<u32>(c64.size()));
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
 }
 
 u64 engine_fingerprint(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 arity) {

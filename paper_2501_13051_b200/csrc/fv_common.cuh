@@ -64,8 +64,13 @@ struct ProfAgg {
     double bytes = 0.0;  // algorithmic bytes (implementation-independent)
 };
 
+class Transport;
+
 struct Ctx {
     int device = 0;
+    // Row exchange with the other ranks of a partitioned evaluation
+    // (transport.h); null for a single-GPU evaluation. Not owned.
+    Transport* tx = nullptr;
     bool prof = false;
     struct ProfRec {
         const char* name;

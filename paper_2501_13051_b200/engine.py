@@ -85,6 +85,13 @@ def _bind():
     B("fv_run", C.c_int, [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p,
                           C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)])
     B("fv_free", None, [C.c_void_p])
+    B("fv_evaluate_program_sharded", C.c_int, [vp, vp, C.POINTER(fv_facts), C.c_uint32, C.c_uint32,
+                                               C.POINTER(vp)])
+    B("fv_state_partition", C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)])
+    B("fv_program_partition_plan", C.c_int, [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)])
+    B("fv_owner", C.c_uint32, [C.c_uint32, C.c_uint32])
+    B("fv_nccl_unique_id", C.c_int, [C.c_void_p])
+    B("fv_ctx_set_nccl", C.c_int, [vp, C.c_int, C.c_int, C.c_void_p])
     _bound = True
 
 
@@ -237,6 +244,15 @@ class Program:
         check(self.l.fv_program_encode(self.h, s.encode(), C.byref(v)))
         return v.value
 
+    def partition_plan(self) -> dict:
+        """Static partitioning decisions of the multi-GPU engine (dist_plan)."""
+        import json
+        ln = C.c_size_t()
+        check(self.l.fv_program_partition_plan(self.h, None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value + 1)
+        check(self.l.fv_program_partition_plan(self.h, buf, ln.value + 1, C.byref(ln)))
+        return json.loads(buf.value.decode())
+
     # -- oracle adaptor (test infrastructure consumes this; plain data only) --
     def relation_index(self, name: str) -> int:
         return [r for r, _ in self.relations()].index(name)
@@ -370,6 +386,41 @@ def evaluate_program(program, facts: Dict[str, np.ndarray], ctx: Optional[Contex
     check(c._lib.fv_evaluate_program(c.h, prog.h, arr, n, C.byref(h)), c.h)
     del keep
     return State(c, h.value)
+
+
+def evaluate_program_sharded(program, facts: Dict[str, np.ndarray], world: int,
+                             ctx: Optional[Context] = None) -> List[State]:
+    """Hash-partitioned evaluation with `world` virtual ranks on one GPU (the
+    multi-GPU code path with an in-process transport). Returns one State per
+    rank holding that rank's home partition; stats are global."""
+    _bind()
+    c = _ctx(ctx)
+    prog = program if isinstance(program, Program) else Program(program)
+    arr, n, keep = _facts_array(facts, dict(prog.relations()))
+    hs = (vp * world)()
+    check(c._lib.fv_evaluate_program_sharded(c.h, prog.h, arr, n, world, hs), c.h)
+    del keep
+    return [State(c, hs[r]) for r in range(world)]
+
+
+def owner(v: int, world: int) -> int:
+    """Rank owning value v in a partitioned evaluation."""
+    _bind()
+    return int(_lib.lib().fv_owner(v, world))
+
+
+def nccl_unique_id() -> bytes:
+    _bind()
+    buf = C.create_string_buffer(128)
+    check(_lib.lib().fv_nccl_unique_id(buf))
+    return buf.raw
+
+
+def set_nccl(ctx: Context, rank: int, world: int, uid: bytes) -> None:
+    """Make later evaluations on ctx hash-partitioned over NCCL."""
+    _bind()
+    b = C.create_string_buffer(uid, 128)
+    check(ctx._lib.fv_ctx_set_nccl(ctx.h, rank, world, b), ctx.h)
 
 
 def evaluate(decls: Sequence[Tuple[str, int]], plans: Sequence[RulePlan], facts: Dict[str, np.ndarray],
