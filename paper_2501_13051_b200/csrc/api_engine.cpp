@@ -461,7 +461,7 @@ fv_status fv_state_relation(const fv_state* s, uint64_t i, const char** name, ui
     const auto& r = *s->st->relations.at(s->names[i]);
     if (name) *name = s->names[i].c_str();
     if (arity) *arity = r.arity;
-    if (rows) *rows = r.full.n;
+    if (rows) *rows = r.rows();
     FV_API_END
 }
 

@@ -34,6 +34,8 @@
 // same sequence (no data-dependent early exits in partitioned mode).
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <exception>
 #include <set>
 #include <thread>
@@ -77,6 +79,15 @@ struct Inter {
     u64 n = 0;
     std::map<ColRef, const u32*> cols;
     std::vector<DBuf<u32>> owned;
+};
+
+// Per head relation per iteration in hash mode: the keys found new so far
+// (appended by the fused join kernel or by hash_insert over a pool).
+struct HeadSink {
+    DBuf<u64> keys;
+    u64 cap = 0;
+    u64 bound = 0;  // host upper bound of the device count
+    DBuf<u64> counter;
 };
 
 // Partition column of plan source s (the copy it is read from when its
@@ -281,7 +292,7 @@ public:
 
     // ---- execute_plan (P/src/engine.cpp:72-146) for one variant ------------------
 
-    void exec_variant(const Plan& plan, const DistPlan& dp, long delta_source, CandPool& out) {
+    void exec_variant(const Plan& plan, const DistPlan& dp, long delta_source, CandPool& out, HeadSink* sink) {
         const u32 ns = static_cast<u32>(plan.sources.size());
         const bool D = dist();
         std::vector<const DevVersion*> ver(ns);
@@ -357,6 +368,17 @@ public:
                 spec.key_mode = 1;
                 spec.n_out = plan.head_arity;
                 for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot_of(plan.output_cols[h]);
+                if (sink) {
+                    // Fused dedup: the join kernel inserts into FULL's key set.
+                    RelState& hr = rel(plan.head);
+                    hash_reserve(hr, *sink, T);
+                    spec.ht_slots = hr.keys.slots.get();
+                    spec.ht_mask = hr.keys.mask;
+                    spec.new_keys = sink->keys.get();
+                    spec.new_count = sink->counter.get();
+                    engine_materialize(c_, offsets.get(), n, T, starts.get(), spec);
+                    return;
+                }
                 out.reserve(c_, T);
                 for (u32 w = 0; w < W; ++w) spec.keys[w] = out.words[w].get() + out.n;
             } else {
@@ -454,6 +476,16 @@ public:
     // Seed one copy of a relation from raw EDB rows (owner-filtered on kc
     // when partitioned).
     void seed_copy(RelState& r, const DevVersion& v, u32 kc) {
+        CandPool pool = seed_pool(r, v, kc);
+        if (kc == 0 && r.hash_mode) {
+            HeadSink sink;
+            hash_finalize(r, sink, pool);
+            return;
+        }
+        dedup_merge(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool);
+    }
+
+    CandPool seed_pool(RelState& r, const DevVersion& v, u32 kc) {
         CandPool pool;
         pool.arity = r.arity;
         pool.reserve(c_, v.n);
@@ -476,7 +508,7 @@ public:
             engine_project(c_, v.n, spec);
             c_->read_scalars(spec.d_count, &pool.n, 1);
         }
-        dedup_merge(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool);
+        return pool;
     }
 
     // Forward the new home Δ rows to the relation's other partition copies.
@@ -509,6 +541,114 @@ public:
             RelCopy& cp = *r.copies.at(kc);
             dedup_merge(cp.full, cp.delta, cp.indexes, r.arity, pool);
         }
+    }
+
+    // ---- hash-mode dedup ---------------------------------------------------------
+
+    u64 sink_count(HeadSink& s) {
+        if (!s.counter.get()) return 0;
+        u64 n = 0;
+        c_->read_scalars(s.counter.get(), &n, 1);
+        s.bound = n;
+        return n;
+    }
+
+    // Room for `extra` more new keys in the sink and for count + extra keys
+    // in the relation's key set at load factor <= 1/2 (rehash when needed).
+    void hash_reserve(RelState& r, HeadSink& s, u64 extra) {
+        if (!s.counter.get()) {
+            s.counter = DBuf<u64>(c_, 1);
+            FV_CUDA(cudaMemsetAsync(s.counter.get(), 0, 8, c_->stream));
+        }
+        if (s.bound + extra > s.cap) {
+            const u64 have = sink_count(s);
+            const u64 nc = std::max<u64>(have + extra, 2 * s.cap);
+            DBuf<u64> nk(c_, nc);
+            if (have) FV_CUDA(cudaMemcpyAsync(nk.get(), s.keys.get(), 8 * have, cudaMemcpyDeviceToDevice, c_->stream));
+            s.keys = std::move(nk);
+            s.cap = nc;
+        }
+        s.bound += extra;
+        // bound counts every candidate as new, so the real load stays far
+        // below the 3/4 worst case the table is sized for.
+        if (4 * (r.keys.count + s.bound) <= 3 * r.keys.capacity()) return;
+        const u64 pending = sink_count(s);
+        u64 cap = 1u << 16;
+        while (cap < 2 * (r.keys.count + pending + extra)) cap <<= 1;
+        KeySet ns;
+        ns.slots = DBuf<u64>(c_, cap);
+        ns.mask = cap - 1;
+        ns.count = r.keys.count;
+        FV_CUDA(cudaMemsetAsync(ns.slots.get(), 0xff, 8 * cap, c_->stream));
+        // Re-insert FULL's rows and the keys already found new this iteration.
+        auto reinsert_rows = [&](const DevVersion& v) {
+            if (!v.n) return;
+            DBuf<u64> k(c_, v.n);
+            u64* kp = k.get();
+            engine_pack_keys(c_, v.ptrs(), v.n, st_.key_shift, &kp);
+            engine_hash_insert(c_, k.get(), v.n, ns, nullptr, nullptr);
+        };
+        if (r.levels_mode)
+            for (auto& lv : r.levels) reinsert_rows(lv);
+        else
+            reinsert_rows(r.full);
+        engine_hash_insert(c_, s.keys.get(), pending, ns, nullptr, nullptr);
+        r.keys = std::move(ns);
+    }
+
+    // Sort the iteration's new keys into Δ and fold them into FULL.
+    u64 hash_finalize(RelState& r, HeadSink& s, CandPool& pool) {
+        if (pool.n) {
+            hash_reserve(r, s, pool.n);
+            engine_hash_insert(c_, pool.words[0].get(), pool.n, r.keys, s.keys.get(), s.counter.get());
+        }
+        const u64 nd = sink_count(s);
+        r.indexes.clear();
+        DevVersion Dv;
+        Dv.n = nd;
+        for (u32 j = 0; j < r.arity; ++j) Dv.cols.emplace_back(c_, nd);
+        if (nd == 0) {
+            r.delta = std::move(Dv);
+            return 0;
+        }
+        r.keys.count += nd;
+        std::vector<DBuf<u64>> words;
+        words.push_back(std::move(s.keys));
+        s.cap = 0;
+        engine_sort_keys(c_, words, nd, r.arity, st_.key_shift);
+        std::vector<u32*> dc;
+        for (auto& col : Dv.cols) dc.push_back(col.get());
+        engine_unpack_keys(c_, words[0].get(), nd, r.arity, st_.key_shift, dc);
+        if (r.levels_mode) {
+            DevVersion lv;
+            lv.n = nd;
+            for (u32 j = 0; j < r.arity; ++j) {
+                lv.cols.emplace_back(c_, nd);
+                FV_CUDA(cudaMemcpyAsync(lv.cols[j].get(), Dv.cols[j].get(), 4 * nd, cudaMemcpyDeviceToDevice,
+                                        c_->stream));
+            }
+            r.levels.push_back(std::move(lv));
+            r.level_rows += nd;
+        } else {
+            // FULL is read by joins: keep it one sorted version.
+            DevVersion C, unused;
+            for (u32 j = 0; j < r.arity; ++j) {
+                C.cols.emplace_back(c_, r.full.n + nd);
+                unused.cols.emplace_back(c_, nd);
+            }
+            std::vector<u64*> bw{words[0].get()};
+            std::vector<u32*> cc, uc;
+            for (u32 j = 0; j < r.arity; ++j) {
+                cc.push_back(C.cols[j].get());
+                uc.push_back(unused.cols[j].get());
+            }
+            u64* d_new = c_->d_scalars + 23;
+            engine_merge(c_, r.full.ptrs(), r.full.n, bw.data(), nd, r.arity, st_.key_shift, cc, uc, d_new);
+            C.n = r.full.n + nd;
+            r.full = std::move(C);
+        }
+        r.delta = std::move(Dv);
+        return nd;
     }
 
     void allreduce(std::vector<u64>& v) {
@@ -702,18 +842,6 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     }
     st->key_shift = std::max<u32>(1, bit_width_u64(vmax));
 
-    // ---- seed: FULL = DELTA = dedup(EDB) (engine.cpp:148-161) ---------------
-    for (auto& [name, vp] : raw) {
-        RelState& r = *st->relations[name];
-        if (eng.partitioned(r)) {
-            for (u32 kc : r.keyset) eng.seed_copy(r, *vp, kc);
-        } else {
-            eng.seed_copy(r, *vp, 0);  // FULL empty: C = D = distinct rows
-        }
-    }
-    raw.clear();
-    concat.clear();
-
     // ---- variants (delta_rewrite, engine.cpp:57-64) --------------------------
     struct Variant {
         const Plan* plan;
@@ -723,6 +851,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     std::vector<DistPlan> dplans;
     for (auto& p : plans) dplans.push_back(dist_plan(p, idb));
     std::vector<Variant> variants;
+    std::set<std::string> full_read;  // relations whose FULL some variant reads
     for (size_t i = 0; i < plans.size(); ++i) {
         const Plan& p = plans[i];
         bool any = false;
@@ -733,27 +862,68 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
             }
         if (!any) variants.push_back({&p, -1, i});
     }
+    for (auto& v : variants)
+        for (size_t s = 0; s < v.plan->sources.size(); ++s)
+            if (static_cast<long>(s) != v.delta_source) full_read.insert(v.plan->sources[s].relation);
+    // Dedup strategy per relation: a key set for binary/unary relations (keys
+    // are one u64 word that can never equal the empty slot), the sort +
+    // merge-path pipeline otherwise. FVLOG_DEDUP=sort forces the latter.
+    const char* mode = std::getenv("FVLOG_DEDUP");
+    const bool hash_ok = !(mode && std::string(mode) == "sort");
+    for (auto& [name, r] : st->relations) {
+        r->hash_mode = hash_ok && r->idb && r->arity <= 2 && (r->arity == 1 || 2 * st->key_shift < 64);
+        r->levels_mode = r->hash_mode && !full_read.count(name);
+    }
+
+    const bool trace = std::getenv("FVLOG_TRACE") != nullptr;
+    auto tr = [&](const char* what, Clock::time_point t, u64 it) {
+        if (trace) {
+            c->sync();
+            std::fprintf(stderr, "[fvlog] it=%llu %-10s %.3f ms\n", static_cast<unsigned long long>(it), what,
+                         ms_since(t));
+        }
+    };
+    if (trace) tr("setup", t0, 0);
+    // ---- seed: FULL = DELTA = dedup(EDB) (engine.cpp:148-161) ---------------
+    const auto ts = Clock::now();
+    for (auto& [name, vp] : raw) {
+        RelState& r = *st->relations[name];
+        if (eng.partitioned(r)) {
+            for (u32 kc : r.keyset) eng.seed_copy(r, *vp, kc);
+        } else {
+            eng.seed_copy(r, *vp, 0);  // FULL empty: C = D = distinct rows
+        }
+    }
+    raw.clear();
+    concat.clear();
+    tr("seed", ts, 0);
 
     // ---- fixpoint (engine.cpp:163-239) ---------------------------------------
     u64 iteration = 0;
     for (;;) {
         const auto ti = Clock::now();
         std::map<std::string, CandPool> pooled;
+        std::map<std::string, HeadSink> sinks;
         for (auto& v : variants) pooled[v.plan->head].arity = v.plan->head_arity;
         for (auto& v : variants) {
             if (v.delta_source < 0 && iteration != 0) continue;
-            eng.exec_variant(*v.plan, dplans[v.plan_index], v.delta_source, pooled[v.plan->head]);
+            RelState& hr = *st->relations.at(v.plan->head);
+            HeadSink* sink = (hr.hash_mode && !eng.dist()) ? &sinks[v.plan->head] : nullptr;
+            eng.exec_variant(*v.plan, dplans[v.plan_index], v.delta_source, pooled[v.plan->head], sink);
         }
+        tr("variants", ti, iteration);
+        const auto tf = Clock::now();
         std::vector<u64> counts;  // per head: |Δ|, |FULL| (local, then global)
         for (auto& [name, pool] : pooled) {
             RelState& r = *st->relations.at(name);
             if (eng.dist()) eng.route_pool(pool);
-            const u64 nd = eng.dedup_merge_home(r, pool);
+            const u64 nd = r.hash_mode ? eng.hash_finalize(r, sinks[name], pool) : eng.dedup_merge_home(r, pool);
             if (eng.dist()) eng.forward_delta(r);
             counts.push_back(nd);
-            counts.push_back(r.full.n);
+            counts.push_back(r.rows());
         }
         eng.allreduce(counts);
+        tr("finalize", tf, iteration);
         bool any_delta = false;
         std::vector<IterStat> its;
         size_t k = 0;
@@ -774,6 +944,13 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     st->iterations = iteration + 1;
     c->sync();
     st->elapsed_ms = ms_since(t0);
+    if (trace) {
+        u64 reserved = 0, used = 0;
+        cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        std::fprintf(stderr, "[fvlog] pool reserved %.2f GB used %.2f GB trims %llu\n", reserved / 1e9, used / 1e9,
+                     static_cast<unsigned long long>(c->pool_trims));
+    }
     return st;
 }
 
@@ -824,10 +1001,41 @@ std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel) {
     auto it = s.relations.find(rel);
     if (it == s.relations.end()) fail(FV_ERR_RANGE, "unknown relation '" + rel + "'");
     const RelState& r = *it->second;
-    std::vector<u32> rows(r.full.n * r.arity), col(r.full.n);
+    Ctx* c = s.ctx;
+    const u64 n = r.rows();
+    DevVersion merged;
+    const DevVersion* src = &r.full;
+    if (r.levels_mode) {
+        // Levels are sorted per iteration; one sort of their concatenation
+        // gives the lexicographic dump (like dump_relation's std::sort).
+        merged.n = n;
+        for (u32 j = 0; j < r.arity; ++j) {
+            DBuf<u32> col(c, n);
+            u64 off = 0;
+            for (auto& lv : r.levels) {
+                if (lv.n)
+                    FV_CUDA(cudaMemcpyAsync(col.get() + off, lv.cols[j].get(), 4 * lv.n, cudaMemcpyDeviceToDevice,
+                                            c->stream));
+                off += lv.n;
+            }
+            merged.cols.push_back(std::move(col));
+        }
+        if (n) {
+            std::vector<DBuf<u64>> words;
+            words.emplace_back(c, n);
+            u64* wp = words[0].get();
+            engine_pack_keys(c, merged.ptrs(), n, s.key_shift, &wp);
+            engine_sort_keys(c, words, n, r.arity, s.key_shift);
+            std::vector<u32*> cols;
+            for (auto& col : merged.cols) cols.push_back(col.get());
+            engine_unpack_keys(c, words[0].get(), n, r.arity, s.key_shift, cols);
+        }
+        src = &merged;
+    }
+    std::vector<u32> rows(n * r.arity), col(n);
     for (u32 j = 0; j < r.arity; ++j) {
-        r.full.cols[j].download(col.data(), r.full.n);
-        for (u64 i = 0; i < r.full.n; ++i) rows[i * r.arity + j] = col[i];
+        src->cols[j].download(col.data(), n);
+        for (u64 i = 0; i < n; ++i) rows[i * r.arity + j] = col[i];
     }
     return rows;
 }
@@ -836,7 +1044,10 @@ u64 fingerprint(const EvalState& s, const std::string& rel) {
     auto it = s.relations.find(rel);
     if (it == s.relations.end()) fail(FV_ERR_RANGE, "unknown relation '" + rel + "'");
     const RelState& r = *it->second;
-    return engine_fingerprint(s.ctx, r.full.ptrs(), r.full.n, r.arity);
+    if (!r.levels_mode) return engine_fingerprint(s.ctx, r.full.ptrs(), r.full.n, r.arity);
+    u64 h = 0;  // the fingerprint is a sum over rows: additive over levels
+    for (auto& lv : r.levels) h += engine_fingerprint(s.ctx, lv.ptrs(), lv.n, r.arity);
+    return h;
 }
 
 }  // namespace fv

@@ -97,6 +97,15 @@ struct JoinIndex {
 
 using IndexMap = std::map<std::pair<int, u32>, std::unique_ptr<JoinIndex>>;
 
+// Open-addressing set of packed row keys (empty slot = all ones, which no
+// key can equal when 2 * shift < 64), load factor <= 1/2.
+struct KeySet {
+    DBuf<u64> slots;
+    u64 mask = 0;
+    u64 count = 0;
+    u64 capacity() const { return slots.size(); }
+};
+
 // A partition copy of a relation keyed on a column other than 0 (partitioned
 // evaluation only): the rows whose owner(hash(row[col])) is this rank.
 struct RelCopy {
@@ -115,6 +124,17 @@ struct RelState {
     // Partitioned evaluation: extra copies keyed on other probed columns.
     std::map<u32, std::unique_ptr<RelCopy>> copies;
     std::set<u32> keyset;  // partition columns this relation is needed on
+    // Hash dedup (arity <= 2): the key set of the home FULL. Candidates are
+    // inserted straight from the join kernel; only new rows get sorted.
+    bool hash_mode = false;
+    KeySet keys;
+    // With hash dedup, a FULL no join reads is kept as sorted levels (one
+    // per iteration, merged only for dumps); otherwise it is `full`, merged
+    // with each sorted Δ.
+    bool levels_mode = false;
+    std::vector<DevVersion> levels;
+    u64 level_rows = 0;
+    u64 rows() const { return levels_mode ? level_rows : full.n; }
 };
 
 struct IterStat {
@@ -213,7 +233,20 @@ struct OutSpec {
     u64* keys[4] = {nullptr, nullptr, nullptr, nullptr};
     u32* out_cols[kMaxSlots] = {nullptr};
     u64* d_count = nullptr;  // compaction counter (n_filters > 0)
+    // Hash-insert mode (key mode, one word): instead of writing every
+    // candidate, insert it into the relation's key set and append only the
+    // keys that were not present to new_keys[*new_count ...].
+    u64* ht_slots = nullptr;
+    u64 ht_mask = 0;
+    u64* new_keys = nullptr;
+    u64* new_count = nullptr;
 };
+
+// Insert n keys; the ones not yet present are appended to
+// new_keys[*d_new ...] (device counter, not reset here).
+void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_keys, u64* d_new);
+// Keys -> SoA columns (one word per row, arity <= 2).
+void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, const std::vector<u32*>& cols);
 
 struct RowFilter {  // predicate on probe-side rows (source constraints)
     u32 n = 0;

@@ -75,6 +75,53 @@ __global__ void probe_count_kernel(const u32* __restrict__ probe, u64 n, const u
     }
 }
 
+__device__ __forceinline__ u64 row_key1(const OutSpec& spec, u64 i, u64 p) {
+    const u64 hi = slot(spec.col[0], i, p);
+    return spec.n_out >= 2 ? (hi << spec.shift) | slot(spec.col[1], i, p) : hi;
+}
+
+// Set-insert of one key: true when the key was absent (this thread inserted
+// it). Duplicates are detected with a plain load first; only empty slots
+// are claimed with a CAS.
+__device__ __forceinline__ bool keyset_insert_probe_from(u64* __restrict__ slots, u64 mask, u64 key, u64 h) {
+    while (true) {
+        const u64 s = __ldcg(slots + h);
+        if (s == key) return false;
+        if (s == kEmptySlot) {
+            const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(slots + h), ~0ull,
+                                       static_cast<unsigned long long>(key));
+            if (prev == ~0ull) return true;
+            if (prev == key) return false;
+        }
+        h = (h + 1) & mask;
+    }
+}
+
+// Insert resolution after a speculative first-slot load `s` (issued early so
+// a thread has many independent table loads in flight).
+__device__ __forceinline__ bool keyset_insert_from(u64* __restrict__ slots, u64 mask, u64 key, u64 h, u64 s) {
+    if (s == key) return false;
+    if (s == kEmptySlot) {
+        const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(slots + h), ~0ull,
+                                   static_cast<unsigned long long>(key));
+        if (prev == ~0ull) return true;
+        if (prev == key) return false;
+    }
+    return keyset_insert_probe_from(slots, mask, key, (h + 1) & mask);
+}
+
+// Warp-aggregated append of the keys flagged new (all lanes must call).
+__device__ __forceinline__ void append_new(u64* __restrict__ out, u64* counter, bool is_new, u64 key) {
+    const u32 m = __ballot_sync(0xffffffffu, is_new);
+    if (!m) return;
+    const u32 lane = lane_id();
+    const u32 leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(reinterpret_cast<unsigned long long*>(counter), static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (is_new) out[base + __popc(m & lanemask_lt())] = key;
+}
+
 // Write one output row (values computed from slots) at position pos.
 __device__ __forceinline__ void write_row(const OutSpec& spec, u64 pos, u64 i, u64 p) {
     if (spec.key_mode) {
@@ -212,6 +259,25 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
             pp[k] = static_cast<u32>(p);
             if (!COMPACT || pass_filters(spec.f, spec.n_filters, i, p)) keep_mask |= 1u << k;
         }
+    }
+    if (spec.ht_slots) {
+        // Fused dedup: probe/insert FULL's key set, keep only new rows. All
+        // first-slot loads are issued before any is resolved (8 in flight).
+        u64 key[kMatItems], hs[kMatItems], sv[kMatItems];
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k) {
+            key[k] = ((keep_mask >> k) & 1u) ? row_key1(spec, ii[k], pp[k]) : 0;
+            hs[k] = mix64(key[k]) & spec.ht_mask;
+        }
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k) sv[k] = ((keep_mask >> k) & 1u) ? __ldcg(spec.ht_slots + hs[k]) : 0;
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k) {
+            const bool keep = (keep_mask >> k) & 1u;
+            const bool is_new = keep && keyset_insert_from(spec.ht_slots, spec.ht_mask, key[k], hs[k], sv[k]);
+            append_new(spec.new_keys, spec.new_count, is_new, key[k]);
+        }
+        return;
     }
     if (!COMPACT) {
 #pragma unroll
@@ -569,6 +635,40 @@ __global__ void fingerprint_kernel(Cols8 c, u32 arity, u64 n, unsigned long long
 
 namespace {
 
+__global__ void hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n, u64* __restrict__ slots, u64 mask,
+                                        u64* __restrict__ new_keys, u64* new_count) {
+    constexpr int ITEMS = 8;  // independent table loads in flight per thread
+    const u64 base = u64(blockIdx.x) * blockDim.x * ITEMS + threadIdx.x;
+    u64 key[ITEMS], hs[ITEMS], sv[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 i = base + u64(k) * blockDim.x;
+        key[k] = i < n ? keys[i] : 0;
+        hs[k] = mix64(key[k]) & mask;
+    }
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) sv[k] = (base + u64(k) * blockDim.x < n) ? __ldcg(slots + hs[k]) : 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const bool valid = base + u64(k) * blockDim.x < n;
+        const bool is_new = valid && keyset_insert_from(slots, mask, key[k], hs[k], sv[k]);
+        if (new_keys) append_new(new_keys, new_count, is_new, key[k]);
+    }
+}
+
+__global__ void unpack_keys_kernel(const u64* __restrict__ keys, u64 n, u32 arity, u32 shift, u32* c0, u32* c1) {
+    const u64 lo_mask = (u64(1) << shift) - 1;
+    GRID_STRIDE(i, n) {
+        const u64 k = keys[i];
+        if (arity == 2) {
+            c0[i] = static_cast<u32>(k >> shift);
+            c1[i] = static_cast<u32>(k & lo_mask);
+        } else {
+            c0[i] = static_cast<u32>(k);
+        }
+    }
+}
+
 constexpr int kMaxRanks = 64;
 
 __device__ __forceinline__ u32 route_dest(const RouteKey& k, u64 i, u32 world) {
@@ -628,6 +728,25 @@ struct SelectRowsOp {
 }  // namespace
 
 // ---- host launchers -------------------------------------------------------------------------
+
+void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_keys, u64* d_new) {
+    if (!n) return;
+    ProfScope prof(c, "hash_insert", double(n) * (8.0 + 16.0));
+    hash_insert_keys_kernel<<<static_cast<unsigned>(ceil_div(n, 256 * 8)), 256, 0, c->stream>>>(
+        keys, n, set.slots.get(), set.mask, new_keys, d_new);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, const std::vector<u32*>& cols) {
+    if (!n) return;
+    if (arity > 2) fail(FV_ERR_ARITY, "unpack_keys: arity > 2");
+    ProfScope prof(c, "unpack_keys", double(n) * (8.0 + 4.0 * arity));
+    unpack_keys_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, n, arity, shift, cols[0],
+                                                            arity == 2 ? cols[1] : nullptr);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
 
 u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids) {
     if (!n) return 0;

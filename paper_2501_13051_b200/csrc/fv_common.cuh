@@ -97,6 +97,7 @@ struct Ctx {
     u64* pinned = nullptr; // small pinned host buffer for scalar readbacks
     u64* d_scalars = nullptr; // device scalar slots
     u32 counter_next = 0;
+    u64 pool_trims = 0;       // allocation retries after trimming the pool
 
     void* alloc(size_t bytes);
     void release(void* p);

@@ -31,6 +31,7 @@ void* Ctx::alloc(size_t bytes) {
         // Give cached blocks back and retry once before reporting OOM.
         FV_CUDA(cudaStreamSynchronize(stream));
         FV_CUDA(cudaMemPoolTrimTo(pool, 0));
+        ++pool_trims;
         e = cudaMallocFromPoolAsync(&p, bytes, pool, stream);
         if (e != cudaSuccess) {
             (void)cudaGetLastError();

@@ -167,7 +167,7 @@ int run(Ctx* c, const RunConfig& cfg, std::ostream& out, std::ostream& err) {
             for (auto& s : st->stats)
                 out << "iter=" << s.iteration << " rel=" << s.relation << " delta=" << s.delta_rows
                     << " ms=" << s.elapsed_ms << "\n";
-        for (auto& [name, rel] : st->relations) out << "rel=" << name << " rows=" << rel->full.n << "\n";
+        for (auto& [name, rel] : st->relations) out << "rel=" << name << " rows=" << rel->rows() << "\n";
         out << "iterations=" << st->iterations << " total_ms=" << st->elapsed_ms << " workers=1\n";
 
         if (!cfg.dump_relations.empty()) {
