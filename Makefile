@@ -18,7 +18,7 @@ CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 HDRS := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/fvlog.h
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP_SRCS))
 
-all: $(PKG)/libfvlog.so $(PKG)/fvlog
+all: $(PKG)/libfvlog.so $(PKG)/fvlog tools/fvlog_membench
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -35,7 +35,10 @@ $(PKG)/fvlog: tools/fvlog_main.cpp $(PKG)/libfvlog.so
 	$(HOSTCXX) -std=c++17 -O2 -Iinclude -o $@ tools/fvlog_main.cpp -L$(PKG) -lfvlog \
 	    -Wl,-rpath,'$$ORIGIN'
 
+tools/fvlog_membench: tools/membench.cu
+	$(NVCC) -O3 $(ARCH) -lineinfo -ccbin $(HOSTCXX) -o $@ $<
+
 clean:
-	rm -rf build $(PKG)/libfvlog.so $(PKG)/fvlog
+	rm -rf build $(PKG)/libfvlog.so $(PKG)/fvlog tools/fvlog_membench
 
 .PHONY: all clean

@@ -205,6 +205,10 @@ def run_fvlog(args):
     _lib.bind("fv_edb_upload", C.c_int, [C.c_void_p, C.POINTER(E.fv_relation_decl), C.c_uint32,
                                          C.POINTER(E.fv_facts), C.c_uint32, C.POINTER(C.c_void_p)])
     _lib.bind("fv_edb_free", None, [C.c_void_p])
+    _lib.bind("fv_ctx_reserve", C.c_int, [C.c_void_p, C.c_uint64])
+    # Map the memory pool once up front (outside every timed region) so the
+    # fixpoints sub-allocate instead of growing the pool mid-iteration.
+    _lib.check(l.fv_ctx_reserve(ctx.h, int(args.reserve_gb * 2**30)), ctx.h)
     _lib.bind("fv_evaluate_program_edb", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)])
 
     if world > 1:
@@ -276,7 +280,10 @@ def run_fvlog(args):
         for _ in range(args.steps):
             st = step_resident()
             tuples += st.derived_tuples()
-            last = st
+            rows, iterations = st.rows("reach"), st.iterations
+            # Drop the step's result before the next step (as a caller
+            # would): two live fixpoints would double the pool footprint.
+            del st
         ev1.record()
         barrier()
     dev_ms = ev0.elapsed_time(ev1)
@@ -288,9 +295,6 @@ def run_fvlog(args):
         _lib.check(l.fv_ctx_profile_entry(ctx.h, i, C.byref(nm), C.byref(la), C.byref(ms), C.byref(by)), ctx.h)
         kernels.append({"name": nm.value.decode(), "launches": la.value, "ms": ms.value, "bytes": by.value})
     kernels.sort(key=lambda k: -k["ms"])
-    rows = last.rows("reach")
-    iterations = last.iterations
-    del last
 
     t_max = max_over_ranks(dev_ms)
     # Stats (hence derived tuples) are global in a partitioned evaluation.
@@ -299,11 +303,15 @@ def run_fvlog(args):
 
     # ---- timed: e2e through the C ABI with host buffers ----
     barrier()
+    if args.no_e2e:
+        args_steps_e2e = 0
+    else:
+        args_steps_e2e = args.steps
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_tuples = 0
     d2h = 0
     e0.record()
-    for _ in range(args.steps):
+    for _ in range(args_steps_e2e):
         st, stats = step_e2e()
         e2e_tuples += st.derived_tuples()
         d2h = 40 * len(stats) + 24 * len(st.relations())
@@ -311,7 +319,7 @@ def run_fvlog(args):
     e1.record()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-    e2e_value = float(e2e_tuples) / (e2e_ms / 1000.0)
+    e2e_value = float(e2e_tuples) / (e2e_ms / 1000.0) if args_steps_e2e else None
 
     if rank != 0:
         if dist is not None:
@@ -347,7 +355,7 @@ def run_fvlog(args):
                                    f"one NCCL all-to-all + all-reduce per iteration") if world > 1 else "1 GPU",
                    "components": COMPONENTS * world,
                    "l2": "inputs larger than L2 (FULL grows to >5 GB per step, L2 126 MB)"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / args.steps,
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / max(1, args_steps_e2e),
                 "h2d_bytes_per_step": int(host_edges.nbytes), "d2h_bytes_per_step": d2h,
                 "path": "fv_evaluate_program (host pinned facts) + fv_state_stat readback"},
         "gpu_launches": int(launches),
@@ -377,6 +385,8 @@ def main():
     ap.add_argument("--ref-components", type=int, default=20)
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
+    ap.add_argument("--reserve-gb", type=float, default=64.0, help="fv_ctx_reserve before warm-up")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_impl(args)

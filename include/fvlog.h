@@ -69,6 +69,12 @@ fv_status fv_ctx_create(int device, fv_ctx** out);
 void fv_ctx_destroy(fv_ctx* ctx);
 const char* fv_last_error(const fv_ctx* ctx);
 fv_status fv_ctx_synchronize(fv_ctx* ctx);
+/* Grow the context's stream-ordered memory pool to at least `bytes` of
+ * mapped device memory now (one allocation, freed back into the pool), so
+ * later evaluations sub-allocate from it instead of mapping new memory in
+ * the middle of a fixpoint. Optional; no reference counterpart (the
+ * reference allocates host vectors per operator). */
+fv_status fv_ctx_reserve(fv_ctx* ctx, uint64_t bytes);
 /* Number of kernels this context has launched so far (profiling evidence). */
 uint64_t fv_ctx_kernel_launches(const fv_ctx* ctx);
 /* Per-kernel-class timing with CUDA events recorded on the context stream

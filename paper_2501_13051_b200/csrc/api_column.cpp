@@ -132,6 +132,13 @@ fv_status fv_ctx_profile(fv_ctx* ctx, int enable) {
     FV_API_END
 }
 
+fv_status fv_ctx_reserve(fv_ctx* ctx, uint64_t bytes) {
+    FV_API_BEGIN(ctx)
+    FV_REQUIRE(ctx, FV_ERR_INVALID, "fv_ctx_reserve: null ctx");
+    ctx->c->reserve(bytes);
+    FV_API_END
+}
+
 uint32_t fv_ctx_profile_count(const fv_ctx* ctx) {
     if (!ctx) return 0;
     ctx->c->sync();

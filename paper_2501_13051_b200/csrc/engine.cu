@@ -615,7 +615,9 @@ public:
         std::vector<DBuf<u64>> words;
         words.push_back(std::move(s.keys));
         s.cap = 0;
-        engine_sort_keys(c_, words, nd, r.arity, st_.key_shift);
+        // Levels-mode FULL is never merged, so Δ only has to be grouped by
+        // column 0 (its join index); a sorted FULL needs the full order.
+        engine_sort_keys(c_, words, nd, r.arity, st_.key_shift, r.levels_mode);
         std::vector<u32*> dc;
         for (auto& col : Dv.cols) dc.push_back(col.get());
         engine_unpack_keys(c_, words[0].get(), nd, r.arity, st_.key_shift, dc);
@@ -1006,7 +1008,7 @@ std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel) {
     DevVersion merged;
     const DevVersion* src = &r.full;
     if (r.levels_mode) {
-        // Levels are sorted per iteration; one sort of their concatenation
+        // Levels are grouped by column 0 per iteration; one sort of their concatenation
         // gives the lexicographic dump (like dump_relation's std::sort).
         merged.n = n;
         for (u32 j = 0; j < r.arity; ++j) {

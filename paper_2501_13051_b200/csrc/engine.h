@@ -291,6 +291,9 @@ void engine_route(Ctx* c, u64 n, const RouteKey& key, u32 world, const std::vect
                   const std::vector<u32*>& c32_out, const std::vector<const u64*>& c64,
                   const std::vector<u64*>& c64_out, u64* cnt, u64* off);
 // Sort W-word keys in place (LSD over words with a permutation payload).
-void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift);
+// Sort packed row keys lexicographically. group_only (one-word keys only):
+// order by the first column alone (rows grouped for a column-0 join index;
+// within a group the order is unspecified) — skips the low-column passes.
+void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift, bool group_only = false);
 
 }  // namespace fv

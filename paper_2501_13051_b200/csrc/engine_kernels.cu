@@ -149,6 +149,8 @@ __device__ __forceinline__ void write_row(const OutSpec& spec, u64 pos, u64 i, u
 constexpr int kMatBlock = 256;
 constexpr int kMatItems = 8;
 constexpr int kMatTile = kMatBlock * kMatItems;
+constexpr int kMatSparseSpan = 8 * kMatTile;
+constexpr int kMatSetSlots = 2 * kMatTile;  // load <= 1/2
 
 __device__ __forceinline__ u64 upper_bound_u64(const u64* __restrict__ a, u64 len, u64 x) {
     u64 lo = 0, hi = len;
@@ -206,18 +208,25 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
                                                                  const u64* __restrict__ tile_jhi,
                                                                  OutSpec spec) {
     __shared__ u32 s_owner[kMatTile];
+    __shared__ unsigned long long s_set[kMatSetSlots];  // tile-local key set (fused dedup only)
     __shared__ u64 s_base;
     __shared__ u32 s_warp[kMatBlock / 32 + 1];
     const u32 tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    if (spec.ht_slots)
+        for (u32 i = tid; i < kMatSetSlots; i += kMatBlock) s_set[i] = ~0ull;
     const u64 o0 = u64(blockIdx.x) * kMatTile;
     const u64 o_end = min(o0 + kMatTile, total);
-    for (u32 i = tid; i < kMatTile; i += kMatBlock) s_owner[i] = 0;
-    __syncthreads();
     const u64 jlo = tile_jlo[blockIdx.x], jhi = tile_jhi[blockIdx.x];
-    for (u64 j = jlo + 1 + tid; j <= jhi; j += kMatBlock)
-        atomicMax(&s_owner[offsets[j] - o0], static_cast<u32>(j - jlo));
-    __syncthreads();
-    {
+    // A tile whose source rows span far more than its outputs is mostly
+    // zero-count rows (probe misses): marking would walk every one of them,
+    // so each output binary-searches its row instead (block-uniform branch).
+    const bool sparse = jhi - jlo > u64(kMatSparseSpan);
+    if (!sparse) {
+        for (u32 i = tid; i < kMatTile; i += kMatBlock) s_owner[i] = 0;
+        __syncthreads();
+        for (u64 j = jlo + 1 + tid; j <= jhi; j += kMatBlock)
+            atomicMax(&s_owner[offsets[j] - o0], static_cast<u32>(j - jlo));
+        __syncthreads();
         u32 v[kMatItems];
         u32 run = 0;
 #pragma unroll
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
         ii[k] = 0;
         pp[k] = 0;
         if (o < o_end) {
-            const u64 i = jlo + s_owner[local];
+            const u64 i = sparse ? jlo + upper_bound_u64(offsets + jlo, jhi - jlo + 1, o) - 1 : jlo + s_owner[local];
             const u64 p = starts[i] + (o - offsets[i]);
             ii[k] = i;
             pp[k] = static_cast<u32>(p);
@@ -261,13 +270,33 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
         }
     }
     if (spec.ht_slots) {
-        // Fused dedup: probe/insert FULL's key set, keep only new rows. All
-        // first-slot loads are issued before any is resolved (8 in flight).
+        // Fused dedup. First a tile-local key set in shared memory drops the
+        // repeats inside the tile: consecutive outputs share the probe row's
+        // head columns, so one derivation per tile and key reaches HBM (about
+        // half of all TC candidates are same-iteration repeats). Survivors
+        // probe/insert FULL's key set; all first-slot loads are issued before
+        // any is resolved (8 in flight per thread).
         u64 key[kMatItems], hs[kMatItems], sv[kMatItems];
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) {
             key[k] = ((keep_mask >> k) & 1u) ? row_key1(spec, ii[k], pp[k]) : 0;
-            hs[k] = mix64(key[k]) & spec.ht_mask;
+            hs[k] = mix64(key[k]);
+        }
+        __syncthreads();  // s_set initialised (the sparse path has no barrier before this)
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k) {
+            if (!((keep_mask >> k) & 1u)) continue;
+            u32 h = static_cast<u32>(hs[k] >> 40) & (kMatSetSlots - 1);
+            while (true) {
+                const unsigned long long prev = atomicCAS(s_set + h, ~0ull, static_cast<unsigned long long>(key[k]));
+                if (prev == ~0ull) break;                 // first in the tile
+                if (prev == key[k]) {                     // repeat: drop
+                    keep_mask &= ~(1u << k);
+                    break;
+                }
+                h = (h + 1) & (kMatSetSlots - 1);
+            }
+            hs[k] &= spec.ht_mask;
         }
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) sv[k] = ((keep_mask >> k) & 1u) ? __ldcg(spec.ht_slots + hs[k]) : 0;
@@ -785,7 +814,12 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
         (spec.f[k].a.side ? side1 : side0) += 4;
         if (spec.f[k].op != kFilterConst) (spec.f[k].b.side ? side1 : side0) += 4;
     }
-    const double out_bytes = spec.key_mode ? 8.0 * ((spec.n_out + 1) / 2) : 4.0 * spec.n_out;
+    // With the fused dedup (spec.ht_slots) the candidate row is never
+    // materialized; it is still charged as written once and read once by
+    // dedup (2 * 4h bytes per candidate) so the figure is the
+    // same implementation-independent lower bound as the unfused pipeline.
+    const double row_bytes = spec.key_mode ? 8.0 * ((spec.n_out + 1) / 2) : 4.0 * spec.n_out;
+    const double out_bytes = spec.ht_slots ? 2.0 * row_bytes : row_bytes;
     DBuf<u64> rows(c, 2 * tiles);
     tile_rows_kernel<<<grid_for(tiles), 256, 0, c->stream>>>(offsets, m, total, tiles, rows.get(),
                                                              rows.get() + tiles);
@@ -963,7 +997,7 @@ u64 engine_fingerprint(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 a
     return h;
 }
 
-void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift) {
+void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift, bool group_only) {
     if (n <= 1) return;
     const u32 W = static_cast<u32>(words.size());
     auto word_bits = [&](u32 w) -> u32 {
@@ -971,8 +1005,9 @@ void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u
     };
     if (W == 1) {
         const u32 bits = arity >= 2 ? 2 * shift : shift;
+        const u32 begin = (group_only && arity == 2) ? shift : 0;
         DBuf<u64> alt(c, n);
-        if (radix_sort_keys_u64(c, words[0].get(), alt.get(), n, 0, bits > 64 ? 64 : bits)) words[0].swap(alt);
+        if (radix_sort_keys_u64(c, words[0].get(), alt.get(), n, begin, bits > 64 ? 64 : bits)) words[0].swap(alt);
         return;
     }
     DBuf<u32> perm(c, n), perm_alt(c, n);

@@ -100,6 +100,7 @@ struct Ctx {
     u64 pool_trims = 0;       // allocation retries after trimming the pool
 
     void* alloc(size_t bytes);
+    void reserve(size_t bytes);  // pre-map pool memory (fv_ctx_reserve)
     void release(void* p);
     void activate() const;  // cudaSetDevice
     void sync();

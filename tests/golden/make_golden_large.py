@@ -9,8 +9,14 @@
       shortest-path distance k+1) -> |reach|, deltas, fingerprint
       (fingerprints add over disjoint components).
   C3  SG forest of 244 depth-10 trees: closed form.
+  C4  CSPA on K disjoint functions (cspa_facts(K, 100, 100, 70)): the
+      UNMODIFIED reference run on batches of components (components are
+      disjoint, so the fixpoint is the union of the per-batch fixpoints:
+      rows, fingerprints and per-iteration deltas add, iterations = max).
+  C5  OWL-RL/LUBM rule set on lubm_facts(340) (~10.2 M facts): the
+      UNMODIFIED reference on the whole input.
 
-    python tests/golden/make_golden_large.py [c1] [c2]
+    python tests/golden/make_golden_large.py [c1] [c2] [c4] [c5]
 Writes tests/golden/large.json (merging with what is already there).
 """
 from __future__ import annotations
@@ -101,6 +107,95 @@ def c2(components=1000, nodes=1000, edges=5000):
             "rows": int(total_rows), "fingerprint": str(fp), "deltas": deltas, "iterations": len(deltas)}
 
 
+def run_reference(program: str, facts: dict, workers: int, dump=True):
+    """Unmodified reference on `facts`: (per-relation rows/fingerprint/deltas,
+    iterations, total_ms)."""
+    with tempfile.TemporaryDirectory() as d:
+        W.write_tsv_dir(os.path.join(d, "facts"), facts)
+        prog = os.path.join(d, "p.dl")
+        open(prog, "w").write(program)
+        import re
+        rels = sorted(set(re.findall(r"([a-z][A-Za-z0-9_]*)\s*\(", program)))
+        r = subprocess.run([REF_BIN, "run", prog, "--facts", os.path.join(d, "facts"), "--out",
+                            os.path.join(d, "out"), "--workers", str(workers), "--stats"]
+                           + (["--dump", ",".join(rels)] if dump else []),
+                           capture_output=True, text=True, check=True,
+                           env=dict(os.environ, OMP_WAIT_POLICY="passive"))
+        out = {}
+        for l in r.stdout.splitlines():
+            f = dict(kv.split("=", 1) for kv in l.split())
+            if l.startswith("iter="):
+                out.setdefault(f["rel"], {"deltas": []})["deltas"].append(int(f["delta"]))
+            elif l.startswith("rel="):
+                out.setdefault(f["rel"], {"deltas": []})["rows"] = int(f["rows"])
+            elif l.startswith("iterations="):
+                iterations, total_ms = int(f["iterations"]), float(f["total_ms"])
+        if dump:
+            import pandas as pd
+            for rel in rels:
+                path = os.path.join(d, "out", rel + ".tsv")
+                if os.path.getsize(path) == 0:
+                    out[rel]["fingerprint"] = "0"
+                    continue
+                rows = pd.read_csv(path, sep="\t", header=None, dtype=np.uint32).to_numpy()
+                out[rel]["fingerprint"] = str(fingerprint_rows(rows))
+    return out, iterations, total_ms
+
+
+C4_SHAPE = dict(components=4000, vars_per=100, assign_per=100, deref_per=70)
+
+
+def _c4_batch(args):
+    lo, hi = args
+    K = C4_SHAPE["components"]
+    f = W.cspa_facts(K, C4_SHAPE["vars_per"], C4_SHAPE["assign_per"], C4_SHAPE["deref_per"])
+    a, dr = C4_SHAPE["assign_per"], C4_SHAPE["deref_per"]
+    sub = {"assign": f["assign"][lo * a:hi * a], "dereference": f["dereference"][lo * dr:hi * dr]}
+    return run_reference(W.CSPA_PROGRAM, sub, 1)
+
+
+def c4(batch=10, procs=None):
+    from multiprocessing import Pool
+    K = C4_SHAPE["components"]
+    jobs = [(lo, min(K, lo + batch)) for lo in range(0, K, batch)]
+    total = {}
+    iterations = 0
+    ms = 0.0
+    t0 = time.time()
+    with Pool(procs or os.cpu_count()) as pool:
+        for i, (rels, it, tms) in enumerate(pool.imap_unordered(_c4_batch, jobs)):
+            iterations = max(iterations, it)
+            ms += tms
+            for rel, g in rels.items():
+                t = total.setdefault(rel, {"rows": 0, "fingerprint": 0, "deltas": []})
+                t["rows"] += g["rows"]
+                t["fingerprint"] = (t["fingerprint"] + int(g["fingerprint"])) & 0xFFFFFFFFFFFFFFFF
+                for k, dv in enumerate(g["deltas"]):
+                    if k >= len(t["deltas"]):
+                        t["deltas"].append(0)
+                    t["deltas"][k] += dv
+            if i % 50 == 0:
+                print(f"C4 batch {i}/{len(jobs)} {time.time() - t0:.0f}s", flush=True)
+    for t in total.values():
+        t["fingerprint"] = str(t["fingerprint"])
+        t["deltas"] += [0] * (iterations - len(t["deltas"]))
+    return {"config": "C4 cspa_facts({components}, {vars_per}, {assign_per}, {deref_per}, seed=3)".format(**C4_SHAPE),
+            "source": f"unmodified reference (oracle/_ref) on {len(jobs)} batches of {batch} disjoint components",
+            "relations": total, "iterations": iterations, "reference_cpu_s_sum": round(ms / 1000.0, 1)}
+
+
+C5_SCALE = 340
+
+
+def c5():
+    f = W.lubm_facts(C5_SCALE)
+    t0 = time.time()
+    rels, it, tms = run_reference(W.LUBM_PROGRAM, f, os.cpu_count() or 1)
+    return {"config": f"C5 lubm_facts({C5_SCALE})", "facts": int(sum(v.shape[0] for v in f.values())),
+            "source": "unmodified reference (oracle/_ref)", "relations": rels, "iterations": it,
+            "reference_total_ms": round(tms, 1), "reference_wall_s": round(time.time() - t0, 1)}
+
+
 def main():
     which = sys.argv[1:] or ["c1", "c2"]
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
@@ -110,6 +205,12 @@ def main():
     if "c1" in which:
         data["C1"] = c1()
         print("C1", data["C1"]["rows"], data["C1"]["iterations"], flush=True)
+    if "c4" in which:
+        data["C4"] = c4()
+        print("C4", {k: v["rows"] for k, v in data["C4"]["relations"].items()}, flush=True)
+    if "c5" in which:
+        data["C5"] = c5()
+        print("C5", data["C5"]["iterations"], flush=True)
     data["C3"] = {"config": "C3 sg_forest(244, 10)", "source": "closed form", "rows": W.sg_count(244, 10),
                   "iterations": 11}
     json.dump(data, open(OUT, "w"), indent=1)
