@@ -37,6 +37,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <exception>
+#include <functional>
+#include <deque>
 #include <set>
 #include <thread>
 
@@ -50,6 +52,9 @@ namespace fv {
 namespace {
 
 using Clock = std::chrono::steady_clock;
+
+// Join outputs per fused join+dedup launch (see exec_variant).
+constexpr u64 kFusedChunk = u64(1) << 27;
 
 double ms_since(Clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
@@ -99,6 +104,80 @@ u32 copy_for_source(const Plan& p, u32 s) {
 }
 
 }  // namespace
+
+// Delta-first join order for one semi-naive variant (engine decision, not
+// part of the reference's plan semantics: the variant's result set does not
+// depend on the join order). compile_rule orders a rule's atoms left to right
+// (P/src/compiler.cpp:19-96), so a variant whose DELTA atom is not first
+// joins FULL x FULL before touching DELTA — e.g. CSPA's valueAlias(x,y) :-
+// valueFlow(z,x), memoryAlias(z,w), valueFlow(w,y) with DELTA at the third
+// atom materializes every (x,w) pair of the two FULL relations each
+// iteration. Here the DELTA source goes first and the others follow in their
+// original order as soon as they share a variable with the joined prefix;
+// every equality of the rule (join keys, residuals, self-equalities) is
+// re-derived from the variable classes. Returns false (p unchanged) when no
+// such connected order exists.
+bool delta_first_plan(const Plan& p, u32 d, Plan& out) {
+    const u32 ns = static_cast<u32>(p.sources.size());
+    if (d == 0 || d >= ns) return false;
+    std::vector<u32> base(ns + 1, 0);
+    for (u32 s = 0; s < ns; ++s) base[s + 1] = base[s] + p.sources[s].arity;
+    std::vector<u32> parent(base[ns]);
+    for (u32 i = 0; i < parent.size(); ++i) parent[i] = i;
+    std::function<u32(u32)> find = [&](u32 x) { return parent[x] == x ? x : parent[x] = find(parent[x]); };
+    auto unite = [&](u32 a, u32 b) { parent[find(a)] = find(b); };
+    auto node = [&](const ColRef& r) { return base[r.source] + r.col; };
+    for (u32 k = 0; k < p.joins.size(); ++k) {
+        const PlanJoin& j = p.joins[k];
+        unite(node(j.left), base[j.right_source] + j.right_col);
+        for (auto& [l, rc] : j.residual_eq) unite(node(l), base[j.right_source] + rc);
+    }
+    for (u32 s = 0; s < ns; ++s)
+        for (auto& [a, b] : p.sources[s].self_eqs) unite(base[s] + a, base[s] + b);
+    std::vector<u32> order{d};
+    std::vector<bool> used(ns, false);
+    used[d] = true;
+    std::map<u32, ColRef> rep;  // class -> first joined occurrence (new numbering)
+    for (u32 c = 0; c < p.sources[d].arity; ++c) rep.emplace(find(base[d] + c), ColRef{0, c});
+    out = Plan();
+    out.head = p.head;
+    out.head_arity = p.head_arity;
+    out.sources.push_back(p.sources[d]);
+    while (order.size() < ns) {
+        bool found = false;
+        for (u32 t = 0; t < ns && !found; ++t) {
+            if (used[t]) continue;
+            PlanJoin jn;
+            bool have_key = false;
+            for (u32 c = 0; c < p.sources[t].arity; ++c) {
+                auto it = rep.find(find(base[t] + c));
+                if (it == rep.end()) continue;
+                if (!have_key) {
+                    jn.left = it->second;
+                    jn.right_col = c;
+                    have_key = true;
+                } else {
+                    jn.residual_eq.emplace_back(it->second, c);
+                }
+            }
+            if (!have_key) continue;
+            const u32 pos = static_cast<u32>(order.size());
+            jn.right_source = pos;
+            for (u32 c = 0; c < p.sources[t].arity; ++c) rep.emplace(find(base[t] + c), ColRef{pos, c});
+            out.sources.push_back(p.sources[t]);
+            out.joins.push_back(std::move(jn));
+            order.push_back(t);
+            used[t] = true;
+            found = true;
+        }
+        if (!found) return false;  // no connected order (cross product)
+    }
+    std::vector<u32> new_of(ns);
+    for (u32 i = 0; i < ns; ++i) new_of[order[i]] = i;
+    for (const ColRef& r : p.output_cols) out.output_cols.push_back(ColRef{new_of[r.source], r.col});
+    out.guard_neq = p.guard_neq;
+    return true;
+}
 
 DistPlan dist_plan(const Plan& p, const std::set<std::string>& idb) {
     DistPlan d;
@@ -347,6 +426,9 @@ public:
             c_->sync();
             const u64 T = c_->pinned[0];
             counts.reset();
+            if (trace_)
+                std::fprintf(stderr, "[fvlog]   %s join %zu/%zu delta@%ld probe=%llu outputs=%llu\n", plan.head.c_str(), k,
+                             nj, delta_source, static_cast<unsigned long long>(n), static_cast<unsigned long long>(T));
             if (!D && T == 0) return;
 
             const bool last = k + 1 == nj;
@@ -370,13 +452,20 @@ public:
                 for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot_of(plan.output_cols[h]);
                 if (sink) {
                     // Fused dedup: the join kernel inserts into FULL's key set.
+                    // Output chunks bound what the key set and the new-key
+                    // buffer must be sized for: each chunk may add at most its
+                    // own size, and the real count is re-read between chunks
+                    // (CSPA joins produce ~10^3 candidates per new row).
                     RelState& hr = rel(plan.head);
-                    hash_reserve(hr, *sink, T);
-                    spec.ht_slots = hr.keys.slots.get();
-                    spec.ht_mask = hr.keys.mask;
-                    spec.new_keys = sink->keys.get();
-                    spec.new_count = sink->counter.get();
-                    engine_materialize(c_, offsets.get(), n, T, starts.get(), spec);
+                    for (u64 t0 = 0; t0 < T; t0 += kFusedChunk) {
+                        const u64 t1 = std::min(T, t0 + kFusedChunk);
+                        hash_reserve(hr, *sink, t1 - t0);
+                        spec.ht_slots = hr.keys.slots.get();
+                        spec.ht_mask = hr.keys.mask;
+                        spec.new_keys = sink->keys.get();
+                        spec.new_count = sink->counter.get();
+                        engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
+                    }
                     return;
                 }
                 out.reserve(c_, T);
@@ -407,6 +496,9 @@ public:
                 return;
             }
             next.n = produced;
+            u32 bound_cols = 0;
+            for (u32 s = 0; s <= R; ++s) bound_cols += plan.sources[s].arity;
+            if (spec.n_out < bound_cols) maybe_dedup_inter(next, std::make_tuple(&plan, k, delta_source));
             cur = std::move(next);
             if (!D && cur.n == 0) return;
         }
@@ -434,6 +526,63 @@ public:
         u64 produced = cur.n;
         if (spec.n_filters) c_->read_scalars(spec.d_count, &produced, 1);
         out.n += produced;
+    }
+
+    // Distinct rows of a join intermediate that dropped columns. The join
+    // multiplies duplicates: in CSPA's valueAlias(x,y) :- valueFlow(z,x),
+    // memoryAlias(z,w), valueFlow(w,y) the (x,w) pairs repeat once per z and
+    // every repeat would re-derive all of valueFlow(w,_). Sets are unchanged
+    // (the reference keeps every id pair; results are compared as sets).
+    // Adaptive per plan step and variant: an intermediate of at least
+    // kInterProbeRows rows is deduplicated and measured; the step keeps
+    // deduplicating once a measurement removed >= 1/4 of the rows, and is
+    // re-measured whenever its intermediates grow 4x past the last
+    // measurement (early iterations often have no repeats yet).
+    using InterKey = std::tuple<const Plan*, size_t, long>;
+    struct InterPolicy {
+        bool on = false;
+        u64 measured = 0;  // size of the last measured intermediate (0: never)
+    };
+    static constexpr u64 kInterProbeRows = u64(1) << 16;
+
+    void maybe_dedup_inter(Inter& x, const InterKey& key) {
+        const u32 a = static_cast<u32>(x.owned.size());
+        if (a == 0 || a > FV_MAX_ARITY || x.n < 2 || x.owned.size() != x.cols.size()) return;
+        InterPolicy& policy = inter_policy_[key];
+        const bool measure = !policy.on && x.n >= kInterProbeRows &&
+                             (policy.measured == 0 || x.n >= 4 * policy.measured);
+        if (!policy.on && !measure) return;
+        std::vector<const u32*> cols;
+        for (auto& b : x.owned) cols.push_back(b.get());
+        const u32 W = (a + 1) / 2;
+        std::vector<DBuf<u64>> words;
+        std::vector<u64*> wp;
+        for (u32 w = 0; w < W; ++w) {
+            words.emplace_back(c_, x.n);
+            wp.push_back(words.back().get());
+        }
+        engine_pack_keys(c_, cols, x.n, st_.key_shift, wp.data());
+        engine_sort_keys(c_, words, x.n, a, st_.key_shift);
+        std::vector<DBuf<u32>> out;
+        std::vector<u32*> op;
+        for (u32 j = 0; j < a; ++j) {
+            out.emplace_back(c_, x.n);
+            op.push_back(out.back().get());
+        }
+        const u64 k = engine_unique_unpack(c_, words, x.n, a, st_.key_shift, op);
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   intermediate dedup %llu -> %llu (%s)\n", static_cast<unsigned long long>(x.n),
+                         static_cast<unsigned long long>(k), policy.on ? "on" : "measured");
+        if (measure) {
+            policy.measured = x.n;
+            policy.on = 4 * k <= 3 * x.n;
+        }
+        // x.cols maps ColRefs to the owned buffers in order of creation.
+        std::map<const u32*, u32*> remap;
+        for (u32 j = 0; j < a; ++j) remap[x.owned[j].get()] = op[j];
+        for (auto& [ref, ptr] : x.cols) ptr = remap.at(ptr);
+        x.owned = std::move(out);
+        x.n = k;
     }
 
     // Sort candidates and fold them into (full, delta); returns |DELTA|.
@@ -572,7 +721,11 @@ public:
         // bound counts every candidate as new, so the real load stays far
         // below the 3/4 worst case the table is sized for.
         if (4 * (r.keys.count + s.bound) <= 3 * r.keys.capacity()) return;
+        // Re-read the real count before growing: a stale bound (earlier
+        // chunks counted as all-new) must not trigger a rehash.
         const u64 pending = sink_count(s);
+        s.bound = pending + extra;
+        if (4 * (r.keys.count + s.bound) <= 3 * r.keys.capacity()) return;
         u64 cap = 1u << 16;
         while (cap < 2 * (r.keys.count + pending + extra)) cap <<= 1;
         KeySet ns;
@@ -580,19 +733,10 @@ public:
         ns.mask = cap - 1;
         ns.count = r.keys.count;
         FV_CUDA(cudaMemsetAsync(ns.slots.get(), 0xff, 8 * cap, c_->stream));
-        // Re-insert FULL's rows and the keys already found new this iteration.
-        auto reinsert_rows = [&](const DevVersion& v) {
-            if (!v.n) return;
-            DBuf<u64> k(c_, v.n);
-            u64* kp = k.get();
-            engine_pack_keys(c_, v.ptrs(), v.n, st_.key_shift, &kp);
-            engine_hash_insert(c_, k.get(), v.n, ns, nullptr, nullptr);
-        };
-        if (r.levels_mode)
-            for (auto& lv : r.levels) reinsert_rows(lv);
-        else
-            reinsert_rows(r.full);
-        engine_hash_insert(c_, s.keys.get(), pending, ns, nullptr, nullptr);
+        // The old table holds FULL's keys and the ones found new so far this
+        // iteration (a relation's keys only ever enter through its table):
+        // move them all in one streaming pass over its slots.
+        if (r.keys.capacity()) engine_hash_rehash(c_, r.keys, ns);
         r.keys = std::move(ns);
     }
 
@@ -662,6 +806,8 @@ public:
 private:
     Ctx* c_;
     EvalState& st_;
+    std::map<InterKey, InterPolicy> inter_policy_;
+    const bool trace_ = std::getenv("FVLOG_TRACE") != nullptr;
     u32 world_ = 1, rank_ = 0;
 };
 
@@ -768,27 +914,6 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     Engine eng(c, *st);
     st->rank = static_cast<int>(eng.rank());
     st->world = static_cast<int>(eng.world());
-    // Partition copies each IDB relation needs (static in the plans).
-    if (eng.dist()) {
-        for (auto& [name, r] : st->relations)
-            if (r->idb) r->keyset.insert(0);
-        for (auto& p : plans) {
-            const DistPlan dp = dist_plan(p, idb);
-            for (u32 s = 0; s < p.sources.size(); ++s) {
-                RelState& r = *st->relations.at(p.sources[s].relation);
-                if (r.idb) r.keyset.insert(dp.src_copy[s]);
-            }
-        }
-        for (auto& [name, r] : st->relations)
-            for (u32 kc : r->keyset)
-                if (kc != 0) {
-                    auto cp = std::make_unique<RelCopy>();
-                    cp->full.cols.resize(r->arity);
-                    cp->delta.cols.resize(r->arity);
-                    r->copies.emplace(kc, std::move(cp));
-                }
-    }
-
     // ---- gather the resident EDB blocks, key shift from the active domain ----
     std::map<std::string, std::vector<const DevVersion*>> by_rel;
     for (const DeviceEdb* e : edbs)
@@ -848,25 +973,69 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     struct Variant {
         const Plan* plan;
         long delta_source;
-        size_t plan_index;
+        size_t plan_index;  // index into dplans
     };
     std::vector<DistPlan> dplans;
-    for (auto& p : plans) dplans.push_back(dist_plan(p, idb));
+    std::deque<Plan> reordered;  // delta-first plans (stable addresses)
     std::vector<Variant> variants;
     std::set<std::string> full_read;  // relations whose FULL some variant reads
+    // FVLOG_JOIN_ORDER=rule keeps every variant in the rule's atom order.
+    const char* order_env = std::getenv("FVLOG_JOIN_ORDER");
+    const bool delta_first = !(order_env && std::string(order_env) == "rule");
     for (size_t i = 0; i < plans.size(); ++i) {
         const Plan& p = plans[i];
         bool any = false;
         for (size_t s = 0; s < p.sources.size(); ++s)
             if (idb.count(p.sources[s].relation)) {
-                variants.push_back({&p, static_cast<long>(s), i});
+                Plan rp;
+                // Only chains of >= 3 atoms where an IDB atom precedes DELTA
+                // (the rule order would join two growing FULL relations
+                // first); for two atoms the rule order probes FULL against
+                // DELTA's index, cheaper than a per-iteration sorted copy of
+                // FULL on another column, and an EDB prefix is fixed-size.
+                bool idb_before = false;
+                for (size_t q = 0; q < s; ++q) idb_before = idb_before || idb.count(p.sources[q].relation) > 0;
+                if (delta_first && idb_before && p.sources.size() >= 3 &&
+                    delta_first_plan(p, static_cast<u32>(s), rp)) {
+                    reordered.push_back(std::move(rp));
+                    dplans.push_back(dist_plan(reordered.back(), idb));
+                    variants.push_back({&reordered.back(), 0, dplans.size() - 1});
+                } else {
+                    dplans.push_back(dist_plan(p, idb));
+                    variants.push_back({&p, static_cast<long>(s), dplans.size() - 1});
+                }
                 any = true;
             }
-        if (!any) variants.push_back({&p, -1, i});
+        if (!any) {
+            dplans.push_back(dist_plan(p, idb));
+            variants.push_back({&p, -1, dplans.size() - 1});
+        }
     }
     for (auto& v : variants)
         for (size_t s = 0; s < v.plan->sources.size(); ++s)
             if (static_cast<long>(s) != v.delta_source) full_read.insert(v.plan->sources[s].relation);
+    // Partition copies each IDB relation needs (static in the executed variant plans).
+    if (eng.dist()) {
+        for (auto& [name, r] : st->relations)
+            if (r->idb) r->keyset.insert(0);
+        for (auto& v : variants) {
+            const Plan& p = *v.plan;
+            const DistPlan& dp = dplans[v.plan_index];
+            for (u32 s = 0; s < p.sources.size(); ++s) {
+                RelState& r = *st->relations.at(p.sources[s].relation);
+                if (r.idb) r.keyset.insert(dp.src_copy[s]);
+            }
+        }
+        for (auto& [name, r] : st->relations)
+            for (u32 kc : r->keyset)
+                if (kc != 0) {
+                    auto cp = std::make_unique<RelCopy>();
+                    cp->full.cols.resize(r->arity);
+                    cp->delta.cols.resize(r->arity);
+                    r->copies.emplace(kc, std::move(cp));
+                }
+    }
+
     // Dedup strategy per relation: a key set for binary/unary relations (keys
     // are one u64 word that can never equal the empty slot), the sort +
     // merge-path pipeline otherwise. FVLOG_DEDUP=sort forces the latter.

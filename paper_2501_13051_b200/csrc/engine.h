@@ -245,6 +245,15 @@ struct OutSpec {
 // Insert n keys; the ones not yet present are appended to
 // new_keys[*d_new ...] (device counter, not reset here).
 void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_keys, u64* d_new);
+// Move every key of `from` into the (larger, emptied) `to` by scanning
+// from's slots in order: with the same hash, a key's home in `to` is its old
+// slot plus a multiple of from's capacity, so the inserts stream through L2
+// instead of landing at random (to.count is not touched).
+void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to);
+// Distinct rows of lexicographically sorted packed keys -> SoA columns
+// (arity <= FV_MAX_ARITY); returns the distinct count.
+u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift,
+                         const std::vector<u32*>& cols);
 // Keys -> SoA columns (one word per row, arity <= 2).
 void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, const std::vector<u32*>& cols);
 
@@ -259,9 +268,11 @@ void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, c
                         u32* starts, u32* counts);
 // Ascending ids of rows passing `pred` (side 0); returns the count.
 u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids);
-// Output-partitioned expansion of T join outputs into `spec`.
+// Output-partitioned expansion of T join outputs into `spec`; only outputs
+// [o_begin, o_end) when given (chunked fused dedup; positional writes of the
+// uncompacted mode stay global output indices).
 void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32* starts,
-                        const OutSpec& spec);
+                        const OutSpec& spec, u64 o_begin = 0, u64 o_end = ~u64(0));
 // Single-source projection of n rows (side 0 only) into `spec`.
 void engine_project(Ctx* c, u64 n, const OutSpec& spec);
 // RLE of a sorted key column into (ukeys, ustart, ucount) + hash table.

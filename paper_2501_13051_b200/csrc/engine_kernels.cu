@@ -190,10 +190,10 @@ __device__ __forceinline__ u32 block_excl_u32(u32 v, u32* s_warp, u32* total) {
 }
 
 // First and last source row of every output tile (parallel binary searches).
-__global__ void tile_rows_kernel(const u64* __restrict__ offsets, u64 m, u64 total, u64 tiles,
+__global__ void tile_rows_kernel(const u64* __restrict__ offsets, u64 m, u64 o_begin, u64 total, u64 tiles,
                                  u64* __restrict__ jlo, u64* __restrict__ jhi) {
     GRID_STRIDE(b, tiles) {
-        const u64 o0 = b * kMatTile;
+        const u64 o0 = o_begin + b * kMatTile;
         const u64 o_end = min(o0 + kMatTile, total);
         jlo[b] = upper_bound_u64(offsets, m + 1, o0) - 1;
         jhi[b] = upper_bound_u64(offsets, m + 1, o_end - 1) - 1;
@@ -203,7 +203,8 @@ __global__ void tile_rows_kernel(const u64* __restrict__ offsets, u64 m, u64 tot
 // Output-partitioned join expansion (see lbs_kernel in column_ops.cu).
 template <bool COMPACT>
 __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __restrict__ offsets, u64 m,
-                                                                 u64 total, const u32* __restrict__ starts,
+                                                                 u64 o_begin, u64 total,
+                                                                 const u32* __restrict__ starts,
                                                                  const u64* __restrict__ tile_jlo,
                                                                  const u64* __restrict__ tile_jhi,
                                                                  OutSpec spec) {
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
     const u32 tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     if (spec.ht_slots)
         for (u32 i = tid; i < kMatSetSlots; i += kMatBlock) s_set[i] = ~0ull;
-    const u64 o0 = u64(blockIdx.x) * kMatTile;
+    const u64 o0 = o_begin + u64(blockIdx.x) * kMatTile;
     const u64 o_end = min(o0 + kMatTile, total);
     const u64 jlo = tile_jlo[blockIdx.x], jhi = tile_jhi[blockIdx.x];
     // A tile whose source rows span far more than its outputs is mostly
@@ -685,6 +686,23 @@ __global__ void hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n, u64
     }
 }
 
+// One tile of consecutive old slots per block (not grid-stride): blocks run
+// roughly in index order, so the inserts of all resident blocks fall into a
+// few narrow windows of the new table that stay in L2.
+constexpr int kRehashItems = 8;
+__global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __restrict__ to, u64 mask) {
+    const u64 base = u64(blockIdx.x) * blockDim.x * kRehashItems + threadIdx.x;
+    u64 key[kRehashItems];
+#pragma unroll
+    for (int k = 0; k < kRehashItems; ++k) {
+        const u64 i = base + u64(k) * blockDim.x;
+        key[k] = i < n ? __ldcs(from + i) : kEmptySlot;
+    }
+#pragma unroll
+    for (int k = 0; k < kRehashItems; ++k)
+        if (key[k] != kEmptySlot) keyset_insert_probe_from(to, mask, key[k], mix64(key[k]) & mask);
+}
+
 __global__ void unpack_keys_kernel(const u64* __restrict__ keys, u64 n, u32 arity, u32 shift, u32* c0, u32* c1) {
     const u64 lo_mask = (u64(1) << shift) - 1;
     GRID_STRIDE(i, n) {
@@ -697,6 +715,34 @@ __global__ void unpack_keys_kernel(const u64* __restrict__ keys, u64 n, u32 arit
         }
     }
 }
+
+// Distinct rows of sorted packed keys, unpacked into SoA columns (one
+// look-back compaction: a row is kept when any word differs from its
+// predecessor's).
+struct UniqueUnpackOp {
+    Words4 w;
+    u32 words, arity, shift;
+    OutCols8 out;
+    __device__ u64 value(u64 i) const {
+        if (i == 0) return 1;
+        for (u32 k = 0; k < words; ++k)
+            if (w.p[k][i] != w.p[k][i - 1]) return 1;
+        return 0;
+    }
+    __device__ void emit(u64 i, u64 pos, u64 v) const {
+        if (!v) return;
+        const u64 lo_mask = (u64(1) << shift) - 1;
+        for (u32 k = 0; k < words; ++k) {
+            const u64 x = w.p[k][i];
+            if (2 * k + 1 < arity) {
+                out.p[2 * k][pos] = static_cast<u32>(x >> shift);
+                out.p[2 * k + 1][pos] = static_cast<u32>(x & lo_mask);
+            } else {
+                out.p[2 * k][pos] = static_cast<u32>(x);
+            }
+        }
+    }
+};
 
 constexpr int kMaxRanks = 64;
 
@@ -767,6 +813,17 @@ void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_ke
     c->count_launch();
 }
 
+void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to) {
+    const u64 n = from.capacity();
+    if (!n) return;
+    // Algorithmic bytes: the old table read once, each key written once.
+    ProfScope prof(c, "hash_rehash", double(n) * 8.0 + double(from.count) * 8.0);
+    hash_rehash_kernel<<<static_cast<unsigned>(ceil_div(n, 256 * kRehashItems)), 256, 0, c->stream>>>(
+        from.slots.get(), n, to.slots.get(), to.mask);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
 void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, const std::vector<u32*>& cols) {
     if (!n) return;
     if (arity > 2) fail(FV_ERR_ARITY, "unpack_keys: arity > 2");
@@ -775,6 +832,26 @@ void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, co
                                                             arity == 2 ? cols[1] : nullptr);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
+}
+
+u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift,
+                         const std::vector<u32*>& cols) {
+    if (!n) return 0;
+    UniqueUnpackOp op{};
+    op.words = static_cast<u32>(words.size());
+    op.arity = arity;
+    op.shift = shift;
+    for (u32 k = 0; k < op.words; ++k) op.w.p[k] = const_cast<u64*>(words[k].get());
+    for (u32 j = 0; j < arity; ++j) op.out.p[j] = cols[j];
+    u64* d = c->d_scalars + 19;
+    {
+        ProfScope prof(c, "unique_unpack", double(n) * 8.0 * op.words);
+        tile_scan(c, op, n, d);
+    }
+    u64 k = 0;
+    c->read_scalars(d, &k, 1);
+    c->prof_add_bytes("unique_unpack", 4.0 * double(k) * arity);
+    return k;
 }
 
 u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids) {
@@ -803,34 +880,37 @@ void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, c
 }
 
 void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32* starts,
-                        const OutSpec& spec) {
-    if (!total) return;
-    const u64 tiles = ceil_div(total, kMatTile);
+                        const OutSpec& spec, u64 o_begin, u64 o_end) {
+    if (o_end > total) o_end = total;
+    if (o_begin >= o_end) return;
+    const u64 outs = o_end - o_begin;
+    const u64 tiles = ceil_div(outs, kMatTile);
     // Algorithmic bytes: per probe row its offset and run start; per output
-    // its build-side operands and the written row.
+    // its build-side operands and the written row. With the fused dedup
+    // (spec.ht_slots) the candidate row is never materialized; it is still
+    // charged as written once and read once by dedup (SURVEY.md §8d:
+    // 2 * 4h bytes per candidate), so the figure is the same implementation-
+    // independent lower bound as the unfused pipeline.
     double side1 = 0, side0 = 0;
     for (u32 k = 0; k < spec.n_out; ++k) (spec.col[k].side ? side1 : side0) += 4;
     for (u32 k = 0; k < spec.n_filters; ++k) {
         (spec.f[k].a.side ? side1 : side0) += 4;
         if (spec.f[k].op != kFilterConst) (spec.f[k].b.side ? side1 : side0) += 4;
     }
-    // With the fused dedup (spec.ht_slots) the candidate row is never
-    // materialized; it is still charged as written once and read once by
-    // dedup (2 * 4h bytes per candidate) so the figure is the
-    // same implementation-independent lower bound as the unfused pipeline.
     const double row_bytes = spec.key_mode ? 8.0 * ((spec.n_out + 1) / 2) : 4.0 * spec.n_out;
     const double out_bytes = spec.ht_slots ? 2.0 * row_bytes : row_bytes;
+    const double frac = double(outs) / double(total);  // a chunk reads its share of the probe rows
     DBuf<u64> rows(c, 2 * tiles);
-    tile_rows_kernel<<<grid_for(tiles), 256, 0, c->stream>>>(offsets, m, total, tiles, rows.get(),
+    tile_rows_kernel<<<grid_for(tiles), 256, 0, c->stream>>>(offsets, m, o_begin, o_end, tiles, rows.get(),
                                                              rows.get() + tiles);
     FV_CUDA(cudaGetLastError());
-    ProfScope prof(c, "join_materialize", double(m) * (12.0 + side0) + double(total) * (side1 + out_bytes));
+    ProfScope prof(c, "join_materialize", frac * double(m) * (12.0 + side0) + double(outs) * (side1 + out_bytes));
     if (spec.n_filters)
         materialize_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(
-            offsets, m, total, starts, rows.get(), rows.get() + tiles, spec);
+            offsets, m, o_begin, o_end, starts, rows.get(), rows.get() + tiles, spec);
     else
         materialize_kernel<false><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(
-            offsets, m, total, starts, rows.get(), rows.get() + tiles, spec);
+            offsets, m, o_begin, o_end, starts, rows.get(), rows.get() + tiles, spec);
     FV_CUDA(cudaGetLastError());
     c->count_launch(2);
 }

@@ -222,3 +222,53 @@ def test_both_dedup_strategies_match_reference(ctx, mode, monkeypatch):
         assert got == [tuple(s) for s in case["stats"]], (mode, case["name"])
         for rel, exp in case["relations"].items():
             assert matches(st.dump(rel).reshape(-1), exp["dump"]), (mode, case["name"], rel)
+
+
+def _check_relations(st, g):
+    rels = st.relations()
+    for rel, exp in g["relations"].items():
+        assert rels[rel][1] == exp["rows"], rel
+        assert str(st.fingerprint(rel)) == exp["fingerprint"], rel
+    deltas = st.delta_counts()
+    for rel, exp in g["relations"].items():
+        if rel in deltas:
+            assert deltas[rel] == exp["deltas"], rel
+    assert st.iterations == g["iterations"]
+
+
+def test_lubm_c5_full_size_against_reference(ctx):
+    """C5: OWL-RL/LUBM rule set on ~10.2 M facts vs the unmodified reference
+    (tests/golden/make_golden_large.py c5)."""
+    g = _large().get("C5")
+    if not g:
+        pytest.skip("C5 golden not generated")
+    st = E.evaluate_program(W.LUBM_PROGRAM, W.lubm_facts(340), ctx=ctx)
+    _check_relations(st, g)
+
+
+def test_cspa_c4_full_size_against_reference(ctx):
+    """C4: CSPA on 4000 disjoint functions vs the unmodified reference run
+    component-batch by component-batch (fingerprints, row counts and
+    per-iteration deltas add over disjoint components)."""
+    g = _large().get("C4")
+    if not g:
+        pytest.skip("C4 golden not generated")
+    st = E.evaluate_program(W.CSPA_PROGRAM, W.cspa_facts(4000, 100, 100, 70), ctx=ctx)
+    _check_relations(st, g)
+
+
+@pytest.mark.parametrize("order", ["rule", "delta"])
+def test_join_orders_match_reference(ctx, order, monkeypatch):
+    # FVLOG_JOIN_ORDER=rule: every variant joins in the rule's atom order
+    # (compile_rule); default: delta-first order for >= 3-atom variants with
+    # an IDB atom before DELTA. Both must give the reference's sets and stats.
+    monkeypatch.setenv("FVLOG_JOIN_ORDER", order)
+    for case in load_golden("engine.json"):
+        if case["name"] == "TC uniform 2000/10000":
+            continue
+        text, facts = golden_cases.program_and_facts(case)
+        st = E.evaluate_program(text, facts, ctx=ctx)
+        got = [(s.index, s.relation, s.delta_rows, s.full_rows, s.merges) for s in st.stats()]
+        assert got == [tuple(s) for s in case["stats"]], (order, case["name"])
+        for rel, exp in case["relations"].items():
+            assert matches(st.dump(rel).reshape(-1), exp["dump"]), (order, case["name"], rel)
