@@ -386,7 +386,7 @@ def main():
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
-    ap.add_argument("--reserve-gb", type=float, default=64.0, help="fv_ctx_reserve before warm-up")
+    ap.add_argument("--reserve-gb", type=float, default=96.0, help="fv_ctx_reserve before warm-up")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_impl(args)

@@ -54,7 +54,7 @@ namespace {
 using Clock = std::chrono::steady_clock;
 
 // Join outputs per fused join+dedup launch (see exec_variant).
-constexpr u64 kFusedChunk = u64(1) << 27;
+constexpr u64 kFusedChunk = u64(1) << 28;
 
 double ms_since(Clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
@@ -718,16 +718,19 @@ public:
             s.cap = nc;
         }
         s.bound += extra;
-        // bound counts every candidate as new, so the real load stays far
-        // below the 3/4 worst case the table is sized for.
-        if (4 * (r.keys.count + s.bound) <= 3 * r.keys.capacity()) return;
+        // bound counts every candidate as new, so the real load stays below
+        // the 1/2 worst case the table is checked against.
+        if (2 * (r.keys.count + s.bound) <= r.keys.capacity()) return;
         // Re-read the real count before growing: a stale bound (earlier
         // chunks counted as all-new) must not trigger a rehash.
         const u64 pending = sink_count(s);
         s.bound = pending + extra;
-        if (4 * (r.keys.count + s.bound) <= 3 * r.keys.capacity()) return;
+        if (2 * (r.keys.count + s.bound) <= r.keys.capacity()) return;
+        // Grow to a worst-case load of 1/4: most probes of a fused join are
+        // repeats of present keys, and short linear-probe runs keep them to
+        // one DRAM access; 4x growth also keeps the number of rehashes low.
         u64 cap = 1u << 16;
-        while (cap < 2 * (r.keys.count + pending + extra)) cap <<= 1;
+        while (cap < 4 * (r.keys.count + pending + extra)) cap <<= 1;
         KeySet ns;
         ns.slots = DBuf<u64>(c_, cap);
         ns.mask = cap - 1;

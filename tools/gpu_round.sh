@@ -26,6 +26,11 @@ if [ -z "${SKIP_BENCH:-}" ]; then
   echo "bench exit $?" >> "$OUT/bench.err"
 fi
 
+if [ -z "${SKIP_WORKLOADS:-}" ]; then
+  timeout 1500 python tools/bench_workloads.py --out "$OUT/workloads.json" > "$OUT/workloads.log" 2>&1
+  echo "workloads exit $?" >> "$OUT/workloads.log"
+fi
+
 if [ -z "${SKIP_NCU:-}" ]; then
   NCU=/usr/local/cuda/bin/ncu
   timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
