@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfvlog.so")
+# FVLOG_LIB: load another build of the library (kernel-variant experiments).
+LIB_PATH = os.environ.get("FVLOG_LIB") or os.path.join(_HERE, "libfvlog.so")
 
 u32p = C.POINTER(C.c_uint32)
 u64p = C.POINTER(C.c_uint64)

@@ -457,6 +457,10 @@ public:
                     // own size, and the real count is re-read between chunks
                     // (CSPA joins produce ~10^3 candidates per new row).
                     RelState& hr = rel(plan.head);
+                    if (trace_) {
+                        spec.probe_count = c_->d_scalars + 24;
+                        FV_CUDA(cudaMemsetAsync(spec.probe_count, 0, 8, c_->stream));
+                    }
                     for (u64 t0 = 0; t0 < T; t0 += kFusedChunk) {
                         const u64 t1 = std::min(T, t0 + kFusedChunk);
                         hash_reserve(hr, *sink, t1 - t0);
@@ -465,6 +469,12 @@ public:
                         spec.new_keys = sink->keys.get();
                         spec.new_count = sink->counter.get();
                         engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
+                    }
+                    if (trace_) {
+                        u64 probes = 0;
+                        c_->read_scalars(spec.probe_count, &probes, 1);
+                        std::fprintf(stderr, "[fvlog]   fused dedup: %llu candidates -> %llu key-set probes\n",
+                                     static_cast<unsigned long long>(T), static_cast<unsigned long long>(probes));
                     }
                     return;
                 }

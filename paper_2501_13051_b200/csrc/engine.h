@@ -240,6 +240,7 @@ struct OutSpec {
     u64 ht_mask = 0;
     u64* new_keys = nullptr;
     u64* new_count = nullptr;
+    u64* probe_count = nullptr;  // optional (trace): key-set probes after the tile-local dedup
 };
 
 // Insert n keys; the ones not yet present are appended to

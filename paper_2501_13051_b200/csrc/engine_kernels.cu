@@ -299,6 +299,10 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
             }
             hs[k] &= spec.ht_mask;
         }
+        if (spec.probe_count) {
+            const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
+            if (lane == 0 && m) atomicAdd(reinterpret_cast<unsigned long long*>(spec.probe_count), static_cast<unsigned long long>(m));
+        }
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) sv[k] = ((keep_mask >> k) & 1u) ? __ldcg(spec.ht_slots + hs[k]) : 0;
 #pragma unroll
@@ -904,7 +908,9 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
     tile_rows_kernel<<<grid_for(tiles), 256, 0, c->stream>>>(offsets, m, o_begin, o_end, tiles, rows.get(),
                                                              rows.get() + tiles);
     FV_CUDA(cudaGetLastError());
-    ProfScope prof(c, "join_materialize", frac * double(m) * (12.0 + side0) + double(outs) * (side1 + out_bytes));
+    // The fused join + key-set dedup is profiled as "join_dedup".
+    ProfScope prof(c, spec.ht_slots ? "join_dedup" : "join_materialize",
+                   frac * double(m) * (12.0 + side0) + double(outs) * (side1 + out_bytes));
     if (spec.n_filters)
         materialize_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(
             offsets, m, o_begin, o_end, starts, rows.get(), rows.get() + tiles, spec);

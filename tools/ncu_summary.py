@@ -24,6 +24,7 @@ from launch_summary import summarise  # noqa: E402
 
 # bench.py / fv_ctx_profile names -> CUDA kernel names in the launch list
 PROFILER_TO_KERNEL = {
+    "join_dedup": "materialize_kernel<0>",
     "join_materialize": "materialize_kernel<0>",
     "hash_insert": "hash_insert_keys_kernel",
     "radix_onesweep_u64": "onesweep_kernel<unsigned long, 0>",
@@ -86,11 +87,16 @@ def main(src, dst):
         if os.path.exists(os.path.join(src, f)):
             shutil.copy(os.path.join(src, f), os.path.join(dst, f))
     summary = {"round_dir": dst, "kernels": {}}
-    for prof, kern in PROFILER_TO_KERNEL.items():
-        if kern in launches:
-            k = launches[kern]
-            summary["kernels"][prof] = {"kernel": kern, "dram_bytes_per_launch": k["dram_bytes_per_launch"],
-                                        "launches_per_step": k["launches"], "share_of_step": k["share"]}
+    for prof, kerns in PROFILER_TO_KERNEL.items():
+        kerns = kerns if isinstance(kerns, list) else [kerns]
+        ks = [launches[k] for k in kerns if k in launches]
+        if not ks:
+            continue
+        n = sum(k["launches"] for k in ks)
+        by = sum((k["dram_read_gb"] + k["dram_write_gb"]) * 1e9 for k in ks)
+        summary["kernels"][prof] = {"kernel": " + ".join(k for k in kerns if k in launches),
+                                    "dram_bytes_per_launch": by / n, "launches_per_step": n,
+                                    "share_of_step": sum(k["share"] for k in ks)}
     json.dump(summary, open(os.path.join(os.path.dirname(dst.rstrip("/")), "ncu_summary.json"), "w"), indent=1)
 
 
