@@ -7,12 +7,13 @@
 // reference's strict (value, id) order, so sorted_idx is bit-identical.
 //
 // Per sort: one histogram kernel computes all digit histograms in a single
-// read of the keys (warp-aggregated shared atomics via __match_any_sync), a
+// read of the keys (shared atomics, warp-uniform digits added once), a
 // tiny kernel turns them into per-digit global bases, then one onesweep
 // kernel per 8-bit digit reads each key once and writes it once:
 //   - tile of BLOCK*ITEMS keys in a warp-striped arrangement (coalesced
 //     128-bit-friendly loads; lane order == input order so ranking is stable)
-//   - per-warp digit ranks with __match_any_sync, per-warp shared histograms
+//   - per-warp digit ranks (peer lanes from one ballot per digit bit),
+//     per-warp shared histograms
 //   - decoupled look-back across tiles per digit (status words carry an epoch
 //     so no clearing between passes)
 //   - shared-memory exchange so global stores are runs of one digit.
@@ -28,15 +29,23 @@ constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortBlock = 256;
 constexpr int kSortWarps = kSortBlock / 32;
 
+#ifndef FV_SORT_ITEMS_U32
+#define FV_SORT_ITEMS_U32 16
+#endif
+#ifndef FV_SORT_ITEMS_U64
+#define FV_SORT_ITEMS_U64 16
+#endif
+
+
 template <typename K>
 struct SortTraits;
 template <>
 struct SortTraits<u32> {
-    static constexpr int kItems = 16;
+    static constexpr int kItems = FV_SORT_ITEMS_U32;
 };
 template <>
 struct SortTraits<u64> {
-    static constexpr int kItems = 12;
+    static constexpr int kItems = FV_SORT_ITEMS_U64;
 };
 
 template <typename K>
@@ -46,32 +55,48 @@ __device__ __forceinline__ u32 digit_of(K key, u32 shift, u32 mask) {
 
 // ---- histogram over all passes -------------------------------------------
 
+// One read of the keys computes every pass's digit histogram. Two shared
+// copies per pass (even/odd warps) take plain shared atomics; a warp whose
+// 32 digits are all equal (sorted or skewed input: high digits of packed row
+// keys often are) adds 32 once instead of 32 conflicting atomics.
+constexpr int kHistItems = 8;
 template <typename K>
 __global__ void __launch_bounds__(256) radix_hist_kernel(const K* __restrict__ keys, u64 n,
                                                          u32 begin_bit, u32 end_bit, u32 npass,
                                                          unsigned long long* __restrict__ hist) {
-    __shared__ u32 s_hist[8][kRadix];
-    for (u32 i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+    __shared__ u32 s_hist[2][8][kRadix];
+    for (u32 i = threadIdx.x; i < 2 * 8 * kRadix; i += blockDim.x) (&s_hist[0][0][0])[i] = 0;
     __syncthreads();
-    const u32 lane = lane_id();
-    const u64 stride = u64(gridDim.x) * blockDim.x;
-    // Whole warps iterate together so __match_any_sync sees full masks.
-    const u64 n_round = ceil_div(n, 32) * 32;
-    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n_round; i += stride) {
-        const bool valid = i < n;
-        const K key = valid ? keys[i] : K(0);
-        for (u32 p = 0; p < npass; ++p) {
-            const u32 shift = begin_bit + p * kRadixBits;
-            const u32 bits = min(u32(kRadixBits), end_bit - shift);
-            const u32 d = valid ? digit_of(key, shift, (1u << bits) - 1) : 0xffffu;
-            const u32 peers = __match_any_sync(0xffffffffu, d);
-            if (valid && lane == static_cast<u32>(__ffs(peers) - 1))
-                atomicAdd(&s_hist[p][d], static_cast<u32>(__popc(peers)));
+    const u32 lane = lane_id(), copy = (threadIdx.x >> 5) & 1;
+    const u64 tile = u64(blockDim.x) * kHistItems;
+    for (u64 base = u64(blockIdx.x) * tile; base < n; base += u64(gridDim.x) * tile) {
+        K key[kHistItems];
+#pragma unroll
+        for (int k = 0; k < kHistItems; ++k) {
+            const u64 i = base + u64(k) * blockDim.x + threadIdx.x;
+            key[k] = i < n ? keys[i] : K(0);
+        }
+#pragma unroll
+        for (int k = 0; k < kHistItems; ++k) {
+            const u64 i = base + u64(k) * blockDim.x + threadIdx.x;
+            const bool valid = i < n;
+            // Warps are fully in or fully out of range except the last one.
+            const bool full = __all_sync(0xffffffffu, valid);
+            for (u32 p = 0; p < npass; ++p) {
+                const u32 shift = begin_bit + p * kRadixBits;
+                const u32 bits = min(u32(kRadixBits), end_bit - shift);
+                const u32 d = digit_of(key[k], shift, (1u << bits) - 1);
+                if (full && __all_sync(0xffffffffu, d == __shfl_sync(0xffffffffu, d, 0))) {
+                    if (lane == 0) atomicAdd(&s_hist[copy][p][d], 32u);
+                } else if (valid) {
+                    atomicAdd(&s_hist[copy][p][d], 1u);
+                }
+            }
         }
     }
     __syncthreads();
     for (u32 i = threadIdx.x; i < npass * kRadix; i += blockDim.x) {
-        const u32 v = (&s_hist[0][0])[i];
+        const u32 v = (&s_hist[0][0][0])[i] + (&s_hist[1][0][0])[i];
         if (v) atomicAdd(hist + i, static_cast<unsigned long long>(v));
     }
 }
@@ -151,7 +176,17 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         const u32 d = dig[k];
-        const u32 peers = __match_any_sync(0xffffffffu, d);
+        // Lanes with the same digit, from one ballot per digit bit (cheaper
+        // than match.any); out-of-range lanes only match each other.
+        const bool valid_item = d != 0xffffu;
+        u32 peers = __ballot_sync(0xffffffffu, valid_item);
+        if (!valid_item) peers = ~peers;
+#pragma unroll
+        for (int b = 0; b < kRadixBits; ++b) {
+            if (!((mask >> b) & 1u)) break;
+            const u32 x = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? x : ~x;
+        }
         const u32 leader = __ffs(peers) - 1;
         u32 b = 0;
         if (d != 0xffffu && lane == leader) {
@@ -236,6 +271,13 @@ void onesweep_pass(Ctx* c, const K* kin, K* kout, const u32* vin, u32* vout, u64
     u32* counter = nullptr;
     const u32 epoch = c->lookback_epoch(tiles * kRadix, &counter);
     const size_t smem = sizeof(K) * TILE + (HAS_VAL ? sizeof(u32) * TILE : 0);
+    // u64 keys + u32 payload need > 48 KB in total (opt-in, once per type).
+    static const bool smem_ok = [&] {
+        FV_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, HAS_VAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        return true;
+    }();
+    (void)smem_ok;
     ProfScope prof(c, sizeof(K) == 8 ? (HAS_VAL ? "radix_onesweep_u64_kv" : "radix_onesweep_u64")
                                      : (HAS_VAL ? "radix_onesweep_u32_kv" : "radix_onesweep_u32"),
                    2.0 * double(n) * (sizeof(K) + (HAS_VAL ? 4 : 0)));
@@ -257,7 +299,7 @@ bool radix_sort_impl(Ctx* c, K* keys, K* keys_alt, u32* vals, u32* vals_alt, u64
     u64* trivial = bins + u64(npass) * kRadix;
     FV_CUDA(cudaMemsetAsync(hist, 0, sizeof(u64) * npass * kRadix, c->stream));
     {
-        const u64 want = ceil_div(n, 256 * 8);
+        const u64 want = ceil_div(n, 256 * kHistItems);
         const unsigned grid = static_cast<unsigned>(want < u64(kNumSMs) * 8 ? (want ? want : 1)
                                                                              : u64(kNumSMs) * 8);
         ProfScope prof(c, "radix_histogram", double(n) * sizeof(K));
