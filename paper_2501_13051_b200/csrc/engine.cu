@@ -480,6 +480,9 @@ public:
                 }
                 out.reserve(c_, T);
                 for (u32 w = 0; w < W; ++w) spec.keys[w] = out.words[w].get() + out.n;
+                // One-word keys: drop tile-local repeats before they are
+                // pooled (and, partitioned, routed over NVLink).
+                if (W == 1) spec.tile_dedup = 1;
             } else {
                 spec.key_mode = 0;
                 u32 j = 0;
@@ -494,13 +497,14 @@ public:
                 }
                 spec.n_out = j;
             }
-            if (spec.n_filters) {
+            const bool compacts = spec.n_filters || spec.tile_dedup;
+            if (compacts) {
                 spec.d_count = c_->d_scalars + 20;
                 FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
             }
             engine_materialize(c_, offsets.get(), n, T, starts.get(), spec);
             u64 produced = T;
-            if (spec.n_filters) c_->read_scalars(spec.d_count, &produced, 1);
+            if (compacts) c_->read_scalars(spec.d_count, &produced, 1);
             if (last) {
                 out.n += produced;
                 return;

@@ -241,6 +241,9 @@ struct OutSpec {
     u64* new_keys = nullptr;
     u64* new_count = nullptr;
     u64* probe_count = nullptr;  // optional (trace): key-set probes after the tile-local dedup
+    // Key mode, one word, no key set: drop tile-local repeats and append the
+    // tile's distinct keys at keys[0][*d_count ...].
+    u32 tile_dedup = 0;
 };
 
 // Insert n keys; the ones not yet present are appended to

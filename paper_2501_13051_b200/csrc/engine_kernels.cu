@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
     __shared__ u64 s_base;
     __shared__ u32 s_warp[kMatBlock / 32 + 1];
     const u32 tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-    if (spec.ht_slots)
+    if (spec.ht_slots || spec.tile_dedup)
         for (u32 i = tid; i < kMatSetSlots; i += kMatBlock) s_set[i] = ~0ull;
     const u64 o0 = o_begin + u64(blockIdx.x) * kMatTile;
     const u64 o_end = min(o0 + kMatTile, total);
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
             if (!COMPACT || pass_filters(spec.f, spec.n_filters, i, p)) keep_mask |= 1u << k;
         }
     }
-    if (spec.ht_slots) {
+    if (spec.ht_slots || spec.tile_dedup) {
         // Fused dedup. First a tile-local key set in shared memory drops the
         // repeats inside the tile: consecutive outputs share the probe row's
         // head columns, so one derivation per tile and key reaches HBM (about
@@ -302,6 +302,22 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
         if (spec.probe_count) {
             const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
             if (lane == 0 && m) atomicAdd(reinterpret_cast<unsigned long long*>(spec.probe_count), static_cast<unsigned long long>(m));
+        }
+        if (spec.tile_dedup) {
+            // Pooled candidates (partitioned runs route them before dedup):
+            // append only the tile's distinct keys, one atomic per CTA.
+            u32 tot;
+            const u32 excl = block_excl_u32(__popc(keep_mask), s_warp, &tot);
+            if (tid == 0)
+                s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(spec.d_count),
+                                         static_cast<unsigned long long>(tot))
+                             : 0;
+            __syncthreads();
+            u64 pos = s_base + excl;
+#pragma unroll
+            for (int k = 0; k < kMatItems; ++k)
+                if (keep_mask & (1u << k)) spec.keys[0][pos++] = key[k];
+            return;
         }
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) sv[k] = ((keep_mask >> k) & 1u) ? __ldcg(spec.ht_slots + hs[k]) : 0;
