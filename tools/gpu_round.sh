@@ -37,7 +37,7 @@ if [ -z "${SKIP_NCU:-}" ]; then
       --clock-control none --csv --log-file "$OUT/launches.csv" \
       python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > "$OUT/ncu_launch_bench.log" 2>&1
   echo "ncu launches exit $?" >> "$OUT/ncu_launch_bench.log"
-  for KS in ${NCU_KERNELS:-materialize_kernel:4 onesweep_kernel:20 hash_insert_keys_kernel:8}; do
+  for KS in ${NCU_KERNELS:-materialize_kernel:6 onesweep_kernel:30 hash_rehash_kernel:1}; do
     K=${KS%%:*}; SKIP=${KS##*:}
     timeout 900 $NCU --set full --clock-control none --import-source on -k "regex:$K" \
         --launch-skip $SKIP -c ${NCU_COUNT:-1} -f -o "$OUT/full_$K" \
