@@ -12,6 +12,8 @@
 //   merge         dedup_rows + deduplicate + difference + merge_delta
 //                 (relation.cpp:71-108, kernels.cpp:210-268) as ONE
 //                 merge-path pass over sorted FULL and sorted candidates.
+#include <cstdlib>
+
 #include "engine.h"
 #include "prim.cuh"
 #include "radix_sort.h"
@@ -78,6 +80,26 @@ __global__ void probe_count_kernel(const u32* __restrict__ probe, u64 n, const u
 __device__ __forceinline__ u64 row_key1(const OutSpec& spec, u64 i, u64 p) {
     const u64 hi = slot(spec.col[0], i, p);
     return spec.n_out >= 2 ? (hi << spec.shift) | slot(spec.col[1], i, p) : hi;
+}
+
+// Key-set home slot: the low FV_KEYSET_GROUP_BITS bits of the key are kept
+// and the rest is scattered, so 2^bits keys that differ only there (same
+// first column, adjacent second-column ids) share a sector/line. A DRAM miss
+// costs a 128-byte line on this part (tools/membench.cu), so grouping cuts
+// DRAM bytes (C2: 215 -> 102 GB at 2 bits) — but repeated probes of a hub's
+// keys then concentrate on a few L2 lines and the fused join gets slower
+// (C2 141 -> 209 ms, C4 248 -> 333 ms); only SG, whose candidates are almost
+// all new, gains (76 -> 54 ms at 1 bit). Default: 0 (plain scattering).
+// Growth keeps the property the streaming rehash needs (new home = old home
+// + j * old capacity) for every setting.
+#ifndef FV_KEYSET_GROUP_BITS
+#define FV_KEYSET_GROUP_BITS 0
+#endif
+constexpr u32 kGroupBits = FV_KEYSET_GROUP_BITS;
+constexpr u64 kGroupMask = (u64(1) << kGroupBits) - 1;
+__device__ __forceinline__ u64 keyset_line_hash(u64 key) { return mix64(key >> kGroupBits); }
+__device__ __forceinline__ u64 keyset_home(u64 line_hash, u64 key, u64 mask) {
+    return ((line_hash << kGroupBits) | (key & kGroupMask)) & mask;
 }
 
 // Set-insert of one key: true when the key was absent (this thread inserted
@@ -200,24 +222,29 @@ __global__ void tile_rows_kernel(const u64* __restrict__ offsets, u64 m, u64 o_b
     }
 }
 
-// Output-partitioned join expansion (see lbs_kernel in column_ops.cu).
+struct MatShared {
+    u32 owner[kMatTile];
+    unsigned long long set[kMatSetSlots];  // tile-local key set (dedup modes only)
+    u64 base;
+    u32 warp[kMatBlock / 32 + 1];
+    u32 set_fill;                           // keys inserted into `set` since its last reset
+};
+
+// One output tile of the output-partitioned join expansion (see lbs_kernel in
+// column_ops.cu). All threads of the block call it for the same tile.
 template <bool COMPACT>
-__global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __restrict__ offsets, u64 m,
-                                                                 u64 o_begin, u64 total,
-                                                                 const u32* __restrict__ starts,
-                                                                 const u64* __restrict__ tile_jlo,
-                                                                 const u64* __restrict__ tile_jhi,
-                                                                 OutSpec spec) {
-    __shared__ u32 s_owner[kMatTile];
-    __shared__ unsigned long long s_set[kMatSetSlots];  // tile-local key set (fused dedup only)
-    __shared__ u64 s_base;
-    __shared__ u32 s_warp[kMatBlock / 32 + 1];
+__device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets, u64 o_begin, u64 total,
+                                                 const u32* __restrict__ starts, const u64* __restrict__ tile_jlo,
+                                                 const u64* __restrict__ tile_jhi, const OutSpec& spec, u64 t,
+                                                 MatShared& sh) {
+    u32* s_owner = sh.owner;
+    unsigned long long* s_set = sh.set;
+    u32* s_warp = sh.warp;
+    u64& s_base = sh.base;
     const u32 tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-    if (spec.ht_slots || spec.tile_dedup)
-        for (u32 i = tid; i < kMatSetSlots; i += kMatBlock) s_set[i] = ~0ull;
-    const u64 o0 = o_begin + u64(blockIdx.x) * kMatTile;
+    const u64 o0 = o_begin + t * kMatTile;
     const u64 o_end = min(o0 + kMatTile, total);
-    const u64 jlo = tile_jlo[blockIdx.x], jhi = tile_jhi[blockIdx.x];
+    const u64 jlo = tile_jlo[t], jhi = tile_jhi[t];
     // A tile whose source rows span far more than its outputs is mostly
     // zero-count rows (probe misses): marking would walk every one of them,
     // so each output binary-searches its row instead (block-uniform branch).
@@ -281,13 +308,13 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) {
             key[k] = ((keep_mask >> k) & 1u) ? row_key1(spec, ii[k], pp[k]) : 0;
-            hs[k] = mix64(key[k]);
+            hs[k] = keyset_line_hash(key[k]);
         }
         __syncthreads();  // s_set initialised (the sparse path has no barrier before this)
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) {
             if (!((keep_mask >> k) & 1u)) continue;
-            u32 h = static_cast<u32>(hs[k] >> 40) & (kMatSetSlots - 1);
+            u32 h = static_cast<u32>((hs[k] >> 40) + (key[k] & kGroupMask)) & (kMatSetSlots - 1);
             while (true) {
                 const unsigned long long prev = atomicCAS(s_set + h, ~0ull, static_cast<unsigned long long>(key[k]));
                 if (prev == ~0ull) break;                 // first in the tile
@@ -297,7 +324,11 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
                 }
                 h = (h + 1) & (kMatSetSlots - 1);
             }
-            hs[k] &= spec.ht_mask;
+            hs[k] = keyset_home(hs[k], key[k], spec.ht_mask);
+        }
+        {
+            const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
+            if (lane == 0 && m) atomicAdd(&sh.set_fill, m);
         }
         if (spec.probe_count) {
             const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
@@ -345,6 +376,37 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
 #pragma unroll
     for (int k = 0; k < kMatItems; ++k)
         if (keep_mask & (1u << k)) write_row(spec, pos++, ii[k], pp[k]);
+}
+
+// Dedup modes can walk `group` consecutive tiles per CTA and keep the
+// tile-local key set across them (reset once a quarter full, so a tile's
+// 2048 keys never push it past 3/4): a high-degree probe row's outputs span
+// many tiles and their repeats only meet when the set outlives one tile.
+// That halves TC's key-set probes, but the dropped ones were L2 hits and the
+// serialised tiles cost more than they save, so the default is one tile.
+constexpr int kMatGroup = 1;  // measured: 1 is best on C1-C4 (FVLOG_MAT_GROUP overrides)
+template <bool COMPACT>
+__global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __restrict__ offsets, u64 m,
+                                                                 u64 o_begin, u64 total,
+                                                                 const u32* __restrict__ starts,
+                                                                 const u64* __restrict__ tile_jlo,
+                                                                 const u64* __restrict__ tile_jhi, u64 tiles,
+                                                                 u32 group, OutSpec spec) {
+    __shared__ MatShared sh;
+    const bool dedup = spec.ht_slots || spec.tile_dedup;
+    const u64 t0 = u64(blockIdx.x) * group;
+    const u64 t1 = min(t0 + group, tiles);
+    for (u64 t = t0; t < t1; ++t) {
+        __syncthreads();  // previous tile's shared reads/updates are done
+        const bool reset = dedup && (t == t0 || sh.set_fill > kMatSetSlots / 4);
+        __syncthreads();  // every thread has read set_fill before it is cleared
+        if (reset) {
+            for (u32 i = threadIdx.x; i < kMatSetSlots; i += kMatBlock) sh.set[i] = ~0ull;
+            if (threadIdx.x == 0) sh.set_fill = 0;
+            __syncthreads();
+        }
+        materialize_tile<COMPACT>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh);
+    }
 }
 
 template <bool COMPACT>
@@ -694,7 +756,7 @@ __global__ void hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n, u64
     for (int k = 0; k < ITEMS; ++k) {
         const u64 i = base + u64(k) * blockDim.x;
         key[k] = i < n ? keys[i] : 0;
-        hs[k] = mix64(key[k]) & mask;
+        hs[k] = keyset_home(keyset_line_hash(key[k]), key[k], mask);
     }
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) sv[k] = (base + u64(k) * blockDim.x < n) ? __ldcg(slots + hs[k]) : 0;
@@ -720,7 +782,8 @@ __global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __r
     }
 #pragma unroll
     for (int k = 0; k < kRehashItems; ++k)
-        if (key[k] != kEmptySlot) keyset_insert_probe_from(to, mask, key[k], mix64(key[k]) & mask);
+        if (key[k] != kEmptySlot)
+            keyset_insert_probe_from(to, mask, key[k], keyset_home(keyset_line_hash(key[k]), key[k], mask));
 }
 
 __global__ void unpack_keys_kernel(const u64* __restrict__ keys, u64 n, u32 arity, u32 shift, u32* c0, u32* c1) {
@@ -927,12 +990,18 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
     // The fused join + key-set dedup is profiled as "join_dedup".
     ProfScope prof(c, spec.ht_slots ? "join_dedup" : "join_materialize",
                    frac * double(m) * (12.0 + side0) + double(outs) * (side1 + out_bytes));
+    static const u32 env_group = [] {
+        const char* e = std::getenv("FVLOG_MAT_GROUP");
+        return e ? static_cast<u32>(std::atoi(e)) : 0u;
+    }();
+    const u32 group = (spec.ht_slots || spec.tile_dedup) ? (env_group ? env_group : u32(kMatGroup)) : 1u;
+    const unsigned grid = static_cast<unsigned>(ceil_div(tiles, group));
     if (spec.n_filters)
-        materialize_kernel<true><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(
-            offsets, m, o_begin, o_end, starts, rows.get(), rows.get() + tiles, spec);
+        materialize_kernel<true><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, rows.get(),
+                                                                   rows.get() + tiles, tiles, group, spec);
     else
-        materialize_kernel<false><<<static_cast<unsigned>(tiles), kMatBlock, 0, c->stream>>>(
-            offsets, m, o_begin, o_end, starts, rows.get(), rows.get() + tiles, spec);
+        materialize_kernel<false><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, rows.get(),
+                                                                    rows.get() + tiles, tiles, group, spec);
     FV_CUDA(cudaGetLastError());
     c->count_launch(2);
 }
