@@ -93,7 +93,16 @@ struct HeadSink {
     u64 cap = 0;
     u64 bound = 0;  // host upper bound of the device count
     DBuf<u64> counter;
+    u64 candidates = 0;  // rows offered to the key set this iteration
 };
+
+// Key-set layout choice (KeySet::group_bits, see keyset_home in
+// engine_kernels.cu): group pairs of adjacent keys while a relation's
+// candidates are (almost) all new rows (<= kGroupedRatio candidates per new row in
+// the last iteration), scatter every key otherwise. FVLOG_KEYSET_GROUP=0/1
+// forces one layout; FVLOG_GROUP_RATIO overrides the threshold (1.05-1.2
+// measured equal; 1.5 switches TC one iteration too late).
+constexpr double kGroupedRatio = 1.1;
 
 // Partition column of plan source s (the copy it is read from when its
 // relation is partitioned): the probe column of the first join for source 0,
@@ -466,10 +475,12 @@ public:
                         hash_reserve(hr, *sink, t1 - t0);
                         spec.ht_slots = hr.keys.slots.get();
                         spec.ht_mask = hr.keys.mask;
+                        spec.ht_group_bits = hr.keys.group_bits;
                         spec.new_keys = sink->keys.get();
                         spec.new_count = sink->counter.get();
                         engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
                     }
+                    sink->candidates += T;
                     if (trace_) {
                         u64 probes = 0;
                         c_->read_scalars(spec.probe_count, &probes, 1);
@@ -749,6 +760,7 @@ public:
         ns.slots = DBuf<u64>(c_, cap);
         ns.mask = cap - 1;
         ns.count = r.keys.count;
+        ns.group_bits = r.keys.capacity() ? r.keys.group_bits : initial_group_bits();
         FV_CUDA(cudaMemsetAsync(ns.slots.get(), 0xff, 8 * cap, c_->stream));
         // The old table holds FULL's keys and the ones found new so far this
         // iteration (a relation's keys only ever enter through its table):
@@ -757,13 +769,39 @@ public:
         r.keys = std::move(ns);
     }
 
+    u32 initial_group_bits() const { return forced_group_ >= 0 ? static_cast<u32>(forced_group_) : 1u; }
+
+    // Re-lay the key set out with `bits` (same capacity): one pass over the
+    // old slots, keys re-scattered into the new layout.
+    void relayout_keys(RelState& r, u32 bits) {
+        KeySet ns;
+        ns.slots = DBuf<u64>(c_, r.keys.capacity());
+        ns.mask = r.keys.mask;
+        ns.count = r.keys.count;
+        ns.group_bits = bits;
+        FV_CUDA(cudaMemsetAsync(ns.slots.get(), 0xff, 8 * ns.capacity(), c_->stream));
+        engine_hash_rehash(c_, r.keys, ns);
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   %s key set -> group_bits %u (%llu slots)\n", r.name.c_str(), bits,
+                         static_cast<unsigned long long>(ns.capacity()));
+        r.keys = std::move(ns);
+    }
+
     // Sort the iteration's new keys into Δ and fold them into FULL.
     u64 hash_finalize(RelState& r, HeadSink& s, CandPool& pool) {
         if (pool.n) {
             hash_reserve(r, s, pool.n);
             engine_hash_insert(c_, pool.words[0].get(), pool.n, r.keys, s.keys.get(), s.counter.get());
+            s.candidates += pool.n;
         }
         const u64 nd = sink_count(s);
+        if (forced_group_ < 0 && r.keys.capacity() && s.candidates) {
+            const u32 want = double(s.candidates) <= group_ratio_ * double(std::max<u64>(nd, 1)) ? 1u : 0u;
+            if (trace_)
+                std::fprintf(stderr, "[fvlog]   %s candidates/new = %.3f\n", r.name.c_str(),
+                             double(s.candidates) / double(std::max<u64>(nd, 1)));
+            if (want != r.keys.group_bits) relayout_keys(r, want);
+        }
         r.indexes.clear();
         DevVersion Dv;
         Dv.n = nd;
@@ -825,6 +863,14 @@ private:
     EvalState& st_;
     std::map<InterKey, InterPolicy> inter_policy_;
     const bool trace_ = std::getenv("FVLOG_TRACE") != nullptr;
+    const double group_ratio_ = [] {
+        const char* e = std::getenv("FVLOG_GROUP_RATIO");
+        return e ? std::atof(e) : kGroupedRatio;
+    }();
+    const int forced_group_ = [] {
+        const char* e = std::getenv("FVLOG_KEYSET_GROUP");
+        return e ? std::atoi(e) : -1;
+    }();
     u32 world_ = 1, rank_ = 0;
 };
 

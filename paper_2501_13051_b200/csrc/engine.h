@@ -103,6 +103,7 @@ struct KeySet {
     DBuf<u64> slots;
     u64 mask = 0;
     u64 count = 0;
+    u32 group_bits = 0;  // home-slot layout (engine_kernels.cu keyset_home)
     u64 capacity() const { return slots.size(); }
 };
 
@@ -238,6 +239,7 @@ struct OutSpec {
     // keys that were not present to new_keys[*new_count ...].
     u64* ht_slots = nullptr;
     u64 ht_mask = 0;
+    u32 ht_group_bits = 0;
     u64* new_keys = nullptr;
     u64* new_count = nullptr;
     u64* probe_count = nullptr;  // optional (trace): key-set probes after the tile-local dedup
@@ -249,10 +251,11 @@ struct OutSpec {
 // Insert n keys; the ones not yet present are appended to
 // new_keys[*d_new ...] (device counter, not reset here).
 void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_keys, u64* d_new);
-// Move every key of `from` into the (larger, emptied) `to` by scanning
-// from's slots in order: with the same hash, a key's home in `to` is its old
-// slot plus a multiple of from's capacity, so the inserts stream through L2
-// instead of landing at random (to.count is not touched).
+// Move every key of `from` into the (emptied) `to` by scanning from's slots
+// in order: with the same layout a key's home in `to` is its old slot plus a
+// multiple of from's capacity, so the inserts stream through L2 instead of
+// landing at random; a layout change (group_bits) re-scatters them
+// (to.count is not touched).
 void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to);
 // Distinct rows of lexicographically sorted packed keys -> SoA columns
 // (arity <= FV_MAX_ARITY); returns the distinct count.

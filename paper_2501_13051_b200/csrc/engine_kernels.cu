@@ -82,24 +82,19 @@ __device__ __forceinline__ u64 row_key1(const OutSpec& spec, u64 i, u64 p) {
     return spec.n_out >= 2 ? (hi << spec.shift) | slot(spec.col[1], i, p) : hi;
 }
 
-// Key-set home slot: the low FV_KEYSET_GROUP_BITS bits of the key are kept
-// and the rest is scattered, so 2^bits keys that differ only there (same
-// first column, adjacent second-column ids) share a sector/line. A DRAM miss
-// costs a 128-byte line on this part (tools/membench.cu), so grouping cuts
-// DRAM bytes (C2: 215 -> 102 GB at 2 bits) — but repeated probes of a hub's
-// keys then concentrate on a few L2 lines and the fused join gets slower
-// (C2 141 -> 209 ms, C4 248 -> 333 ms); only SG, whose candidates are almost
-// all new, gains (76 -> 54 ms at 1 bit). Default: 0 (plain scattering).
-// Growth keeps the property the streaming rehash needs (new home = old home
-// + j * old capacity) for every setting.
-#ifndef FV_KEYSET_GROUP_BITS
-#define FV_KEYSET_GROUP_BITS 0
-#endif
-constexpr u32 kGroupBits = FV_KEYSET_GROUP_BITS;
-constexpr u64 kGroupMask = (u64(1) << kGroupBits) - 1;
-__device__ __forceinline__ u64 keyset_line_hash(u64 key) { return mix64(key >> kGroupBits); }
-__device__ __forceinline__ u64 keyset_home(u64 line_hash, u64 key, u64 mask) {
-    return ((line_hash << kGroupBits) | (key & kGroupMask)) & mask;
+// Key-set home slot (KeySet::group_bits = b): the low b bits of the key are
+// kept and the rest is scattered, so the 2^b keys that differ only there
+// (same first column, adjacent second-column ids) share a sector. A DRAM miss
+// costs a 128-byte line on this part (tools/membench.cu), so b = 1 halves the
+// misses of a relation whose candidates are mostly new (SG: 76 -> 54 ms);
+// when most candidates are repeats, grouped keys concentrate the probes of a
+// hub's outputs on a few L2 lines and b = 0 (plain scattering) is faster
+// (C2 141 vs 162 ms, C4 248 vs 271 ms). The engine picks b per relation from
+// the last iteration's candidates per new row. Growth keeps the property the
+// streaming rehash needs (new home = old home + j * old capacity).
+__device__ __forceinline__ u64 keyset_line_hash(u64 key, u32 bits) { return mix64(key >> bits); }
+__device__ __forceinline__ u64 keyset_home(u64 line_hash, u64 key, u32 bits, u64 mask) {
+    return ((line_hash << bits) | (key & ((u64(1) << bits) - 1))) & mask;
 }
 
 // Set-insert of one key: true when the key was absent (this thread inserted
@@ -308,13 +303,13 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) {
             key[k] = ((keep_mask >> k) & 1u) ? row_key1(spec, ii[k], pp[k]) : 0;
-            hs[k] = keyset_line_hash(key[k]);
+            hs[k] = keyset_line_hash(key[k], spec.ht_group_bits);
         }
         __syncthreads();  // s_set initialised (the sparse path has no barrier before this)
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) {
             if (!((keep_mask >> k) & 1u)) continue;
-            u32 h = static_cast<u32>((hs[k] >> 40) + (key[k] & kGroupMask)) & (kMatSetSlots - 1);
+            u32 h = static_cast<u32>(hs[k] >> 40) & (kMatSetSlots - 1);
             while (true) {
                 const unsigned long long prev = atomicCAS(s_set + h, ~0ull, static_cast<unsigned long long>(key[k]));
                 if (prev == ~0ull) break;                 // first in the tile
@@ -324,7 +319,7 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
                 }
                 h = (h + 1) & (kMatSetSlots - 1);
             }
-            hs[k] = keyset_home(hs[k], key[k], spec.ht_mask);
+            hs[k] = keyset_home(hs[k], key[k], spec.ht_group_bits, spec.ht_mask);
         }
         {
             const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
@@ -748,7 +743,7 @@ __global__ void fingerprint_kernel(Cols8 c, u32 arity, u64 n, unsigned long long
 namespace {
 
 __global__ void hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n, u64* __restrict__ slots, u64 mask,
-                                        u64* __restrict__ new_keys, u64* new_count) {
+                                        u32 bits, u64* __restrict__ new_keys, u64* new_count) {
     constexpr int ITEMS = 8;  // independent table loads in flight per thread
     const u64 base = u64(blockIdx.x) * blockDim.x * ITEMS + threadIdx.x;
     u64 key[ITEMS], hs[ITEMS], sv[ITEMS];
@@ -756,7 +751,7 @@ __global__ void hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n, u64
     for (int k = 0; k < ITEMS; ++k) {
         const u64 i = base + u64(k) * blockDim.x;
         key[k] = i < n ? keys[i] : 0;
-        hs[k] = keyset_home(keyset_line_hash(key[k]), key[k], mask);
+        hs[k] = keyset_home(keyset_line_hash(key[k], bits), key[k], bits, mask);
     }
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) sv[k] = (base + u64(k) * blockDim.x < n) ? __ldcg(slots + hs[k]) : 0;
@@ -772,7 +767,7 @@ __global__ void hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n, u64
 // roughly in index order, so the inserts of all resident blocks fall into a
 // few narrow windows of the new table that stay in L2.
 constexpr int kRehashItems = 8;
-__global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __restrict__ to, u64 mask) {
+__global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __restrict__ to, u64 mask, u32 bits) {
     const u64 base = u64(blockIdx.x) * blockDim.x * kRehashItems + threadIdx.x;
     u64 key[kRehashItems];
 #pragma unroll
@@ -783,7 +778,7 @@ __global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __r
 #pragma unroll
     for (int k = 0; k < kRehashItems; ++k)
         if (key[k] != kEmptySlot)
-            keyset_insert_probe_from(to, mask, key[k], keyset_home(keyset_line_hash(key[k]), key[k], mask));
+            keyset_insert_probe_from(to, mask, key[k], keyset_home(keyset_line_hash(key[k], bits), key[k], bits, mask));
 }
 
 __global__ void unpack_keys_kernel(const u64* __restrict__ keys, u64 n, u32 arity, u32 shift, u32* c0, u32* c1) {
@@ -891,7 +886,7 @@ void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_ke
     if (!n) return;
     ProfScope prof(c, "hash_insert", double(n) * (8.0 + 16.0));
     hash_insert_keys_kernel<<<static_cast<unsigned>(ceil_div(n, 256 * 8)), 256, 0, c->stream>>>(
-        keys, n, set.slots.get(), set.mask, new_keys, d_new);
+        keys, n, set.slots.get(), set.mask, set.group_bits, new_keys, d_new);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }
@@ -902,7 +897,7 @@ void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to) {
     // Algorithmic bytes: the old table read once, each key written once.
     ProfScope prof(c, "hash_rehash", double(n) * 8.0 + double(from.count) * 8.0);
     hash_rehash_kernel<<<static_cast<unsigned>(ceil_div(n, 256 * kRehashItems)), 256, 0, c->stream>>>(
-        from.slots.get(), n, to.slots.get(), to.mask);
+        from.slots.get(), n, to.slots.get(), to.mask, to.group_bits);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }
