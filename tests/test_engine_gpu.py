@@ -272,3 +272,20 @@ def test_join_orders_match_reference(ctx, order, monkeypatch):
         assert got == [tuple(s) for s in case["stats"]], (order, case["name"])
         for rel, exp in case["relations"].items():
             assert matches(st.dump(rel).reshape(-1), exp["dump"]), (order, case["name"], rel)
+
+
+@pytest.mark.parametrize("group", ["0", "1"])
+def test_keyset_layouts_match_reference(ctx, group, monkeypatch):
+    # FVLOG_KEYSET_GROUP forces the key-set home layout (0: every key
+    # scattered, 1: adjacent key pairs share a sector); the default picks one
+    # per relation from candidates per new row. Results must not depend on it.
+    monkeypatch.setenv("FVLOG_KEYSET_GROUP", group)
+    for case in load_golden("engine.json"):
+        if case["name"] == "TC uniform 2000/10000":
+            continue
+        text, facts = golden_cases.program_and_facts(case)
+        st = E.evaluate_program(text, facts, ctx=ctx)
+        got = [(s.index, s.relation, s.delta_rows, s.full_rows, s.merges) for s in st.stats()]
+        assert got == [tuple(s) for s in case["stats"]], (group, case["name"])
+        for rel, exp in case["relations"].items():
+            assert matches(st.dump(rel).reshape(-1), exp["dump"]), (group, case["name"], rel)
