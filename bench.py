@@ -181,6 +181,9 @@ def run_reference_impl(args):
 
 def run_fvlog(args):
     rank, world, local = rank_env()
+    # Keep stdout to the one JSON line (NCCL prints its version banner at
+    # INFO/VERSION levels).
+    os.environ["NCCL_DEBUG"] = "WARN"
     import torch
     dist = None
     if world > 1:
@@ -215,6 +218,11 @@ def run_fvlog(args):
         uid = [E.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         E.set_nccl(ctx, rank, world, uid[0])
+    elif args.partitioned:
+        # The multi-GPU code path on one GPU: a 1-rank NCCL communicator with
+        # the partitioned engine forced on (routing + NCCL exchange to self).
+        os.environ["FVLOG_FORCE_PARTITIONED"] = "1"
+        E.set_nccl(ctx, 0, 1, E.nccl_unique_id())
     edges = graph_for(world)
     # pinned host copy of the EDB for the e2e leg
     pinned = torch.empty(edges.shape, dtype=torch.int32, pin_memory=True)
@@ -352,7 +360,8 @@ def run_fvlog(args):
                    "derived_tuples_per_step": int(tuples // args.steps), "reach_rows": rows,
                    "iterations": iterations,
                    "parallelism": (f"hash-partitioned x{world}: reach by hash(col 0), edge replicated, "
-                                   f"one NCCL all-to-all + all-reduce per iteration") if world > 1 else "1 GPU",
+                                   f"one NCCL all-to-all + all-reduce per iteration")
+                                  if world > 1 or args.partitioned else "1 GPU",
                    "components": COMPONENTS * world,
                    "l2": "inputs larger than L2 (FULL grows to >5 GB per step, L2 126 MB)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms / max(1, args_steps_e2e),
@@ -387,6 +396,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
     ap.add_argument("--reserve-gb", type=float, default=96.0, help="fv_ctx_reserve before warm-up")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="N=1 only: run the hash-partitioned multi-GPU path over a 1-rank NCCL communicator")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_impl(args)

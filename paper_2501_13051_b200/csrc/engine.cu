@@ -216,10 +216,15 @@ public:
         if (c->tx) {
             world_ = static_cast<u32>(c->tx->world());
             rank_ = static_cast<u32>(c->tx->rank());
+            const char* e = std::getenv("FVLOG_FORCE_PARTITIONED");
+            force_partitioned_ = e && std::string(e) == "1";
         }
     }
 
-    bool dist() const { return world_ > 1; }
+    // FVLOG_FORCE_PARTITIONED=1 runs the partitioned path even with one
+    // rank (a context with a transport), so the NCCL code path — routing,
+    // grouped send/recv, all-reduce — is exercised on a single GPU.
+    bool dist() const { return world_ > 1 || force_partitioned_; }
     bool partitioned(const RelState& r) const { return dist() && r.idb; }
     RelState& rel(const std::string& name) { return *st_.relations.at(name); }
 
@@ -861,6 +866,7 @@ public:
 private:
     Ctx* c_;
     EvalState& st_;
+    bool force_partitioned_ = false;
     std::map<InterKey, InterPolicy> inter_policy_;
     const bool trace_ = std::getenv("FVLOG_TRACE") != nullptr;
     const double group_ratio_ = [] {

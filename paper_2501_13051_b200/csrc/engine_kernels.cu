@@ -163,8 +163,15 @@ __device__ __forceinline__ void write_row(const OutSpec& spec, u64 pos, u64 i, u
     }
 }
 
-constexpr int kMatBlock = 256;
-constexpr int kMatItems = 8;
+// 512 threads x 4 outputs per 2048-output tile: the fused key-set probes are
+// latency-bound random loads, and more warps with fewer items each keep more
+// of them in flight (C2 141.7 -> 123.7 ms, C3 55.3 -> 46.2, C4 250 -> 223
+// against 256 x 8; 1024 x 2 is equal on C2/C3 and slower on C4).
+#ifndef FV_MAT_BLOCK
+#define FV_MAT_BLOCK 512
+#endif
+constexpr int kMatBlock = FV_MAT_BLOCK;
+constexpr int kMatItems = 2048 / kMatBlock;  // one 2048-output tile per CTA
 constexpr int kMatTile = kMatBlock * kMatItems;
 constexpr int kMatSparseSpan = 8 * kMatTile;
 constexpr int kMatSetSlots = 2 * kMatTile;  // load <= 1/2
@@ -742,9 +749,22 @@ __global__ void fingerprint_kernel(Cols8 c, u32 arity, u64 n, unsigned long long
 
 namespace {
 
-__global__ void hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n, u64* __restrict__ slots, u64 mask,
-                                        u32 bits, u64* __restrict__ new_keys, u64* new_count) {
-    constexpr int ITEMS = 8;  // independent table loads in flight per thread
+#ifndef FV_INSERT_ITEMS
+#define FV_INSERT_ITEMS 1
+#endif
+#ifdef FV_INSERT_MINB
+#define FV_INSERT_BOUNDS __launch_bounds__(256, FV_INSERT_MINB)
+#else
+#define FV_INSERT_BOUNDS
+#endif
+// One key per thread: the probe is a latency-bound random load, and 20
+// registers give full occupancy (the partitioned C2 insert: 167.6 ms at 8
+// keys/thread and 64 registers, 119 ms at 2, 97 ms at 1).
+constexpr int kInsertItems = FV_INSERT_ITEMS;
+__global__ void FV_INSERT_BOUNDS hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n,
+                                                         u64* __restrict__ slots, u64 mask, u32 bits,
+                                                         u64* __restrict__ new_keys, u64* new_count) {
+    constexpr int ITEMS = kInsertItems;
     const u64 base = u64(blockIdx.x) * blockDim.x * ITEMS + threadIdx.x;
     u64 key[ITEMS], hs[ITEMS], sv[ITEMS];
 #pragma unroll
@@ -885,7 +905,7 @@ struct SelectRowsOp {
 void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_keys, u64* d_new) {
     if (!n) return;
     ProfScope prof(c, "hash_insert", double(n) * (8.0 + 16.0));
-    hash_insert_keys_kernel<<<static_cast<unsigned>(ceil_div(n, 256 * 8)), 256, 0, c->stream>>>(
+    hash_insert_keys_kernel<<<static_cast<unsigned>(ceil_div(n, 256 * kInsertItems)), 256, 0, c->stream>>>(
         keys, n, set.slots.get(), set.mask, set.group_bits, new_keys, d_new);
     FV_CUDA(cudaGetLastError());
     c->count_launch();

@@ -92,3 +92,19 @@ def test_sharded_c1_size(ctx):
     assert shards[0].delta_counts() == single.delta_counts()
     fp = sum(s.fingerprint("reach") for s in shards) & 0xFFFFFFFFFFFFFFFF
     assert fp == single.fingerprint("reach")
+
+
+def test_nccl_transport_single_rank(monkeypatch):
+    """The NCCL transport itself (dlopen'ed libnccl, ncclCommInitRank, grouped
+    ncclSend/ncclRecv, ncclAllReduce) on one GPU: a 1-rank communicator with
+    the partitioned path forced on, so every routing/exchange step goes
+    through NCCL (to self). Results must equal the single-GPU evaluation."""
+    from paper_2501_13051_b200 import colog
+    monkeypatch.setenv("FVLOG_FORCE_PARTITIONED", "1")
+    ctx = colog.Context(0)
+    E.set_nccl(ctx, 0, 1, E.nccl_unique_id())
+    plain = colog.Context(0)
+    for name, text, facts in CASES:
+        single = E.evaluate_program(text, facts, ctx=plain)
+        part = E.evaluate_program(text, facts, ctx=ctx)
+        _check(single, [part], name)
