@@ -759,10 +759,19 @@ public:
         // Grow to a worst-case load of 1/4: most probes of a fused join are
         // repeats of present keys, and short linear-probe runs keep them to
         // one DRAM access; 4x growth also keeps the number of rehashes low.
+        const u64 need = r.keys.count + pending + extra;
         u64 cap = 1u << 16;
-        while (cap < 4 * (r.keys.count + pending + extra)) cap <<= 1;
+        while (cap < 4 * need) cap <<= 1;
         KeySet ns;
-        ns.slots = DBuf<u64>(c_, cap);
+        try {
+            ns.slots = DBuf<u64>(c_, cap);
+        } catch (const Error& e) {
+            // Memory-tight: settle for the 1/2 worst-case load the check above
+            // guarantees (fails loudly if even that does not fit).
+            if (e.status != FV_ERR_OOM || cap / 2 < 2 * need) throw;
+            cap /= 2;
+            ns.slots = DBuf<u64>(c_, cap);
+        }
         ns.mask = cap - 1;
         ns.count = r.keys.count;
         ns.group_bits = r.keys.capacity() ? r.keys.group_bits : initial_group_bits();
