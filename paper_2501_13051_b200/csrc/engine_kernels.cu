@@ -174,7 +174,11 @@ constexpr int kMatBlock = FV_MAT_BLOCK;
 constexpr int kMatItems = 2048 / kMatBlock;  // one 2048-output tile per CTA
 constexpr int kMatTile = kMatBlock * kMatItems;
 constexpr int kMatSparseSpan = 8 * kMatTile;
-constexpr int kMatSetSlots = 2 * kMatTile;  // load <= 1/2
+#ifndef FV_MAT_SET_SLOTS
+#define FV_MAT_SET_SLOTS (2 * kMatTile)
+#endif
+constexpr int kMatSetSlots = FV_MAT_SET_SLOTS;  // tile-local set; load <= 1/2 at the default size
+constexpr int kMatSetProbes = 16;               // bounded: an unplaced key is simply probed globally
 
 __device__ __forceinline__ u64 upper_bound_u64(const u64* __restrict__ a, u64 len, u64 x) {
     u64 lo = 0, hi = len;
@@ -317,7 +321,7 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
         for (int k = 0; k < kMatItems; ++k) {
             if (!((keep_mask >> k) & 1u)) continue;
             u32 h = static_cast<u32>(hs[k] >> 40) & (kMatSetSlots - 1);
-            while (true) {
+            for (int probe = 0; probe < kMatSetProbes; ++probe) {
                 const unsigned long long prev = atomicCAS(s_set + h, ~0ull, static_cast<unsigned long long>(key[k]));
                 if (prev == ~0ull) break;                 // first in the tile
                 if (prev == key[k]) {                     // repeat: drop
