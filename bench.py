@@ -62,10 +62,20 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def graph_for(world: int = 1):
-    """N x C2: components 0..999 are the N=1 graph; more are appended."""
+def graph_for(world: int = 1, dist=None):
+    """N x C2: components 0..999 are the N=1 graph; more are appended. Under
+    torchrun every rank generates its own 1000 components and the slices are
+    all-gathered (the EDB is replicated)."""
     from paper_2501_13051_b200 import workloads as W
-    return W.tc_powerlaw(COMPONENTS * world, NODES, EDGES, seed=1)
+    if dist is None or world == 1:
+        return W.tc_powerlaw(COMPONENTS * world, NODES, EDGES, seed=1)
+    import torch
+    rank = dist.get_rank()
+    mine = W.tc_powerlaw(COMPONENTS, NODES, EDGES, seed=1, first=rank * COMPONENTS)
+    t = torch.from_numpy(mine.view(np.int32)).cuda()
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    return torch.cat(parts).cpu().numpy().view(np.uint32)
 
 
 # ---- clocks ---------------------------------------------------------------------------
@@ -223,7 +233,7 @@ def run_fvlog(args):
         # the partitioned engine forced on (routing + NCCL exchange to self).
         os.environ["FVLOG_FORCE_PARTITIONED"] = "1"
         E.set_nccl(ctx, 0, 1, E.nccl_unique_id())
-    edges = graph_for(world)
+    edges = graph_for(world, dist)
     # pinned host copy of the EDB for the e2e leg
     pinned = torch.empty(edges.shape, dtype=torch.int32, pin_memory=True)
     pinned.numpy()[:] = edges.view(np.int32)

@@ -102,15 +102,17 @@ def tc_uniform(nodes: int, edges: int, seed: int = 1) -> np.ndarray:
 
 
 def tc_powerlaw(components: int = 1000, nodes: int = 1000, edges: int = 5000, seed: int = 1,
-                alpha: float = 1.0) -> np.ndarray:
+                alpha: float = 1.0, first: int = 0) -> np.ndarray:
     """C2: `components` disjoint blocks of `nodes` nodes with `edges` distinct
     edges each; sources Zipf(alpha) over a per-block node permutation,
-    targets uniform (no giant SCC, |TC| ~ components * 0.65 C^2)."""
+    targets uniform (no giant SCC, |TC| ~ components * 0.65 C^2).
+    `first` generates blocks first .. first + components - 1 of the same
+    sequence (a slice of a larger graph)."""
     w = 1.0 / np.arange(1, nodes + 1, dtype=np.float64) ** alpha
     cdf = np.cumsum(w)
     cdf /= cdf[-1]
     out = []
-    for c in range(components):
+    for c in range(first, first + components):
         s = seed * 1_000_003 + c
         perm = np.argsort(splitmix64(s ^ 0x7777, nodes), kind="stable").astype(np.uint32)
         draw = edges * 3
