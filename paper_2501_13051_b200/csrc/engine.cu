@@ -749,28 +749,33 @@ public:
         }
         s.bound += extra;
         // bound counts every candidate as new, so the real load stays below
-        // the 1/2 worst case the table is checked against.
-        if (2 * (r.keys.count + s.bound) <= r.keys.capacity()) return;
+        // the worst case the table accepts (KeySet::limit: half its slots,
+        // three quarters when memory forced a smaller table).
+        if (r.keys.count + s.bound <= r.keys.limit) return;
         // Re-read the real count before growing: a stale bound (earlier
         // chunks counted as all-new) must not trigger a rehash.
         const u64 pending = sink_count(s);
         s.bound = pending + extra;
-        if (2 * (r.keys.count + s.bound) <= r.keys.capacity()) return;
+        if (r.keys.count + s.bound <= r.keys.limit) return;
         // Grow to a worst-case load of 1/4: most probes of a fused join are
         // repeats of present keys, and short linear-probe runs keep them to
         // one DRAM access; 4x growth also keeps the number of rehashes low.
+        // Memory-tight: settle for 1/2, then 3/4 (fails loudly beyond).
         const u64 need = r.keys.count + pending + extra;
         u64 cap = 1u << 16;
         while (cap < 4 * need) cap <<= 1;
         KeySet ns;
-        try {
-            ns.slots = DBuf<u64>(c_, cap);
-        } catch (const Error& e) {
-            // Memory-tight: settle for the 1/2 worst-case load the check above
-            // guarantees (fails loudly if even that does not fit).
-            if (e.status != FV_ERR_OOM || cap / 2 < 2 * need) throw;
-            cap /= 2;
-            ns.slots = DBuf<u64>(c_, cap);
+        for (int attempt = 0;; ++attempt) {
+            try {
+                ns.slots = DBuf<u64>(c_, cap);
+                ns.limit = attempt < 2 ? cap / 2 : cap / 4 * 3;
+                break;
+            } catch (const Error& e) {
+                const u64 next = cap / 2;
+                const bool fits_next = attempt == 0 ? next >= 2 * need : 3 * (next / 4) >= need;
+                if (e.status != FV_ERR_OOM || attempt >= 2 || !fits_next) throw;
+                cap = next;
+            }
         }
         ns.mask = cap - 1;
         ns.count = r.keys.count;
@@ -791,6 +796,7 @@ public:
         KeySet ns;
         ns.slots = DBuf<u64>(c_, r.keys.capacity());
         ns.mask = r.keys.mask;
+        ns.limit = r.keys.limit;
         ns.count = r.keys.count;
         ns.group_bits = bits;
         FV_CUDA(cudaMemsetAsync(ns.slots.get(), 0xff, 8 * ns.capacity(), c_->stream));

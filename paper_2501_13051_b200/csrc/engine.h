@@ -98,12 +98,14 @@ struct JoinIndex {
 using IndexMap = std::map<std::pair<int, u32>, std::unique_ptr<JoinIndex>>;
 
 // Open-addressing set of packed row keys (empty slot = all ones, which no
-// key can equal when 2 * shift < 64), load factor <= 1/2.
+// key can equal when 2 * shift < 64), load factor <= 1/2 (3/4 when memory
+// forced a smaller table).
 struct KeySet {
     DBuf<u64> slots;
     u64 mask = 0;
     u64 count = 0;
     u32 group_bits = 0;  // home-slot layout (engine_kernels.cu keyset_home)
+    u64 limit = 0;       // most keys (worst case) the table accepts before growing
     u64 capacity() const { return slots.size(); }
 };
 

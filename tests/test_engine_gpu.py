@@ -195,6 +195,15 @@ def test_sg_c3_full_size_closed_form(ctx):
     assert sum(st.delta_counts()["sg"]) == 340_637_176
 
 
+def test_sg_beyond_c3_1e9_tuples(ctx):
+    # Maximum-size case: 61 depth-12 trees (499,590 edges) derive 1.36e9 SG
+    # tuples (~4x C3): key set, levels and sort scratch must fit one B200.
+    st = E.evaluate_program(W.SG_PROGRAM, {"edge": W.sg_forest(61, 12)}, ctx=ctx)
+    assert st.rows("sg") == W.sg_count(61, 12) == 1_364_047_230
+    assert st.iterations == 13
+    assert sum(st.delta_counts()["sg"]) == 1_364_047_230
+
+
 @pytest.mark.parametrize("cfg", ["C1", "C2"])
 def test_tc_full_size_against_large_goldens(ctx, cfg):
     g = _large().get(cfg)
