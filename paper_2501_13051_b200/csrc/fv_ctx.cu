@@ -150,16 +150,6 @@ Ctx* ctx_new(int device) {
         if (prop.major < 10)
             fail(FV_ERR_CUDA, std::string("fvlog is built for sm_100a (Blackwell); device is ") +
                                   prop.name);
-        // The fused join+dedup kernel and the key-set inserts are random 8-byte
-        // accesses into tables far larger than L2; a 32-byte L2 fetch
-        // granularity keeps each miss to one DRAM sector instead of a
-        // promoted 64/128-byte fetch (streaming kernels read whole lines
-        // anyway). FVLOG_L2_FETCH overrides (0 = leave the driver default).
-        {
-            size_t gran = 32;
-            if (const char* e = std::getenv("FVLOG_L2_FETCH")) gran = static_cast<size_t>(std::atoi(e));
-            if (gran) FV_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran));
-        }
         FV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         FV_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, device));
         // Keep freed blocks cached in the pool: relations are rebuilt every
