@@ -46,6 +46,7 @@
 #include "prim.cuh"
 #include "radix_sort.h"
 #include "transport.h"
+#include "tsv.h"
 
 namespace fv {
 
@@ -1252,47 +1253,68 @@ std::vector<std::unique_ptr<EvalState>> evaluate_sharded(Ctx* base, u32 world, c
     return out;
 }
 
-std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel) {
-    auto it = s.relations.find(rel);
-    if (it == s.relations.end()) fail(FV_ERR_RANGE, "unknown relation '" + rel + "'");
-    const RelState& r = *it->second;
+namespace {
+
+// The relation's rows as lexicographically sorted device columns: FULL
+// itself, or (levels mode) one sort of the concatenated levels into `tmp`.
+const DevVersion& sorted_rows(const EvalState& s, const RelState& r, DevVersion& tmp) {
+    if (!r.levels_mode) return r.full;
     Ctx* c = s.ctx;
     const u64 n = r.rows();
-    DevVersion merged;
-    const DevVersion* src = &r.full;
-    if (r.levels_mode) {
-        // Levels are grouped by column 0 per iteration; one sort of their concatenation
-        // gives the lexicographic dump (like dump_relation's std::sort).
-        merged.n = n;
-        for (u32 j = 0; j < r.arity; ++j) {
-            DBuf<u32> col(c, n);
-            u64 off = 0;
-            for (auto& lv : r.levels) {
-                if (lv.n)
-                    FV_CUDA(cudaMemcpyAsync(col.get() + off, lv.cols[j].get(), 4 * lv.n, cudaMemcpyDeviceToDevice,
-                                            c->stream));
-                off += lv.n;
-            }
-            merged.cols.push_back(std::move(col));
+    // Levels are grouped by column 0 per iteration; one sort of their
+    // concatenation gives the lexicographic dump (like dump_relation's std::sort).
+    tmp.n = n;
+    tmp.cols.clear();
+    for (u32 j = 0; j < r.arity; ++j) {
+        DBuf<u32> col(c, n);
+        u64 off = 0;
+        for (auto& lv : r.levels) {
+            if (lv.n)
+                FV_CUDA(cudaMemcpyAsync(col.get() + off, lv.cols[j].get(), 4 * lv.n, cudaMemcpyDeviceToDevice,
+                                        c->stream));
+            off += lv.n;
         }
-        if (n) {
-            std::vector<DBuf<u64>> words;
-            words.emplace_back(c, n);
-            u64* wp = words[0].get();
-            engine_pack_keys(c, merged.ptrs(), n, s.key_shift, &wp);
-            engine_sort_keys(c, words, n, r.arity, s.key_shift);
-            std::vector<u32*> cols;
-            for (auto& col : merged.cols) cols.push_back(col.get());
-            engine_unpack_keys(c, words[0].get(), n, r.arity, s.key_shift, cols);
-        }
-        src = &merged;
+        tmp.cols.push_back(std::move(col));
     }
+    if (n) {
+        std::vector<DBuf<u64>> words;
+        words.emplace_back(c, n);
+        u64* wp = words[0].get();
+        engine_pack_keys(c, tmp.ptrs(), n, s.key_shift, &wp);
+        engine_sort_keys(c, words, n, r.arity, s.key_shift);
+        std::vector<u32*> cols;
+        for (auto& col : tmp.cols) cols.push_back(col.get());
+        engine_unpack_keys(c, words[0].get(), n, r.arity, s.key_shift, cols);
+    }
+    return tmp;
+}
+
+const RelState& find_rel(const EvalState& s, const std::string& rel) {
+    auto it = s.relations.find(rel);
+    if (it == s.relations.end()) fail(FV_ERR_RANGE, "unknown relation '" + rel + "'");
+    return *it->second;
+}
+
+}  // namespace
+
+std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel) {
+    const RelState& r = find_rel(s, rel);
+    DevVersion tmp;
+    const DevVersion& src = sorted_rows(s, r, tmp);
+    const u64 n = r.rows();
     std::vector<u32> rows(n * r.arity), col(n);
     for (u32 j = 0; j < r.arity; ++j) {
-        src->cols[j].download(col.data(), n);
+        src.cols[j].download(col.data(), n);
         for (u64 i = 0; i < n; ++i) rows[i * r.arity + j] = col[i];
     }
     return rows;
+}
+
+std::string dump_sorted_text(const EvalState& s, const std::string& rel) {
+    const RelState& r = find_rel(s, rel);
+    DevVersion tmp;
+    const DevVersion& src = sorted_rows(s, r, tmp);
+    return tsv_format_u32(s.ctx, src.ptrs(), r.rows(), r.arity);
 }
 
 u64 fingerprint(const EvalState& s, const std::string& rel) {

@@ -203,6 +203,8 @@ void check_plans(const std::vector<RelationDecl>& decls, const std::vector<Plan>
 
 // Lexicographically sorted row-major dump of FULL (host).
 std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel);
+// dump_relation text (integer mode) of the sorted rows, formatted on the device.
+std::string dump_sorted_text(const EvalState& s, const std::string& rel);
 u64 fingerprint(const EvalState& s, const std::string& rel);
 
 // ---- kernels (engine_kernels.cu) ---------------------------------------------

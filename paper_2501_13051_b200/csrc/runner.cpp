@@ -3,7 +3,12 @@
 // line formats), driving the device engine.
 #include "runner.h"
 
+#include "tsv.h"
+
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <charconv>
 #include <filesystem>
 #include <fstream>
@@ -104,6 +109,17 @@ std::string dump_text(const std::vector<u32>& rows, u32 arity, const fe::Diction
 }
 
 int run(Ctx* c, const RunConfig& cfg, std::ostream& out, std::ostream& err) {
+    // FVLOG_TRACE=1: host phase times on stderr (stdout keeps the reference's lines).
+    const bool trace = std::getenv("FVLOG_TRACE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+        if (!trace) return;
+        c->sync();
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[fvlog] run %-12s %.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     try {
         std::ifstream pin(cfg.program_path, std::ios::binary);
         if (!pin) fail(FV_ERR_IO, "cannot open program file: " + cfg.program_path);
@@ -124,6 +140,7 @@ int run(Ctx* c, const RunConfig& cfg, std::ostream& out, std::ostream& err) {
         }
         fe::Dictionary dict;
         fe::resolve_strings(prog, dict);
+        phase("parse");
         auto pfacts = fe::program_facts(prog);
 
         // Host-side staging of the EDB (excluded from the timed span, like
@@ -142,11 +159,27 @@ int run(Ctx* c, const RunConfig& cfg, std::ostream& out, std::ostream& err) {
             }
             blocks.push_back(std::move(b));
         }
+        // Facts files: integer-mode files are parsed on the device straight
+        // into EDB columns (tsv.cu); dictionary-mode files (first non-empty
+        // line not all integers) go through the host dictionary as before.
         std::vector<LoadedFacts> loaded;
         std::vector<std::string> loaded_rel;
+        DeviceEdb file_edb;
         for (auto& d : prog.relations) {
             const fs::path path = fs::path(cfg.facts_dir) / (d.name + ".tsv");
             if (!fs::exists(path)) continue;
+            std::ifstream fin(path, std::ios::binary | std::ios::ate);
+            if (!fin) fail(FV_ERR_IO, "cannot open facts file: " + path.string());
+            std::string bytes(static_cast<size_t>(fin.tellg()), '\0');
+            fin.seekg(0);
+            if (!bytes.empty() && !fin.read(bytes.data(), static_cast<std::streamsize>(bytes.size())))
+                fail(FV_ERR_IO, "cannot read facts file: " + path.string());
+            if (tsv_first_line_is_integer(bytes.data(), bytes.size(), d.arity)) {
+                DevVersion v;
+                v.n = tsv_parse_u32(c, bytes.data(), bytes.size(), d.arity, path.string(), v.cols);
+                if (v.n) file_edb.rels.emplace(d.name, std::move(v));
+                continue;
+            }
             loaded.push_back(load_facts(path.string(), d.arity, dict));
             loaded_rel.push_back(d.name);
         }
@@ -160,8 +193,13 @@ int run(Ctx* c, const RunConfig& cfg, std::ostream& out, std::ostream& err) {
             blocks.push_back(std::move(b));
         }
 
+        phase("load facts");
         auto plans = fe::compile(prog);
-        auto st = evaluate(c, fe::declarations(prog), plans, blocks);
+        const auto decls = fe::declarations(prog);
+        check_plans(decls, plans);
+        DeviceEdb host_edb = upload_facts(c, decls, blocks);
+        auto st = evaluate_device(c, decls, plans, {&host_edb, &file_edb});
+        phase("evaluate");
 
         if (cfg.print_stats)
             for (auto& s : st->stats)
@@ -180,7 +218,14 @@ int run(Ctx* c, const RunConfig& cfg, std::ostream& out, std::ostream& err) {
                 }
                 std::ofstream o(fs::path(cfg.out_dir) / (name + ".tsv"), std::ios::binary);
                 if (!o) fail(FV_ERR_IO, "cannot open output file: " + (fs::path(cfg.out_dir) / (name + ".tsv")).string());
-                o << dump_text(dump_sorted(*st, name), it->second->arity, dict.empty() ? nullptr : &dict);
+                // Quirk kept (P/src/runner.cpp:83): a non-empty dictionary
+                // decodes every dumped relation (host path); otherwise the
+                // sorted rows are formatted on the device.
+                if (dict.empty())
+                    o << dump_sorted_text(*st, name);
+                else
+                    o << dump_text(dump_sorted(*st, name), it->second->arity, &dict);
+                phase("dump");
             }
         }
         return 0;
