@@ -127,7 +127,7 @@ u32 copy_for_source(const Plan& p, u32 s) {
 // every equality of the rule (join keys, residuals, self-equalities) is
 // re-derived from the variable classes. Returns false (p unchanged) when no
 // such connected order exists.
-bool delta_first_plan(const Plan& p, u32 d, Plan& out) {
+bool delta_first_plan(const Plan& p, u32 d, Plan& out, std::vector<u32>* order_out) {
     const u32 ns = static_cast<u32>(p.sources.size());
     if (d == 0 || d >= ns) return false;
     std::vector<u32> base(ns + 1, 0);
@@ -184,6 +184,7 @@ bool delta_first_plan(const Plan& p, u32 d, Plan& out) {
     }
     std::vector<u32> new_of(ns);
     for (u32 i = 0; i < ns; ++i) new_of[order[i]] = i;
+    if (order_out) *order_out = order;
     for (const ColRef& r : p.output_cols) out.output_cols.push_back(ColRef{new_of[r.source], r.col});
     out.guard_neq = p.guard_neq;
     return true;
@@ -233,13 +234,21 @@ public:
     DevVersion& vdelta(RelState& r, u32 kc) { return kc ? r.copies.at(kc)->delta : r.delta; }
     IndexMap& vindexes(RelState& r, u32 kc) { return kc ? r.copies.at(kc)->indexes : r.indexes; }
 
-    JoinIndex& index(RelState& r, u32 kc, bool delta, u32 col) {
+    // FULL - DELTA of the home copy (see RelState::full_old).
+    DevVersion& vold(RelState& r) { return r.old_is_full ? r.full : r.full_old; }
+    enum Which { kFull = 0, kDelta = 1, kOld = 2 };
+    DevVersion& version(RelState& r, u32 kc, Which w) {
+        return w == kDelta ? vdelta(r, kc) : (w == kOld ? vold(r) : vfull(r, kc));
+    }
+
+    JoinIndex& index(RelState& r, u32 kc, Which which, u32 col) {
+        if (which == kOld && r.old_is_full) which = kFull;
         IndexMap& m = vindexes(r, kc);
-        auto key = std::make_pair(delta ? 1 : 0, col);
+        auto key = std::make_pair(static_cast<int>(which), col);
         auto it = m.find(key);
         if (it != m.end()) return *it->second;
         auto idx = std::make_unique<JoinIndex>();
-        build_index_on(delta ? vdelta(r, kc) : vfull(r, kc), col, *idx, nullptr);
+        build_index_on(version(r, kc, which), col, *idx, nullptr);
         JoinIndex& ref = *idx;
         m.emplace(key, std::move(idx));
         return ref;
@@ -386,14 +395,20 @@ public:
 
     // ---- execute_plan (P/src/engine.cpp:72-146) for one variant ------------------
 
-    void exec_variant(const Plan& plan, const DistPlan& dp, long delta_source, CandPool& out, HeadSink* sink) {
+    // `old_src[s]`: source s reads FULL - DELTA instead of FULL (exactly-once
+    // variants; empty = every non-DELTA source reads FULL, the reference).
+    void exec_variant(const Plan& plan, const DistPlan& dp, long delta_source, const std::vector<u8>& old_src,
+                      CandPool& out, HeadSink* sink) {
         const u32 ns = static_cast<u32>(plan.sources.size());
         const bool D = dist();
         std::vector<const DevVersion*> ver(ns);
+        std::vector<Which> which(ns, kFull);
         for (u32 s = 0; s < ns; ++s) {
             RelState& r = rel(plan.sources[s].relation);
             const u32 kc = partitioned(r) ? dp.src_copy[s] : 0;
-            ver[s] = (static_cast<long>(s) == delta_source) ? &vdelta(r, kc) : &vfull(r, kc);
+            if (static_cast<long>(s) == delta_source) which[s] = kDelta;
+            else if (!old_src.empty() && old_src[s]) which[s] = kOld;
+            ver[s] = &version(r, kc, which[s]);
             if (!D && ver[s]->n == 0) return;  // engine.cpp:76-78
         }
         Inter cur;
@@ -427,7 +442,7 @@ public:
                 build_index_on(*ver[R], jn.right_col, *tmp, &plan.sources[R]);
                 idx = tmp.get();
             } else {
-                idx = &index(rr, rpart ? jn.right_col : 0, static_cast<long>(R) == delta_source, jn.right_col);
+                idx = &index(rr, rpart ? jn.right_col : 0, which[R], jn.right_col);
             }
             if (!D && idx->rows->n == 0) return;
             const u64 n = cur.n;
@@ -617,12 +632,14 @@ public:
     }
 
     // Sort candidates and fold them into (full, delta); returns |DELTA|.
-    u64 dedup_merge(DevVersion& full, DevVersion& delta, IndexMap& indexes, u32 arity, CandPool& cand) {
+    u64 dedup_merge(DevVersion& full, DevVersion& delta, IndexMap& indexes, u32 arity, CandPool& cand,
+                    RelState* home = nullptr) {
         if (cand.n == 0) {
             delta = DevVersion();
             delta.n = 0;
             delta.cols.resize(arity);
             indexes.clear();
+            if (home) set_old(*home, nullptr);
             return 0;
         }
         engine_sort_keys(c_, cand.words, cand.n, arity, st_.key_shift);
@@ -645,13 +662,31 @@ public:
         c_->prof_add_bytes("merge_dedup", 8.0 * double(nd) * arity);
         C.n = full.n + nd;
         Dv.n = nd;
+        if (home && nd) {
+            set_old(*home, &full);
+        } else if (home) {
+            set_old(*home, nullptr);
+        }
         full = std::move(C);
         delta = std::move(Dv);
         indexes.clear();
         return nd;
     }
 
-    u64 dedup_merge_home(RelState& r, CandPool& cand) { return dedup_merge(r.full, r.delta, r.indexes, r.arity, cand); }
+    // The FULL a merge is about to replace becomes FULL - DELTA (moved, no
+    // copy); null: nothing new, FULL - DELTA = FULL.
+    void set_old(RelState& r, DevVersion* replaced) {
+        r.full_old = DevVersion();
+        r.old_is_full = true;
+        if (replaced && r.keep_old) {
+            r.full_old = std::move(*replaced);
+            r.old_is_full = false;
+        }
+    }
+
+    u64 dedup_merge_home(RelState& r, CandPool& cand) {
+        return dedup_merge(r.full, r.delta, r.indexes, r.arity, cand, &r);
+    }
 
     // Seed one copy of a relation from raw EDB rows (owner-filtered on kc
     // when partitioned).
@@ -662,7 +697,7 @@ public:
             hash_finalize(r, sink, pool);
             return;
         }
-        dedup_merge(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool);
+        dedup_merge(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool, kc == 0 ? &r : nullptr);
     }
 
     CandPool seed_pool(RelState& r, const DevVersion& v, u32 kc) {
@@ -829,6 +864,7 @@ public:
         for (u32 j = 0; j < r.arity; ++j) Dv.cols.emplace_back(c_, nd);
         if (nd == 0) {
             r.delta = std::move(Dv);
+            set_old(r, nullptr);
             return 0;
         }
         r.keys.count += nd;
@@ -867,6 +903,7 @@ public:
             u64* d_new = c_->d_scalars + 23;
             engine_merge(c_, r.full.ptrs(), r.full.n, bw.data(), nd, r.arity, st_.key_shift, cc, uc, d_new);
             C.n = r.full.n + nd;
+            set_old(r, &r.full);
             r.full = std::move(C);
         }
         r.delta = std::move(Dv);
@@ -1058,7 +1095,8 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     struct Variant {
         const Plan* plan;
         long delta_source;
-        size_t plan_index;  // index into dplans
+        size_t plan_index;     // index into dplans
+        std::vector<u8> old_src;  // per executed source: read FULL - DELTA
     };
     std::vector<DistPlan> dplans;
     std::deque<Plan> reordered;  // delta-first plans (stable addresses)
@@ -1067,6 +1105,14 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     // FVLOG_JOIN_ORDER=rule keeps every variant in the rule's atom order.
     const char* order_env = std::getenv("FVLOG_JOIN_ORDER");
     const bool delta_first = !(order_env && std::string(order_env) == "rule");
+    // Exactly-once variants (single GPU): the variant with DELTA at IDB
+    // occurrence i reads FULL - DELTA at the IDB occurrences before i and FULL
+    // after it, so a derivation using several DELTA rows is produced by one
+    // variant instead of each (the reference reads FULL everywhere,
+    // P/src/engine.cpp:180-183). The union over variants is the same set.
+    // FVLOG_SEMINAIVE=reference restores the reference's variants.
+    const char* sn_env = std::getenv("FVLOG_SEMINAIVE");
+    const bool exactly_once = !eng.dist() && !(sn_env && std::string(sn_env) == "reference");
     for (size_t i = 0; i < plans.size(); ++i) {
         const Plan& p = plans[i];
         bool any = false;
@@ -1080,25 +1126,35 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
                 // FULL on another column, and an EDB prefix is fixed-size.
                 bool idb_before = false;
                 for (size_t q = 0; q < s; ++q) idb_before = idb_before || idb.count(p.sources[q].relation) > 0;
+                // old_by_rule[q]: rule atom q reads FULL - DELTA in this variant.
+                std::vector<u8> old_by_rule(p.sources.size(), 0);
+                if (exactly_once)
+                    for (size_t q = 0; q < s; ++q) old_by_rule[q] = idb.count(p.sources[q].relation) ? 1 : 0;
+                std::vector<u32> order;
                 if (delta_first && idb_before && p.sources.size() >= 3 &&
-                    delta_first_plan(p, static_cast<u32>(s), rp)) {
+                    delta_first_plan(p, static_cast<u32>(s), rp, &order)) {
+                    std::vector<u8> old_src(order.size());
+                    for (size_t i = 0; i < order.size(); ++i) old_src[i] = old_by_rule[order[i]];
                     reordered.push_back(std::move(rp));
                     dplans.push_back(dist_plan(reordered.back(), idb));
-                    variants.push_back({&reordered.back(), 0, dplans.size() - 1});
+                    variants.push_back({&reordered.back(), 0, dplans.size() - 1, std::move(old_src)});
                 } else {
                     dplans.push_back(dist_plan(p, idb));
-                    variants.push_back({&p, static_cast<long>(s), dplans.size() - 1});
+                    variants.push_back({&p, static_cast<long>(s), dplans.size() - 1, old_by_rule});
                 }
                 any = true;
             }
         if (!any) {
             dplans.push_back(dist_plan(p, idb));
-            variants.push_back({&p, -1, dplans.size() - 1});
+            variants.push_back({&p, -1, dplans.size() - 1, {}});
         }
     }
     for (auto& v : variants)
-        for (size_t s = 0; s < v.plan->sources.size(); ++s)
-            if (static_cast<long>(s) != v.delta_source) full_read.insert(v.plan->sources[s].relation);
+        for (size_t s = 0; s < v.plan->sources.size(); ++s) {
+            if (static_cast<long>(s) == v.delta_source) continue;
+            full_read.insert(v.plan->sources[s].relation);
+            if (!v.old_src.empty() && v.old_src[s]) st->relations.at(v.plan->sources[s].relation)->keep_old = true;
+        }
     // Partition copies each IDB relation needs (static in the executed variant plans).
     if (eng.dist()) {
         for (auto& [name, r] : st->relations)
@@ -1165,7 +1221,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
             if (v.delta_source < 0 && iteration != 0) continue;
             RelState& hr = *st->relations.at(v.plan->head);
             HeadSink* sink = (hr.hash_mode && !eng.dist()) ? &sinks[v.plan->head] : nullptr;
-            eng.exec_variant(*v.plan, dplans[v.plan_index], v.delta_source, pooled[v.plan->head], sink);
+            eng.exec_variant(*v.plan, dplans[v.plan_index], v.delta_source, v.old_src, pooled[v.plan->head], sink);
         }
         tr("variants", ti, iteration);
         const auto tf = Clock::now();

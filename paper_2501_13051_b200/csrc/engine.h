@@ -122,6 +122,12 @@ struct RelState {
     bool idb = false;
     // Home copy: all rows (single GPU) or the rows owned by hash(col 0).
     DevVersion full, delta;
+    // FULL before the last merge (= FULL minus DELTA), kept when some variant
+    // reads it (exactly-once semi-naive variants); old_is_full when the last
+    // iteration added nothing.
+    bool keep_old = false;
+    bool old_is_full = true;
+    DevVersion full_old;
     // (0 = full, 1 = delta, col) -> index; invalidated when the version changes
     IndexMap indexes;
     // Partitioned evaluation: extra copies keyed on other probed columns.

@@ -298,3 +298,21 @@ def test_keyset_layouts_match_reference(ctx, group, monkeypatch):
         assert got == [tuple(s) for s in case["stats"]], (group, case["name"])
         for rel, exp in case["relations"].items():
             assert matches(st.dump(rel).reshape(-1), exp["dump"]), (group, case["name"], rel)
+
+
+@pytest.mark.parametrize("mode", ["reference", "exactly-once"])
+def test_seminaive_variants_match_reference(ctx, mode, monkeypatch):
+    # Default: the variant with DELTA at IDB occurrence i reads FULL - DELTA
+    # before i (each multi-DELTA derivation once); FVLOG_SEMINAIVE=reference
+    # reads FULL everywhere like P/src/engine.cpp:180-183. Same sets/stats.
+    if mode == "reference":
+        monkeypatch.setenv("FVLOG_SEMINAIVE", "reference")
+    for case in load_golden("engine.json"):
+        if case["name"] == "TC uniform 2000/10000":
+            continue
+        text, facts = golden_cases.program_and_facts(case)
+        st = E.evaluate_program(text, facts, ctx=ctx)
+        got = [(s.index, s.relation, s.delta_rows, s.full_rows, s.merges) for s in st.stats()]
+        assert got == [tuple(s) for s in case["stats"]], (mode, case["name"])
+        for rel, exp in case["relations"].items():
+            assert matches(st.dump(rel).reshape(-1), exp["dump"]), (mode, case["name"], rel)
