@@ -491,6 +491,17 @@ public:
                         spec.probe_count = c_->d_scalars + 24;
                         FV_CUDA(cudaMemsetAsync(spec.probe_count, 0, 8, c_->stream));
                     }
+                    // Partitioned: rows owned here are deduplicated in this
+                    // kernel, the others are pooled for the all-to-all.
+                    const bool route = D && !dp.replicated_out;
+                    if (route) {
+                        out.reserve(c_, T);
+                        spec.keys[0] = out.words[0].get() + out.n;
+                        spec.d_count = c_->d_scalars + 26;
+                        spec.remote_world = world_;
+                        spec.remote_rank = rank_;
+                        FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
+                    }
                     for (u64 t0 = 0; t0 < T; t0 += kFusedChunk) {
                         const u64 t1 = std::min(T, t0 + kFusedChunk);
                         hash_reserve(hr, *sink, t1 - t0);
@@ -502,6 +513,11 @@ public:
                         engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
                     }
                     sink->candidates += T;
+                    if (route) {
+                        u64 pooled = 0;
+                        c_->read_scalars(spec.d_count, &pooled, 1);
+                        out.n += pooled;
+                    }
                     if (trace_) {
                         u64 probes = 0;
                         c_->read_scalars(spec.probe_count, &probes, 1);
@@ -1220,7 +1236,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         for (auto& v : variants) {
             if (v.delta_source < 0 && iteration != 0) continue;
             RelState& hr = *st->relations.at(v.plan->head);
-            HeadSink* sink = (hr.hash_mode && !eng.dist()) ? &sinks[v.plan->head] : nullptr;
+            HeadSink* sink = hr.hash_mode ? &sinks[v.plan->head] : nullptr;
             eng.exec_variant(*v.plan, dplans[v.plan_index], v.delta_source, v.old_src, pooled[v.plan->head], sink);
         }
         tr("variants", ti, iteration);

@@ -253,6 +253,10 @@ struct OutSpec {
     u64* new_keys = nullptr;
     u64* new_count = nullptr;
     u64* probe_count = nullptr;  // optional (trace): key-set probes after the tile-local dedup
+    // Partitioned fused dedup: rows whose owner(hash(head col 0)) is not
+    // remote_rank are appended to keys[0][*d_count ...] (to be routed)
+    // instead of probing the local key set. remote_world = 0: all local.
+    u32 remote_world = 0, remote_rank = 0;
     // Key mode, one word, no key set: drop tile-local repeats and append the
     // tile's distinct keys at keys[0][*d_count ...].
     u32 tile_dedup = 0;

@@ -336,6 +336,21 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
             const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
             if (lane == 0 && m) atomicAdd(&sh.set_fill, m);
         }
+        if (spec.remote_world) {
+            // Rows owned by another rank go to the routing pool (one
+            // warp-aggregated append each) instead of the local key set.
+#pragma unroll
+            for (int k = 0; k < kMatItems; ++k) {
+                bool remote = false;
+                if ((keep_mask >> k) & 1u) {
+                    const u32 c0 = static_cast<u32>(spec.n_out >= 2 ? key[k] >> spec.shift : key[k]);
+                    remote = static_cast<u32>((static_cast<u64>(hash32(c0)) * spec.remote_world) >> 32) !=
+                             spec.remote_rank;
+                }
+                append_new(spec.keys[0], spec.d_count, remote, key[k]);
+                if (remote) keep_mask &= ~(1u << k);
+            }
+        }
         if (spec.probe_count) {
             const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
             if (lane == 0 && m) atomicAdd(reinterpret_cast<unsigned long long*>(spec.probe_count), static_cast<unsigned long long>(m));
