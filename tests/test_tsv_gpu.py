@@ -100,3 +100,18 @@ def test_large_integer_file_roundtrip():
     e = W.tc_uniform(2000, 10000, 5)
     text = "\n".join(f"{a}\t{b}" for a, b in e.tolist()) + "\n"
     _compare(W.TC_PROGRAM, {"edge": text}, ["reach", "edge"])
+
+
+@pytest.mark.parametrize("files", [
+    {"edge": ""},                      # empty file
+    {"edge": "\n\r\n\n"},              # only blank lines
+    {},                                # no facts file at all
+    {"edge": "1\t2\n", "reach": "5\t6\n7\t7\n"},   # IDB relation seeded from a file
+])
+def test_empty_and_seeded_inputs(files):
+    _compare(W.TC_PROGRAM, files, ["reach", "edge"])
+
+
+def test_relation_without_rules_or_facts():
+    # A relation declared only in a body: empty EDB, empty result, 1 iteration.
+    _compare("a(x, y) :- b(x, y), c(y).\n", {"b": "1\t2\n"}, ["a", "b", "c"])
