@@ -888,8 +888,15 @@ public:
         words.push_back(std::move(s.keys));
         s.cap = 0;
         // Levels-mode FULL is never merged, so Δ only has to be grouped by
-        // column 0 (its join index); a sorted FULL needs the full order.
-        engine_sort_keys(c_, words, nd, r.arity, st_.key_shift, r.levels_mode);
+        // column 0 (its join index): unary keys are distinct (already
+        // grouped), binary keys take a counting sort on column 0 when its
+        // domain is small, else the column-0 radix passes. A sorted FULL
+        // needs the full order.
+        if (!r.levels_mode) {
+            engine_sort_keys(c_, words, nd, r.arity, st_.key_shift);
+        } else if (r.arity == 2 && !engine_group_keys(c_, words[0], nd, st_.key_shift)) {
+            engine_sort_keys(c_, words, nd, r.arity, st_.key_shift, true);
+        }
         std::vector<u32*> dc;
         for (auto& col : Dv.cols) dc.push_back(col.get());
         engine_unpack_keys(c_, words[0].get(), nd, r.arity, st_.key_shift, dc);
