@@ -37,6 +37,11 @@ if [ -z "${SKIP_NCU:-}" ]; then
       --clock-control none --csv --log-file "$OUT/launches.csv" \
       python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > "$OUT/ncu_launch_bench.log" 2>&1
   echo "ncu launches exit $?" >> "$OUT/ncu_launch_bench.log"
+  for CFG in C1 C3 C4 C5; do
+    timeout 600 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --clock-control none --csv --log-file "$OUT/launches_$CFG.csv" \
+        python tools/bench_workloads.py --configs $CFG --steps 1 --warmup 0 --no-reference > /dev/null 2>&1
+  done
   for KS in ${NCU_KERNELS:-materialize_kernel:6 onesweep_kernel:30 hash_rehash_kernel:1}; do
     K=${KS%%:*}; SKIP=${KS##*:}
     timeout 900 $NCU --set full --clock-control none --import-source on -k "regex:$K" \

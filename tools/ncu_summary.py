@@ -79,6 +79,12 @@ def main(src, dst):
                "total_kernel_ms": total_ms, "kernels": launches},
               open(os.path.join(dst, "launches.json"), "w"), indent=1)
     for f in sorted(os.listdir(src)):
+        if f.startswith("launches_") and f.endswith(".csv"):
+            ks, tot = summarise(os.path.join(src, f))
+            json.dump({"source": f"ncu launch list of one {f[9:-4]} fixpoint (tools/bench_workloads.py)",
+                       "total_kernel_ms": tot, "kernels": ks},
+                      open(os.path.join(dst, f.replace(".csv", ".json")), "w"), indent=1)
+    for f in sorted(os.listdir(src)):
         if f.startswith("full_") and f.endswith(".ncu-rep"):
             cap = full_capture(os.path.join(src, f))
             if cap:
