@@ -42,12 +42,17 @@ if [ -z "${SKIP_NCU:-}" ]; then
         --clock-control none --csv --log-file "$OUT/launches_$CFG.csv" \
         python tools/bench_workloads.py --configs $CFG --steps 1 --warmup 0 --no-reference > /dev/null 2>&1
   done
-  for KS in ${NCU_KERNELS:-materialize_kernel:6 onesweep_kernel:30 hash_rehash_kernel:1}; do
+  for KS in ${NCU_KERNELS:-materialize_kernel:6 group_scatter_kernel:10 hash_rehash_kernel:1}; do
     K=${KS%%:*}; SKIP=${KS##*:}
     timeout 900 $NCU --set full --clock-control none --import-source on -k "regex:$K" \
         --launch-skip $SKIP -c ${NCU_COUNT:-1} -f -o "$OUT/full_$K" \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > "$OUT/ncu_full_$K.log" 2>&1
     echo "ncu full $K exit $?" >> "$OUT/ncu_full_$K.log"
   done
+fi
+if [ -z "${SKIP_NCU:-}" ] && [ -x tools/fvlog_sortbench ]; then
+  timeout 300 tools/fvlog_sortbench 200 40 > "$OUT/sortbench.json" 2>&1
+  timeout 600 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:onesweep_kernel \
+      --launch-skip 2 -c 1 -f -o "$OUT/full_onesweep_kernel" tools/fvlog_sortbench 200 40 > /dev/null 2>&1
 fi
 echo done > "$OUT/DONE"
