@@ -238,7 +238,7 @@ struct MatShared {
 
 // One output tile of the output-partitioned join expansion (see lbs_kernel in
 // column_ops.cu). All threads of the block call it for the same tile.
-template <bool COMPACT>
+template <bool COMPACT, bool REMOTE>
 __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets, u64 o_begin, u64 total,
                                                  const u32* __restrict__ starts, const u64* __restrict__ tile_jlo,
                                                  const u64* __restrict__ tile_jhi, const OutSpec& spec, u64 t,
@@ -336,7 +336,7 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
             const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
             if (lane == 0 && m) atomicAdd(&sh.set_fill, m);
         }
-        if (spec.remote_world) {
+        if (REMOTE) {
             // Rows owned by another rank go to the routing pool (one
             // warp-aggregated append each) instead of the local key set.
 #pragma unroll
@@ -406,8 +406,15 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
 // That halves TC's key-set probes, but the dropped ones were L2 hits and the
 // serialised tiles cost more than they save, so the default is one tile.
 constexpr int kMatGroup = 1;  // measured: 1 is best on C1-C4 (FVLOG_MAT_GROUP overrides)
-template <bool COMPACT>
-__global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __restrict__ offsets, u64 m,
+// REMOTE: partitioned fused dedup (spec.remote_world > 0), a separate
+// instantiation so the single-GPU kernel keeps its register budget.
+// Three 512-thread CTAs per SM (<= 42 registers): C2 125 -> 121 ms, C4 208 ->
+// 194 ms against the compiler's unbounded choice (48 registers, 2 CTAs).
+#ifndef FV_MAT_MIN_BLOCKS
+#define FV_MAT_MIN_BLOCKS 3
+#endif
+template <bool COMPACT, bool REMOTE>
+__global__ void __launch_bounds__(kMatBlock, FV_MAT_MIN_BLOCKS) materialize_kernel(const u64* __restrict__ offsets, u64 m,
                                                                  u64 o_begin, u64 total,
                                                                  const u32* __restrict__ starts,
                                                                  const u64* __restrict__ tile_jlo,
@@ -426,7 +433,7 @@ __global__ void __launch_bounds__(kMatBlock) materialize_kernel(const u64* __res
             if (threadIdx.x == 0) sh.set_fill = 0;
             __syncthreads();
         }
-        materialize_tile<COMPACT>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh);
+        materialize_tile<COMPACT, REMOTE>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh);
     }
 }
 
@@ -1109,12 +1116,22 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
     }();
     const u32 group = (spec.ht_slots || spec.tile_dedup) ? (env_group ? env_group : u32(kMatGroup)) : 1u;
     const unsigned grid = static_cast<unsigned>(ceil_div(tiles, group));
-    if (spec.n_filters)
-        materialize_kernel<true><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, rows.get(),
-                                                                   rows.get() + tiles, tiles, group, spec);
-    else
-        materialize_kernel<false><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, rows.get(),
-                                                                    rows.get() + tiles, tiles, group, spec);
+    const u64* jlo = rows.get();
+    const u64* jhi = rows.get() + tiles;
+    if (spec.remote_world) {
+        if (spec.n_filters)
+            materialize_kernel<true, true><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, jlo,
+                                                                             jhi, tiles, group, spec);
+        else
+            materialize_kernel<false, true><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts,
+                                                                              jlo, jhi, tiles, group, spec);
+    } else if (spec.n_filters) {
+        materialize_kernel<true, false><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, jlo,
+                                                                          jhi, tiles, group, spec);
+    } else {
+        materialize_kernel<false, false><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, jlo,
+                                                                           jhi, tiles, group, spec);
+    }
     FV_CUDA(cudaGetLastError());
     c->count_launch(2);
 }
