@@ -892,10 +892,15 @@ public:
         // grouped), binary keys take a counting sort on column 0 when its
         // domain is small, else the column-0 radix passes. A sorted FULL
         // needs the full order.
+        // The counting sort also yields DELTA's column-0 join index (its runs
+        // are the non-empty counters), installed below once DELTA is in place.
+        auto delta_index = std::make_unique<JoinIndex>();
+        bool have_index = false;
         if (!r.levels_mode) {
             engine_sort_keys(c_, words, nd, r.arity, st_.key_shift);
-        } else if (r.arity == 2 && !engine_group_keys(c_, words[0], nd, st_.key_shift)) {
-            engine_sort_keys(c_, words, nd, r.arity, st_.key_shift, true);
+        } else if (r.arity == 2) {
+            have_index = engine_group_keys(c_, words[0], nd, st_.key_shift, delta_index.get());
+            if (!have_index) engine_sort_keys(c_, words, nd, r.arity, st_.key_shift, true);
         }
         std::vector<u32*> dc;
         for (auto& col : Dv.cols) dc.push_back(col.get());
@@ -930,6 +935,10 @@ public:
             r.full = std::move(C);
         }
         r.delta = std::move(Dv);
+        if (have_index) {
+            delta_index->rows = &r.delta;
+            r.indexes.emplace(std::make_pair(static_cast<int>(kDelta), 0u), std::move(delta_index));
+        }
         return nd;
     }
 

@@ -278,7 +278,9 @@ u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32
 // Group n one-word arity-2 keys by their first column (key >> shift; order
 // inside a group unspecified) by counting sort; false (keys untouched) when
 // the first-column domain exceeds 2^24 or averages > 512 keys per value.
-bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift);
+// With `runs`, also fills its column-0 run index (ukeys/ustart/ucount +
+// hash; rows left to the caller) for the grouped keys.
+bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs = nullptr);
 // Keys -> SoA columns (one word per row, arity <= 2).
 void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, const std::vector<u32*>& cols);
 

@@ -873,6 +873,24 @@ __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 sh
     }
 }
 
+// Runs of the grouped keys straight from the counters: one row per non-empty
+// value (value, base, count) — the column-0 join index of the grouped DELTA
+// without a pass over its rows.
+struct GroupRunsOp {
+    const u32* cnt;
+    const u64* base;
+    u32* ukeys;
+    u32* ustart;
+    u32* ucount;
+    __device__ u64 value(u64 i) const { return cnt[i] ? 1 : 0; }
+    __device__ void emit(u64 i, u64 p, u64 v) const {
+        if (!v) return;
+        ukeys[p] = static_cast<u32>(i);
+        ustart[p] = static_cast<u32>(base[i]);
+        ucount[p] = cnt[i];
+    }
+};
+
 struct GroupBaseOp {
     const u32* cnt;
     u64* base;
@@ -1003,11 +1021,13 @@ void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to) {
     c->count_launch();
 }
 
-bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift) {
+static void build_run_hash(Ctx* c, JoinIndex& idx);
+
+bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs) {
     // Small domains with thousands of keys per value serialize on the
     // counters (C1: 2.6 K keys per value, 2.2 -> 5.1 ms); radix there.
     if (shift > kGroupMaxBits || n > (u64(kGroupMaxPerValue) << shift)) return false;
-    if (n <= 1) return true;
+    if (n <= 1) return false;  // already grouped; the caller indexes it the usual way
     const u64 domain = u64(1) << shift;
     DBuf<u32> cnt(c, domain), cursor(c, domain);
     DBuf<u64> base(c, domain), out(c, n);
@@ -1024,6 +1044,16 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift) {
         c->count_launch(2);
     }
     keys.swap(out);
+    if (runs) {
+        DBuf<u32> uk(c, std::min<u64>(n, domain)), us(c, std::min<u64>(n, domain)), uc(c, std::min<u64>(n, domain));
+        u64* d = c->d_scalars + 34;
+        tile_scan(c, GroupRunsOp{cnt.get(), base.get(), uk.get(), us.get(), uc.get()}, domain, d);
+        c->read_scalars(d, &runs->n_unique, 1);
+        runs->ukeys = std::move(uk);
+        runs->ustart = std::move(us);
+        runs->ucount = std::move(uc);
+        build_run_hash(c, *runs);
+    }
     return true;
 }
 
@@ -1163,15 +1193,24 @@ void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx) {
     FV_CUDA(cudaMemcpyAsync(idx.ukeys.get(), uk.get(), 4 * nu, cudaMemcpyDeviceToDevice, c->stream));
     FV_CUDA(cudaMemcpyAsync(idx.ustart.get(), us.get(), 4 * nu, cudaMemcpyDeviceToDevice, c->stream));
     runs_count_kernel<<<grid_for(nu), 256, 0, c->stream>>>(idx.ustart.get(), idx.ucount.get(), nu, n);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+    build_run_hash(c, idx);
+}
+
+// Hash table over the unique keys of idx (key -> run number).
+static void build_run_hash(Ctx* c, JoinIndex& idx) {
+    const u64 nu = idx.n_unique;
     u64 cap = 64;
     while (cap < 2 * nu) cap <<= 1;
     idx.ht.slots = DBuf<u64>(c, cap);
     idx.ht.mask = static_cast<u32>(cap - 1);
     FV_CUDA(cudaMemsetAsync(idx.ht.slots.get(), 0xff, 8 * cap, c->stream));
+    if (!nu) return;
     hash_build_kernel<<<grid_for(nu), 256, 0, c->stream>>>(
         idx.ukeys.get(), nu, reinterpret_cast<unsigned long long*>(idx.ht.slots.get()), idx.ht.mask);
     FV_CUDA(cudaGetLastError());
-    c->count_launch(2);
+    c->count_launch();
 }
 
 static Cols8 cols8(const std::vector<const u32*>& cols) {
