@@ -878,6 +878,9 @@ public:
         DevVersion Dv;
         Dv.n = nd;
         for (u32 j = 0; j < r.arity; ++j) Dv.cols.emplace_back(c_, nd);
+        // Levels mode: the previous DELTA becomes a level (moved, no copy);
+        // the current DELTA is the newest level until the next iteration.
+        if (r.levels_mode && r.delta.n) r.levels.push_back(std::move(r.delta));
         if (nd == 0) {
             r.delta = std::move(Dv);
             set_old(r, nullptr);
@@ -899,21 +902,17 @@ public:
         if (!r.levels_mode) {
             engine_sort_keys(c_, words, nd, r.arity, st_.key_shift);
         } else if (r.arity == 2) {
-            have_index = engine_group_keys(c_, words[0], nd, st_.key_shift, delta_index.get());
+            // The scatter writes DELTA's columns directly (no unpack pass).
+            have_index = engine_group_keys(c_, words[0], nd, st_.key_shift, delta_index.get(), Dv.cols[0].get(),
+                                           Dv.cols[1].get());
             if (!have_index) engine_sort_keys(c_, words, nd, r.arity, st_.key_shift, true);
         }
-        std::vector<u32*> dc;
-        for (auto& col : Dv.cols) dc.push_back(col.get());
-        engine_unpack_keys(c_, words[0].get(), nd, r.arity, st_.key_shift, dc);
+        if (!have_index) {
+            std::vector<u32*> dc;
+            for (auto& col : Dv.cols) dc.push_back(col.get());
+            engine_unpack_keys(c_, words[0].get(), nd, r.arity, st_.key_shift, dc);
+        }
         if (r.levels_mode) {
-            DevVersion lv;
-            lv.n = nd;
-            for (u32 j = 0; j < r.arity; ++j) {
-                lv.cols.emplace_back(c_, nd);
-                FV_CUDA(cudaMemcpyAsync(lv.cols[j].get(), Dv.cols[j].get(), 4 * nd, cudaMemcpyDeviceToDevice,
-                                        c_->stream));
-            }
-            r.levels.push_back(std::move(lv));
             r.level_rows += nd;
         } else {
             // FULL is read by joins: keep it one sorted version.
@@ -1343,6 +1342,14 @@ std::vector<std::unique_ptr<EvalState>> evaluate_sharded(Ctx* base, u32 world, c
 
 namespace {
 
+// Levels-mode FULL: the past DELTAs plus the current one.
+std::vector<const DevVersion*> levels_of(const RelState& r) {
+    std::vector<const DevVersion*> out;
+    for (auto& lv : r.levels) out.push_back(&lv);
+    if (r.delta.n) out.push_back(&r.delta);
+    return out;
+}
+
 // The relation's rows as lexicographically sorted device columns: FULL
 // itself, or (levels mode) one sort of the concatenated levels into `tmp`.
 const DevVersion& sorted_rows(const EvalState& s, const RelState& r, DevVersion& tmp) {
@@ -1356,11 +1363,11 @@ const DevVersion& sorted_rows(const EvalState& s, const RelState& r, DevVersion&
     for (u32 j = 0; j < r.arity; ++j) {
         DBuf<u32> col(c, n);
         u64 off = 0;
-        for (auto& lv : r.levels) {
-            if (lv.n)
-                FV_CUDA(cudaMemcpyAsync(col.get() + off, lv.cols[j].get(), 4 * lv.n, cudaMemcpyDeviceToDevice,
+        for (const DevVersion* lv : levels_of(r)) {
+            if (lv->n)
+                FV_CUDA(cudaMemcpyAsync(col.get() + off, lv->cols[j].get(), 4 * lv->n, cudaMemcpyDeviceToDevice,
                                         c->stream));
-            off += lv.n;
+            off += lv->n;
         }
         tmp.cols.push_back(std::move(col));
     }
@@ -1411,7 +1418,7 @@ u64 fingerprint(const EvalState& s, const std::string& rel) {
     const RelState& r = *it->second;
     if (!r.levels_mode) return engine_fingerprint(s.ctx, r.full.ptrs(), r.full.n, r.arity);
     u64 h = 0;  // the fingerprint is a sum over rows: additive over levels
-    for (auto& lv : r.levels) h += engine_fingerprint(s.ctx, lv.ptrs(), lv.n, r.arity);
+    for (const DevVersion* lv : levels_of(r)) h += engine_fingerprint(s.ctx, lv->ptrs(), lv->n, r.arity);
     return h;
 }
 

@@ -137,8 +137,9 @@ struct RelState {
     // inserted straight from the join kernel; only new rows get sorted.
     bool hash_mode = false;
     KeySet keys;
-    // With hash dedup, a FULL no join reads is kept as sorted levels (one
-    // per iteration, merged only for dumps); otherwise it is `full`, merged
+    // With hash dedup, a FULL no join reads is kept as levels: the past DELTAs
+    // (one per iteration, grouped by column 0) plus the current `delta`,
+    // concatenated and sorted only for dumps; otherwise it is `full`, merged
     // with each sorted Δ.
     bool levels_mode = false;
     std::vector<DevVersion> levels;
@@ -280,7 +281,10 @@ u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32
 // the first-column domain exceeds 2^24 or averages > 512 keys per value.
 // With `runs`, also fills its column-0 run index (ukeys/ustart/ucount +
 // hash; rows left to the caller) for the grouped keys.
-bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs = nullptr);
+// With col0/col1, the grouped rows are written as SoA columns instead
+// (keys left as they were).
+bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs = nullptr, u32* col0 = nullptr,
+                       u32* col1 = nullptr);
 // Keys -> SoA columns (one word per row, arity <= 2).
 void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, const std::vector<u32*>& cols);
 

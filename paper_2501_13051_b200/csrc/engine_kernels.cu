@@ -853,7 +853,8 @@ __global__ void group_count_kernel(const u64* __restrict__ keys, u64 n, u32 shif
 }
 
 __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 shift, const u64* __restrict__ base,
-                                     u32* __restrict__ cursor, u64* __restrict__ out) {
+                                     u32* __restrict__ cursor, u64* __restrict__ out, u32* __restrict__ c0,
+                                     u32* __restrict__ c1) {
     const u64 n_round = ceil_div(n, 32) * 32;
     const u32 lane = lane_id();
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n_round; i += u64(gridDim.x) * blockDim.x) {
@@ -869,7 +870,14 @@ __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 sh
         } else {
             pos = valid ? base[g] + atomicAdd(cursor + g, 1u) : 0;
         }
-        if (valid) out[pos] = key;
+        if (valid) {
+            if (c0) {  // unpacked straight into SoA columns
+                c0[pos] = g;
+                c1[pos] = static_cast<u32>(key & ((u64(1) << shift) - 1));
+            } else {
+                out[pos] = key;
+            }
+        }
     }
 }
 
@@ -1023,14 +1031,14 @@ void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to) {
 
 static void build_run_hash(Ctx* c, JoinIndex& idx);
 
-bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs) {
+bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs, u32* col0, u32* col1) {
     // Small domains with thousands of keys per value serialize on the
     // counters (C1: 2.6 K keys per value, 2.2 -> 5.1 ms); radix there.
     if (shift > kGroupMaxBits || n > (u64(kGroupMaxPerValue) << shift)) return false;
     if (n <= 1) return false;  // already grouped; the caller indexes it the usual way
     const u64 domain = u64(1) << shift;
     DBuf<u32> cnt(c, domain), cursor(c, domain);
-    DBuf<u64> base(c, domain), out(c, n);
+    DBuf<u64> base(c, domain), out(c, col0 ? 0 : n);
     FV_CUDA(cudaMemsetAsync(cnt.get(), 0, 4 * domain, c->stream));
     FV_CUDA(cudaMemsetAsync(cursor.get(), 0, 4 * domain, c->stream));
     {
@@ -1039,11 +1047,11 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
         FV_CUDA(cudaGetLastError());
         tile_scan(c, GroupBaseOp{cnt.get(), base.get()}, domain, nullptr);
         group_scatter_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys.get(), n, shift, base.get(), cursor.get(),
-                                                                  out.get());
+                                                                  out.get(), col0, col1);
         FV_CUDA(cudaGetLastError());
         c->count_launch(2);
     }
-    keys.swap(out);
+    if (!col0) keys.swap(out);
     if (runs) {
         DBuf<u32> uk(c, std::min<u64>(n, domain)), us(c, std::min<u64>(n, domain)), uc(c, std::min<u64>(n, domain));
         u64* d = c->d_scalars + 34;
