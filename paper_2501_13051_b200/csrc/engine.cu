@@ -54,6 +54,12 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 
+#ifndef FV_KEYSET_GROWTH
+#define FV_KEYSET_GROWTH 4
+#endif
+// New key-set capacity >= kKeysetGrowth x the worst-case key count.
+constexpr u64 kKeysetGrowth = FV_KEYSET_GROWTH;
+
 // Join outputs per fused join+dedup launch (see exec_variant).
 constexpr u64 kFusedChunk = u64(1) << 28;
 
@@ -815,7 +821,7 @@ public:
         // Memory-tight: settle for 1/2, then 3/4 (fails loudly beyond).
         const u64 need = r.keys.count + pending + extra;
         u64 cap = 1u << 16;
-        while (cap < 4 * need) cap <<= 1;
+        while (cap < kKeysetGrowth * need) cap <<= 1;
         KeySet ns;
         for (int attempt = 0;; ++attempt) {
             try {
