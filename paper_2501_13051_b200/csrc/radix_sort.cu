@@ -25,6 +25,7 @@ namespace fv {
 namespace {
 
 constexpr int kRadixBits = 8;
+constexpr u64 kSkipCheckMin = u64(1) << 20;  // sorts smaller than this run every pass
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortBlock = 256;
 constexpr int kSortWarps = kSortBlock / 32;
@@ -309,8 +310,10 @@ bool radix_sort_impl(Ctx* c, K* keys, K* keys_alt, u32* vals, u32* vals_alt, u64
         FV_CUDA(cudaGetLastError());
         c->count_launch(2);
     }
+    // Skipping constant-digit passes needs the histogram on the host (one
+    // sync); for small inputs every pass is cheaper than the round trip.
     u64 triv[8] = {0};
-    c->read_scalars(trivial, triv, static_cast<int>(npass));
+    if (n >= kSkipCheckMin) c->read_scalars(trivial, triv, static_cast<int>(npass));
 
     bool in_alt = false;
     for (u32 p = 0; p < npass; ++p) {
