@@ -1109,15 +1109,14 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     for (auto& p : plans)
         for (auto& s : p.sources)
             for (auto& cs : s.const_selects) vmax = std::max<u64>(vmax, cs.second);
-    u64* dmax = c->d_scalars + 22;
-    for (auto& [name, vp] : raw) {
-        const DevVersion& v = *vp;
-        for (auto& col : v.cols) {
-            reduce_max_u32(c, col.get(), v.n, dmax);
-            u64 m = 0;
-            c->read_scalars(dmax, &m, 1);
-            vmax = std::max(vmax, m);
-        }
+    u64* dmax = c->d_scalars + 22;  // one max over every EDB column, one readback
+    FV_CUDA(cudaMemsetAsync(dmax, 0, sizeof(u64), c->stream));
+    for (auto& [name, vp] : raw)
+        for (auto& col : vp->cols) reduce_max_u32(c, col.get(), vp->n, dmax, true);
+    {
+        u64 m = 0;
+        c->read_scalars(dmax, &m, 1);
+        vmax = std::max(vmax, m);
     }
     if (eng.dist()) {  // every rank must pack keys with the same shift
         std::vector<u64> bits(64, 0);

@@ -41,8 +41,8 @@ void exclusive_scan_counts(Ctx* c, const u32* counts, u64* offsets, u64 n) {
     tile_scan(c, ScanCountsOp{counts, offsets, n}, n, nullptr);
 }
 
-void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out) {
-    FV_CUDA(cudaMemsetAsync(d_out, 0, sizeof(u64), c->stream));
+void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out, bool accumulate) {
+    if (!accumulate) FV_CUDA(cudaMemsetAsync(d_out, 0, sizeof(u64), c->stream));
     if (n == 0) return;
     reduce_max_kernel<<<grid_for(n), 256, 0, c->stream>>>(in, n,
                                                          reinterpret_cast<unsigned long long*>(d_out));

@@ -145,7 +145,8 @@ struct SelectFlagsOp {
 void exclusive_scan_counts(Ctx* c, const u32* counts, u64* offsets, u64 n);
 
 // Device reductions returning to a device scalar.
-void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out);
+// accumulate: fold into the existing *d_out (max) instead of resetting it.
+void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out, bool accumulate = false);
 
 // Fill / iota helpers.
 void iota_u32(Ctx* c, u32* out, u64 n);
