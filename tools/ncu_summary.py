@@ -24,8 +24,9 @@ from launch_summary import summarise  # noqa: E402
 
 # bench.py / fv_ctx_profile names -> CUDA kernel names in the launch list
 PROFILER_TO_KERNEL = {
-    "join_dedup": "materialize_kernel<0>",
-    "join_materialize": "materialize_kernel<0>",
+    "join_dedup": "materialize_kernel<0, 0>",
+    "join_materialize": "materialize_kernel<0, 0>",
+    "group_keys": ["group_count_kernel", "group_scatter_kernel"],
     "hash_insert": "hash_insert_keys_kernel",
     "radix_onesweep_u64": "onesweep_kernel<unsigned long, 0>",
     "radix_histogram": "radix_hist_kernel<unsigned long>",
