@@ -60,6 +60,12 @@ using Clock = std::chrono::steady_clock;
 // New key-set capacity >= kKeysetGrowth x the worst-case key count.
 constexpr u64 kKeysetGrowth = FV_KEYSET_GROWTH;
 
+// Pooled (unfused) candidates: rows per join chunk, and the pool size that
+// triggers a sort-unique compaction before the next chunk (FVLOG_POOL_BUDGET
+// and FVLOG_POOL_CHUNK, in rows, override both — tests use tiny values).
+constexpr u64 kPoolChunk = u64(1) << 27;
+constexpr u64 kPoolBudget = u64(1) << 29;
+
 // Join outputs per fused join+dedup launch (see exec_variant).
 constexpr u64 kFusedChunk = u64(1) << 28;
 
@@ -532,11 +538,31 @@ public:
                     }
                     return;
                 }
-                out.reserve(c_, T);
-                for (u32 w = 0; w < W; ++w) spec.keys[w] = out.words[w].get() + out.n;
                 // One-word keys: drop tile-local repeats before they are
                 // pooled (and, partitioned, routed over NVLink).
                 if (W == 1) spec.tile_dedup = 1;
+                // Pooled candidates (no key set) are produced in chunks and
+                // the pool is sort-uniqued whenever the next chunk would
+                // push it past kPoolBudget rows (SURVEY.md §7 hard part 1:
+                // the reference materializes every candidate at once).
+                const bool compacts = spec.n_filters || spec.tile_dedup;
+                for (u64 t0 = 0; t0 < T; t0 += pool_chunk_) {
+                    const u64 t1 = std::min(T, t0 + pool_chunk_);
+                    if (out.n && out.n + (t1 - t0) > pool_budget_) compact_pool(out);
+                    out.reserve(c_, t1 - t0);
+                    // Positional (uncompacted) writes use absolute output
+                    // indices: bias the base so output t0 lands at out.n.
+                    for (u32 w = 0; w < W; ++w) spec.keys[w] = out.words[w].get() + out.n - (compacts ? 0 : t0);
+                    if (compacts) {
+                        spec.d_count = c_->d_scalars + 20;
+                        FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
+                    }
+                    engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
+                    u64 produced = t1 - t0;
+                    if (compacts) c_->read_scalars(spec.d_count, &produced, 1);
+                    out.n += produced;
+                }
+                return;
             } else {
                 spec.key_mode = 0;
                 u32 j = 0;
@@ -559,10 +585,6 @@ public:
             engine_materialize(c_, offsets.get(), n, T, starts.get(), spec);
             u64 produced = T;
             if (compacts) c_->read_scalars(spec.d_count, &produced, 1);
-            if (last) {
-                out.n += produced;
-                return;
-            }
             next.n = produced;
             u32 bound_cols = 0;
             for (u32 s = 0; s <= R; ++s) bound_cols += plan.sources[s].arity;
@@ -651,6 +673,19 @@ public:
         for (auto& [ref, ptr] : x.cols) ptr = remap.at(ptr);
         x.owned = std::move(out);
         x.n = k;
+    }
+
+    // Sort-unique the pooled candidates in place (bounded-memory pooling).
+    void compact_pool(CandPool& pool) {
+        engine_sort_keys(c_, pool.words, pool.n, pool.arity, st_.key_shift);
+        std::vector<DBuf<u64>> uniq;
+        const u64 k = engine_unique_words(c_, pool.words, pool.n, uniq);
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   pool compaction %llu -> %llu rows\n",
+                         static_cast<unsigned long long>(pool.n), static_cast<unsigned long long>(k));
+        pool.words = std::move(uniq);
+        pool.cap = pool.n;  // buffers were sized n; k rows are live
+        pool.n = k;
     }
 
     // Sort candidates and fold them into (full, delta); returns |DELTA|.
@@ -959,6 +994,12 @@ private:
     bool force_partitioned_ = false;
     std::map<InterKey, InterPolicy> inter_policy_;
     const bool trace_ = std::getenv("FVLOG_TRACE") != nullptr;
+    static u64 env_rows(const char* name, u64 dflt) {
+        const char* e = std::getenv(name);
+        return e && std::atoll(e) > 0 ? static_cast<u64>(std::atoll(e)) : dflt;
+    }
+    const u64 pool_chunk_ = env_rows("FVLOG_POOL_CHUNK", kPoolChunk);
+    const u64 pool_budget_ = env_rows("FVLOG_POOL_BUDGET", kPoolBudget);
     const double group_ratio_ = [] {
         const char* e = std::getenv("FVLOG_GROUP_RATIO");
         return e ? std::atof(e) : kGroupedRatio;

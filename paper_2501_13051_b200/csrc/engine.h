@@ -285,6 +285,8 @@ u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32
 // (keys left as they were).
 bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs = nullptr, u32* col0 = nullptr,
                        u32* col1 = nullptr);
+// Distinct rows of sorted packed keys into fresh word buffers; returns the count.
+u64 engine_unique_words(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, std::vector<DBuf<u64>>& out);
 // Keys -> SoA columns (one word per row, arity <= 2).
 void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, const std::vector<u32*>& cols);
 

@@ -1095,6 +1095,42 @@ u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32
     return k;
 }
 
+// Distinct rows of sorted packed keys, kept packed (pool compaction).
+struct UniqueWordsOp {
+    Words4 w, out;
+    u32 words;
+    __device__ u64 value(u64 i) const {
+        if (i == 0) return 1;
+        for (u32 k = 0; k < words; ++k)
+            if (w.p[k][i] != w.p[k][i - 1]) return 1;
+        return 0;
+    }
+    __device__ void emit(u64 i, u64 pos, u64 v) const {
+        if (!v) return;
+        for (u32 k = 0; k < words; ++k) out.p[k][pos] = w.p[k][i];
+    }
+};
+
+u64 engine_unique_words(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, std::vector<DBuf<u64>>& out) {
+    out.clear();
+    UniqueWordsOp op{};
+    op.words = static_cast<u32>(words.size());
+    for (u32 k = 0; k < op.words; ++k) {
+        out.emplace_back(c, n);
+        op.w.p[k] = const_cast<u64*>(words[k].get());
+        op.out.p[k] = out.back().get();
+    }
+    if (!n) return 0;
+    u64* d = c->d_scalars + 35;
+    {
+        ProfScope prof(c, "unique_words", double(n) * 8.0 * op.words);
+        tile_scan(c, op, n, d);
+    }
+    u64 k = 0;
+    c->read_scalars(d, &k, 1);
+    return k;
+}
+
 u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids) {
     if (!n) return 0;
     u64* d = c->d_scalars + 18;

@@ -316,3 +316,21 @@ def test_seminaive_variants_match_reference(ctx, mode, monkeypatch):
         assert got == [tuple(s) for s in case["stats"]], (mode, case["name"])
         for rel, exp in case["relations"].items():
             assert matches(st.dump(rel).reshape(-1), exp["dump"]), (mode, case["name"], rel)
+
+
+def test_bounded_pool_compaction_matches_reference(ctx, monkeypatch):
+    # Sorted-mode dedup with tiny join chunks and pool budget: candidates are
+    # produced chunk by chunk and the pool is sort-uniqued whenever it would
+    # outgrow the budget (bounded memory); results and stats must not change.
+    monkeypatch.setenv("FVLOG_DEDUP", "sort")
+    monkeypatch.setenv("FVLOG_POOL_CHUNK", "1000")
+    monkeypatch.setenv("FVLOG_POOL_BUDGET", "3000")
+    for case in load_golden("engine.json"):
+        if case["name"] in ("TC uniform 2000/10000", "SG tree depth 10"):
+            continue
+        text, facts = golden_cases.program_and_facts(case)
+        st = E.evaluate_program(text, facts, ctx=ctx)
+        got = [(s.index, s.relation, s.delta_rows, s.full_rows, s.merges) for s in st.stats()]
+        assert got == [tuple(s) for s in case["stats"]], case["name"]
+        for rel, exp in case["relations"].items():
+            assert matches(st.dump(rel).reshape(-1), exp["dump"]), (case["name"], rel)
