@@ -408,7 +408,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fvlog", choices=["fvlog", "reference"])
-    ap.add_argument("--ref-components", type=int, default=20)
+    ap.add_argument("--ref-components", type=int, default=30)
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")

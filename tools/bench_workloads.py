@@ -37,8 +37,8 @@ CONFIGS = {
                sample=lambda: {"edge": W.tc_uniform(2_000, 10_000, 1)}, sample_desc="tc_uniform(2000, 10000, 1)"),
     "C2": dict(name="TC power-law 1000 x (1000 nodes, 5000 edges)", program=W.TC_PROGRAM,
                facts=lambda: {"edge": W.tc_powerlaw(1000, 1000, 5000, 1)},
-               sample=lambda: {"edge": W.tc_powerlaw(1000, 1000, 5000, 1)[:20 * 5000]},
-               sample_desc="first 20 of the 1000 components"),
+               sample=lambda: {"edge": W.tc_powerlaw(1000, 1000, 5000, 1)[:30 * 5000]},
+               sample_desc="first 30 of the 1000 components"),
     "C3": dict(name="SG forest of 244 complete binary trees, depth 10 (499,224 edges)", program=W.SG_PROGRAM,
                facts=lambda: {"edge": W.sg_forest(244, 10)},
                sample=lambda: {"edge": W.sg_forest(8, 10)}, sample_desc="sg_forest(8, 10)"),
