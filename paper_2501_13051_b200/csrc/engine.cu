@@ -64,6 +64,9 @@ constexpr u64 kKeysetGrowth = FV_KEYSET_GROWTH;
 // triggers a sort-unique compaction before the next chunk (FVLOG_POOL_BUDGET
 // and FVLOG_POOL_CHUNK, in rows, override both — tests use tiny values).
 constexpr u64 kPoolChunk = u64(1) << 27;
+// Join intermediates larger than this are carried through the rest of the
+// chain chunk by chunk (FVLOG_INTER_CHUNK overrides).
+constexpr u64 kInterChunk = u64(1) << 28;
 constexpr u64 kPoolBudget = u64(1) << 29;
 
 // Join outputs per fused join+dedup launch (see exec_variant).
@@ -407,202 +410,65 @@ public:
 
     // ---- execute_plan (P/src/engine.cpp:72-146) for one variant ------------------
 
+    // One variant's execution state (execute_plan, P/src/engine.cpp:72-146).
+    struct VarRun {
+        const Plan& plan;
+        const DistPlan& dp;
+        long delta_source;
+        std::vector<const DevVersion*> ver;
+        std::vector<Which> which;
+        std::vector<std::set<ColRef>> needed;  // columns still needed after join step k
+        u32 W = 1;
+        bool src0_pending = false;
+        bool D = false;
+        CandPool& out;
+        HeadSink* sink;
+    };
+
     // `old_src[s]`: source s reads FULL - DELTA instead of FULL (exactly-once
     // variants; empty = every non-DELTA source reads FULL, the reference).
     void exec_variant(const Plan& plan, const DistPlan& dp, long delta_source, const std::vector<u8>& old_src,
                       CandPool& out, HeadSink* sink) {
         const u32 ns = static_cast<u32>(plan.sources.size());
-        const bool D = dist();
-        std::vector<const DevVersion*> ver(ns);
-        std::vector<Which> which(ns, kFull);
+        VarRun v{plan, dp, delta_source, std::vector<const DevVersion*>(ns), std::vector<Which>(ns, kFull),
+                 {}, (plan.head_arity + 1) / 2, plan.sources[0].constrained(), dist(), out, sink};
         for (u32 s = 0; s < ns; ++s) {
             RelState& r = rel(plan.sources[s].relation);
             const u32 kc = partitioned(r) ? dp.src_copy[s] : 0;
-            if (static_cast<long>(s) == delta_source) which[s] = kDelta;
-            else if (!old_src.empty() && old_src[s]) which[s] = kOld;
-            ver[s] = &version(r, kc, which[s]);
-            if (!D && ver[s]->n == 0) return;  // engine.cpp:76-78
+            if (static_cast<long>(s) == delta_source) v.which[s] = kDelta;
+            else if (!old_src.empty() && old_src[s]) v.which[s] = kOld;
+            v.ver[s] = &version(r, kc, v.which[s]);
+            if (!v.D && v.ver[s]->n == 0) return;  // engine.cpp:76-78
         }
         Inter cur;
-        cur.n = ver[0]->n;
-        for (u32 j = 0; j < plan.sources[0].arity; ++j) cur.cols[ColRef{0, j}] = ver[0]->cols[j].get();
-        const bool src0_pending = plan.sources[0].constrained();
-
-        // Columns still needed after join step k.
+        cur.n = v.ver[0]->n;
+        for (u32 j = 0; j < plan.sources[0].arity; ++j) cur.cols[ColRef{0, j}] = v.ver[0]->cols[j].get();
         const size_t nj = plan.joins.size();
-        std::vector<std::set<ColRef>> needed(nj);
+        v.needed.resize(nj);
         for (size_t k = 0; k < nj; ++k) {
-            std::set<ColRef>& s = needed[k];
+            std::set<ColRef>& s = v.needed[k];
             for (size_t q = k + 1; q < nj; ++q) {
                 s.insert(plan.joins[q].left);
                 for (auto& r : plan.joins[q].residual_eq) s.insert(r.first);
             }
             for (auto& r : plan.output_cols) s.insert(r);
         }
-        const u32 W = (plan.head_arity + 1) / 2;
-
-        for (size_t k = 0; k < nj; ++k) {
-            const PlanJoin& jn = plan.joins[k];
-            const u32 R = jn.right_source;
-            RelState& rr = rel(plan.sources[R].relation);
-            const bool rpart = partitioned(rr);
-            if (D && dp.shuffle[k]) cur = shuffle(cur, jn.left);
-            std::unique_ptr<JoinIndex> tmp;
-            JoinIndex* idx;
-            if (plan.sources[R].constrained()) {
-                tmp = std::make_unique<JoinIndex>();
-                build_index_on(*ver[R], jn.right_col, *tmp, &plan.sources[R]);
-                idx = tmp.get();
-            } else {
-                idx = &index(rr, rpart ? jn.right_col : 0, which[R], jn.right_col);
-            }
-            if (!D && idx->rows->n == 0) return;
-            const u64 n = cur.n;
-            DBuf<u32> starts(c_, n), counts(c_, n);
-            RowFilter pred;
-            if (k == 0 && src0_pending) pred = source_filter(plan.sources[0], *ver[0]);
-            engine_probe_count(c_, cur.cols.at(jn.left), n, *idx, pred, starts.get(), counts.get());
-            DBuf<u64> offsets(c_, n + 1);
-            exclusive_scan_counts(c_, counts.get(), offsets.get(), n);
-            FV_CUDA(cudaMemcpyAsync(c_->pinned, offsets.get() + n, 8, cudaMemcpyDeviceToHost, c_->stream));
-            c_->sync();
-            const u64 T = c_->pinned[0];
-            counts.reset();
-            if (trace_)
-                std::fprintf(stderr, "[fvlog]   %s join %zu/%zu delta@%ld probe=%llu outputs=%llu\n", plan.head.c_str(), k,
-                             nj, delta_source, static_cast<unsigned long long>(n), static_cast<unsigned long long>(T));
-            if (!D && T == 0) return;
-
-            const bool last = k + 1 == nj;
-            auto slot_of = [&](const ColRef& r) -> SlotRef {
-                if (r.source == R) return SlotRef{idx->rows->cols[r.col].get(), 1};
-                auto it = cur.cols.find(r);
-                if (it == cur.cols.end()) fail(FV_ERR_PLAN, "plan references an unbound column");
-                return SlotRef{it->second, 0};
-            };
-            OutSpec spec;
-            spec.shift = st_.key_shift;
-            for (auto& [lref, rcol] : jn.residual_eq)
-                push(spec, Filter{slot_of(lref), SlotRef{idx->rows->cols[rcol].get(), 1}, kFilterEq, 0});
-            Inter next;
-            if (last) {
-                for (auto& [ga, gb] : plan.guard_neq)
-                    push(spec, Filter{slot_of(plan.output_cols[ga]), slot_of(plan.output_cols[gb]), kFilterNeq, 0});
-                if (D && dp.replicated_out) push(spec, owner_filter(slot_of(plan.output_cols[0])));
-                spec.key_mode = 1;
-                spec.n_out = plan.head_arity;
-                for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot_of(plan.output_cols[h]);
-                if (sink) {
-                    // Fused dedup: the join kernel inserts into FULL's key set.
-                    // Output chunks bound what the key set and the new-key
-                    // buffer must be sized for: each chunk may add at most its
-                    // own size, and the real count is re-read between chunks
-                    // (CSPA joins produce ~10^3 candidates per new row).
-                    RelState& hr = rel(plan.head);
-                    if (trace_) {
-                        spec.probe_count = c_->d_scalars + 24;
-                        FV_CUDA(cudaMemsetAsync(spec.probe_count, 0, 8, c_->stream));
-                    }
-                    // Partitioned: rows owned here are deduplicated in this
-                    // kernel, the others are pooled for the all-to-all.
-                    const bool route = D && !dp.replicated_out;
-                    if (route) {
-                        out.reserve(c_, T);
-                        spec.keys[0] = out.words[0].get() + out.n;
-                        spec.d_count = c_->d_scalars + 26;
-                        spec.remote_world = world_;
-                        spec.remote_rank = rank_;
-                        FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
-                    }
-                    for (u64 t0 = 0; t0 < T; t0 += kFusedChunk) {
-                        const u64 t1 = std::min(T, t0 + kFusedChunk);
-                        hash_reserve(hr, *sink, t1 - t0);
-                        spec.ht_slots = hr.keys.slots.get();
-                        spec.ht_mask = hr.keys.mask;
-                        spec.ht_group_bits = hr.keys.group_bits;
-                        spec.new_keys = sink->keys.get();
-                        spec.new_count = sink->counter.get();
-                        engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
-                    }
-                    sink->candidates += T;
-                    if (route) {
-                        u64 pooled = 0;
-                        c_->read_scalars(spec.d_count, &pooled, 1);
-                        out.n += pooled;
-                    }
-                    if (trace_) {
-                        u64 probes = 0;
-                        c_->read_scalars(spec.probe_count, &probes, 1);
-                        std::fprintf(stderr, "[fvlog]   fused dedup: %llu candidates -> %llu key-set probes\n",
-                                     static_cast<unsigned long long>(T), static_cast<unsigned long long>(probes));
-                    }
-                    return;
-                }
-                // One-word keys: drop tile-local repeats before they are
-                // pooled (and, partitioned, routed over NVLink).
-                if (W == 1) spec.tile_dedup = 1;
-                // Pooled candidates (no key set) are produced in chunks and
-                // the pool is sort-uniqued whenever the next chunk would
-                // push it past kPoolBudget rows (SURVEY.md §7 hard part 1:
-                // the reference materializes every candidate at once).
-                const bool compacts = spec.n_filters || spec.tile_dedup;
-                for (u64 t0 = 0; t0 < T; t0 += pool_chunk_) {
-                    const u64 t1 = std::min(T, t0 + pool_chunk_);
-                    if (out.n && out.n + (t1 - t0) > pool_budget_) compact_pool(out);
-                    out.reserve(c_, t1 - t0);
-                    // Positional (uncompacted) writes use absolute output
-                    // indices: bias the base so output t0 lands at out.n.
-                    for (u32 w = 0; w < W; ++w) spec.keys[w] = out.words[w].get() + out.n - (compacts ? 0 : t0);
-                    if (compacts) {
-                        spec.d_count = c_->d_scalars + 20;
-                        FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
-                    }
-                    engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
-                    u64 produced = t1 - t0;
-                    if (compacts) c_->read_scalars(spec.d_count, &produced, 1);
-                    out.n += produced;
-                }
-                return;
-            } else {
-                spec.key_mode = 0;
-                u32 j = 0;
-                for (const ColRef& r : needed[k]) {
-                    if (r.source > R) continue;
-                    if (j >= static_cast<u32>(kMaxSlots)) fail(FV_ERR_PLAN, "join intermediate wider than 16 columns");
-                    spec.col[j] = slot_of(r);
-                    next.owned.emplace_back(c_, T);
-                    spec.out_cols[j] = next.owned.back().get();
-                    next.cols[r] = spec.out_cols[j];
-                    ++j;
-                }
-                spec.n_out = j;
-            }
-            const bool compacts = spec.n_filters || spec.tile_dedup;
-            if (compacts) {
-                spec.d_count = c_->d_scalars + 20;
-                FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
-            }
-            engine_materialize(c_, offsets.get(), n, T, starts.get(), spec);
-            u64 produced = T;
-            if (compacts) c_->read_scalars(spec.d_count, &produced, 1);
-            next.n = produced;
-            u32 bound_cols = 0;
-            for (u32 s = 0; s <= R; ++s) bound_cols += plan.sources[s].arity;
-            if (spec.n_out < bound_cols) maybe_dedup_inter(next, std::make_tuple(&plan, k, delta_source));
-            cur = std::move(next);
-            if (!D && cur.n == 0) return;
+        if (nj) {
+            join_step(v, 0, std::move(cur));
+            return;
         }
         // No joins: a single-atom rule (copy / projection / selection).
+        const u32 W = v.W;
         OutSpec spec;
         spec.shift = st_.key_shift;
-        if (src0_pending) {
-            RowFilter f = source_filter(plan.sources[0], *ver[0]);
+        if (v.src0_pending) {
+            RowFilter f = source_filter(plan.sources[0], *v.ver[0]);
             for (u32 q = 0; q < f.n; ++q) push(spec, f.f[q]);
         }
-        auto slot0 = [&](const ColRef& r) { return SlotRef{ver[0]->cols[r.col].get(), 0}; };
+        auto slot0 = [&](const ColRef& r) { return SlotRef{v.ver[0]->cols[r.col].get(), 0}; };
         for (auto& [ga, gb] : plan.guard_neq)
             push(spec, Filter{slot0(plan.output_cols[ga]), slot0(plan.output_cols[gb]), kFilterNeq, 0});
-        if (D && dp.replicated_out) push(spec, owner_filter(slot0(plan.output_cols[0])));
+        if (v.D && dp.replicated_out) push(spec, owner_filter(slot0(plan.output_cols[0])));
         spec.key_mode = 1;
         spec.n_out = plan.head_arity;
         for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot0(plan.output_cols[h]);
@@ -616,6 +482,179 @@ public:
         u64 produced = cur.n;
         if (spec.n_filters) c_->read_scalars(spec.d_count, &produced, 1);
         out.n += produced;
+    }
+
+    // Join step k of a variant on intermediate `cur`; recurses into step k+1.
+    // An intermediate larger than inter_chunk_ rows is produced and carried
+    // through the rest of the chain chunk by chunk (single GPU: every rank of
+    // a partitioned run must issue the same collectives, so it stays whole
+    // there), so memory stays O(chunk x depth + output).
+    void join_step(VarRun& v, size_t k, Inter cur) {
+        const Plan& plan = v.plan;
+        const DistPlan& dp = v.dp;
+        const bool D = v.D;
+        const u32 W = v.W;
+        CandPool& out = v.out;
+        HeadSink* sink = v.sink;
+        const long delta_source = v.delta_source;
+        const size_t nj = plan.joins.size();
+        const PlanJoin& jn = plan.joins[k];
+        const u32 R = jn.right_source;
+        RelState& rr = rel(plan.sources[R].relation);
+        const bool rpart = partitioned(rr);
+        if (D && dp.shuffle[k]) cur = shuffle(cur, jn.left);
+        std::unique_ptr<JoinIndex> tmp;
+        JoinIndex* idx;
+        if (plan.sources[R].constrained()) {
+            tmp = std::make_unique<JoinIndex>();
+            build_index_on(*v.ver[R], jn.right_col, *tmp, &plan.sources[R]);
+            idx = tmp.get();
+        } else {
+            idx = &index(rr, rpart ? jn.right_col : 0, v.which[R], jn.right_col);
+        }
+        if (!D && idx->rows->n == 0) return;
+        const u64 n = cur.n;
+        DBuf<u32> starts(c_, n), counts(c_, n);
+        RowFilter pred;
+        if (k == 0 && v.src0_pending) pred = source_filter(plan.sources[0], *v.ver[0]);
+        engine_probe_count(c_, cur.cols.at(jn.left), n, *idx, pred, starts.get(), counts.get());
+        DBuf<u64> offsets(c_, n + 1);
+        exclusive_scan_counts(c_, counts.get(), offsets.get(), n);
+        FV_CUDA(cudaMemcpyAsync(c_->pinned, offsets.get() + n, 8, cudaMemcpyDeviceToHost, c_->stream));
+        c_->sync();
+        const u64 T = c_->pinned[0];
+        counts.reset();
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   %s join %zu/%zu delta@%ld probe=%llu outputs=%llu\n", plan.head.c_str(), k, nj,
+                         delta_source, static_cast<unsigned long long>(n), static_cast<unsigned long long>(T));
+        if (!D && T == 0) return;
+
+        const bool last = k + 1 == nj;
+        auto slot_of = [&](const ColRef& r) -> SlotRef {
+            if (r.source == R) return SlotRef{idx->rows->cols[r.col].get(), 1};
+            auto it = cur.cols.find(r);
+            if (it == cur.cols.end()) fail(FV_ERR_PLAN, "plan references an unbound column");
+            return SlotRef{it->second, 0};
+        };
+        OutSpec spec;
+        spec.shift = st_.key_shift;
+        for (auto& [lref, rcol] : jn.residual_eq)
+            push(spec, Filter{slot_of(lref), SlotRef{idx->rows->cols[rcol].get(), 1}, kFilterEq, 0});
+        if (last) {
+            for (auto& [ga, gb] : plan.guard_neq)
+                push(spec, Filter{slot_of(plan.output_cols[ga]), slot_of(plan.output_cols[gb]), kFilterNeq, 0});
+            if (D && dp.replicated_out) push(spec, owner_filter(slot_of(plan.output_cols[0])));
+            spec.key_mode = 1;
+            spec.n_out = plan.head_arity;
+            for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot_of(plan.output_cols[h]);
+            if (sink) {
+                // Fused dedup: the join kernel inserts into FULL's key set.
+                // Output chunks bound what the key set and the new-key
+                // buffer must be sized for: each chunk may add at most its
+                // own size, and the real count is re-read between chunks
+                // (CSPA joins produce ~10^3 candidates per new row).
+                RelState& hr = rel(plan.head);
+                if (trace_) {
+                    spec.probe_count = c_->d_scalars + 24;
+                    FV_CUDA(cudaMemsetAsync(spec.probe_count, 0, 8, c_->stream));
+                }
+                // Partitioned: rows owned here are deduplicated in this
+                // kernel, the others are pooled for the all-to-all.
+                const bool route = D && !dp.replicated_out;
+                if (route) {
+                    out.reserve(c_, T);
+                    spec.keys[0] = out.words[0].get() + out.n;
+                    spec.d_count = c_->d_scalars + 26;
+                    spec.remote_world = world_;
+                    spec.remote_rank = rank_;
+                    FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
+                }
+                for (u64 t0 = 0; t0 < T; t0 += kFusedChunk) {
+                    const u64 t1 = std::min(T, t0 + kFusedChunk);
+                    hash_reserve(hr, *sink, t1 - t0);
+                    spec.ht_slots = hr.keys.slots.get();
+                    spec.ht_mask = hr.keys.mask;
+                    spec.ht_group_bits = hr.keys.group_bits;
+                    spec.new_keys = sink->keys.get();
+                    spec.new_count = sink->counter.get();
+                    engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
+                }
+                sink->candidates += T;
+                if (route) {
+                    u64 pooled = 0;
+                    c_->read_scalars(spec.d_count, &pooled, 1);
+                    out.n += pooled;
+                }
+                if (trace_) {
+                    u64 probes = 0;
+                    c_->read_scalars(spec.probe_count, &probes, 1);
+                    std::fprintf(stderr, "[fvlog]   fused dedup: %llu candidates -> %llu key-set probes\n",
+                                 static_cast<unsigned long long>(T), static_cast<unsigned long long>(probes));
+                }
+                return;
+            }
+            // One-word keys: drop tile-local repeats before they are
+            // pooled (and, partitioned, routed over NVLink).
+            if (W == 1) spec.tile_dedup = 1;
+            // Pooled candidates (no key set) are produced in chunks and
+            // the pool is sort-uniqued whenever the next chunk would
+            // push it past kPoolBudget rows (SURVEY.md §7 hard part 1:
+            // the reference materializes every candidate at once).
+            const bool compacts = spec.n_filters || spec.tile_dedup;
+            for (u64 t0 = 0; t0 < T; t0 += pool_chunk_) {
+                const u64 t1 = std::min(T, t0 + pool_chunk_);
+                if (out.n && out.n + (t1 - t0) > pool_budget_) compact_pool(out);
+                out.reserve(c_, t1 - t0);
+                // Positional (uncompacted) writes use absolute output
+                // indices: bias the base so output t0 lands at out.n.
+                for (u32 w = 0; w < W; ++w) spec.keys[w] = out.words[w].get() + out.n - (compacts ? 0 : t0);
+                if (compacts) {
+                    spec.d_count = c_->d_scalars + 20;
+                    FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
+                }
+                engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
+                u64 produced = t1 - t0;
+                if (compacts) c_->read_scalars(spec.d_count, &produced, 1);
+                out.n += produced;
+            }
+            return;
+        }
+        // Intermediate: the columns later steps and the head still need.
+        std::vector<ColRef> refs;
+        for (const ColRef& r : v.needed[k]) {
+            if (r.source > R) continue;
+            if (refs.size() >= static_cast<size_t>(kMaxSlots)) fail(FV_ERR_PLAN, "join intermediate wider than 16 columns");
+            refs.push_back(r);
+        }
+        spec.key_mode = 0;
+        spec.n_out = static_cast<u32>(refs.size());
+        for (u32 j = 0; j < spec.n_out; ++j) spec.col[j] = slot_of(refs[j]);
+        const bool compacts = spec.n_filters != 0;
+        u32 bound_cols = 0;
+        for (u32 s = 0; s <= R; ++s) bound_cols += plan.sources[s].arity;
+        const u64 chunk = D ? T : std::max<u64>(inter_chunk_, 1);
+        for (u64 t0 = 0; t0 < std::max<u64>(T, 1); t0 += chunk) {
+            const u64 t1 = std::min(T, t0 + chunk);
+            Inter next;
+            for (u32 j = 0; j < spec.n_out; ++j) {
+                next.owned.emplace_back(c_, t1 - t0);
+                // positional writes use absolute output indices (see above)
+                spec.out_cols[j] = next.owned.back().get() - (compacts ? 0 : t0);
+                next.cols[refs[j]] = next.owned.back().get();
+            }
+            if (compacts) {
+                spec.d_count = c_->d_scalars + 20;
+                FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
+            }
+            engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
+            u64 produced = t1 - t0;
+            if (compacts) c_->read_scalars(spec.d_count, &produced, 1);
+            next.n = produced;
+            if (spec.n_out < bound_cols) maybe_dedup_inter(next, std::make_tuple(&plan, k, delta_source));
+            if (!D && next.n == 0) continue;
+            join_step(v, k + 1, std::move(next));
+            if (T == 0) break;
+        }
     }
 
     // Distinct rows of a join intermediate that dropped columns. The join
@@ -999,6 +1038,7 @@ private:
         return e && std::atoll(e) > 0 ? static_cast<u64>(std::atoll(e)) : dflt;
     }
     const u64 pool_chunk_ = env_rows("FVLOG_POOL_CHUNK", kPoolChunk);
+    const u64 inter_chunk_ = env_rows("FVLOG_INTER_CHUNK", kInterChunk);
     const u64 pool_budget_ = env_rows("FVLOG_POOL_BUDGET", kPoolBudget);
     const double group_ratio_ = [] {
         const char* e = std::getenv("FVLOG_GROUP_RATIO");
