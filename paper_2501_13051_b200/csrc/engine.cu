@@ -575,6 +575,8 @@ public:
                     spec.ht_slots = hr.keys.slots.get();
                     spec.ht_mask = hr.keys.mask;
                     spec.ht_group_bits = hr.keys.group_bits;
+                    // grouped layout <=> last iteration's candidates were all new
+                    spec.tile_set = hr.keys.group_bits == 0 ? 1u : 0u;
                     spec.new_keys = sink->keys.get();
                     spec.new_count = sink->counter.get();
                     engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);

@@ -321,7 +321,7 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
         for (int k = 0; k < kMatItems; ++k) {
             if (!((keep_mask >> k) & 1u)) continue;
             u32 h = static_cast<u32>(hs[k] >> 40) & (kMatSetSlots - 1);
-            for (int probe = 0; probe < kMatSetProbes; ++probe) {
+            for (int probe = 0; probe < (spec.tile_set ? kMatSetProbes : 0); ++probe) {
                 const unsigned long long prev = atomicCAS(s_set + h, ~0ull, static_cast<unsigned long long>(key[k]));
                 if (prev == ~0ull) break;                 // first in the tile
                 if (prev == key[k]) {                     // repeat: drop
