@@ -231,6 +231,28 @@ __global__ void runs_intersect_kernel(RunsArgs args, u32 arity, u64 n, u8* __res
     }
 }
 
+// Rows of arity <= 2 as one u64 key: (c0 << bits) | c1 (bits = value width).
+__global__ void pack_rows_kernel(const u32* __restrict__ c0, const u32* __restrict__ c1, u64 n, u32 bits,
+                                 u64* __restrict__ keys) {
+    GRID_STRIDE(i, n) keys[i] = c1 ? (static_cast<u64>(c0[i]) << bits) | c1[i] : c0[i];
+}
+
+// flags[i] = NEW row i occurs in FULL: binary search of its packed key in the
+// sorted FULL keys.
+__global__ void member_kernel(const u32* __restrict__ c0, const u32* __restrict__ c1, u64 n, u32 bits,
+                              const u64* __restrict__ full_keys, u64 n_full, u8* __restrict__ flags) {
+    GRID_STRIDE(i, n) {
+        const u64 key = c1 ? (static_cast<u64>(c0[i]) << bits) | c1[i] : c0[i];
+        u64 lo = 0, hi = n_full;
+        while (lo < hi) {
+            const u64 mid = (lo + hi) >> 1;
+            if (full_keys[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        flags[i] = (lo < n_full && full_keys[lo] == key) ? 1 : 0;
+    }
+}
+
 __device__ __forceinline__ u64 upper_bound_u64(const u64* __restrict__ a, u64 len, u64 x) {
     u64 lo = 0, hi = len;
     while (lo < hi) {
@@ -415,6 +437,7 @@ std::unique_ptr<Version> version_from_device(Ctx* c, std::vector<DBuf<u32>>&& co
 void column_probe_device(Ctx* c, const Column& col, const u32* values, u64 n, u32* starts,
                          u32* counts) {
     if (!n) return;
+    ProfScope prof(c, "column_probe", double(n) * 12.0);
     probe_kernel<<<grid_for(n), 256, 0, c->stream>>>(col.ht.slots.get(), col.ht.mask,
                                                       col.ustart.get(), col.ucount.get(), values, n,
                                                       starts, counts);
@@ -479,6 +502,8 @@ void join_write_phase(Ctx* c, const Match& m, const u64* offsets, u64 total, con
                       DBuf<u32>& a, DBuf<u32>& b) {
     a = DBuf<u32>(c, total);
     b = DBuf<u32>(c, total);
+    // Per output: its sorted_idx entry read and the id pair written.
+    ProfScope prof(c, "join_write_phase", double(m.m) * 16.0 + double(total) * 12.0);
     lbs_launch(c, offsets, m.m, total,
                JoinWriteOp{m.starts.get(), m.matched.get(), build.sorted_idx.get(), a.get(), b.get()});
 }
@@ -594,6 +619,36 @@ DBuf<u8> deduplicate(Ctx* c, const Version& nv, const Version& full) {
     if (n == 0) return flags;
     if (full.rows == 0) {
         FV_CUDA(cudaMemsetAsync(flags.get(), 0, n, c->stream));
+        return flags;
+    }
+    if (nv.arity <= 2) {
+        // Same flags as Algorithm 2 (a NEW row is marked iff it occurs in
+        // FULL), computed as membership of packed row keys in FULL's sorted
+        // keys instead of intersecting per-column id runs (runs of hot
+        // values are thousands of ids long): one radix sort of FULL + one
+        // binary search per NEW row.
+        u64* dmax = c->d_scalars + 12;
+        FV_CUDA(cudaMemsetAsync(dmax, 0, sizeof(u64), c->stream));
+        for (u32 j = 0; j < nv.arity; ++j) {
+            reduce_max_u32(c, nv.cols[j]->raw.get(), n, dmax, true);
+            reduce_max_u32(c, full.cols[j]->raw.get(), full.rows, dmax, true);
+        }
+        u64 vmax = 0;
+        c->read_scalars(dmax, &vmax, 1);
+        const u32 bits = std::max<u32>(1, bit_width_u64(vmax));
+        const u32* f1 = nv.arity == 2 ? full.cols[1]->raw.get() : nullptr;
+        const u32* n1 = nv.arity == 2 ? nv.cols[1]->raw.get() : nullptr;
+        DBuf<u64> keys(c, full.rows), alt(c, full.rows);
+        ProfScope prof(c, "deduplicate", double(full.rows) * (4.0 * nv.arity + 8.0) + double(n) * (4.0 * nv.arity + 1.0));
+        pack_rows_kernel<<<grid_for(full.rows), 256, 0, c->stream>>>(full.cols[0]->raw.get(), f1, full.rows, bits,
+                                                                     keys.get());
+        FV_CUDA(cudaGetLastError());
+        if (radix_sort_keys_u64(c, keys.get(), alt.get(), full.rows, 0, nv.arity == 2 ? 2 * bits : bits))
+            keys.swap(alt);
+        member_kernel<<<grid_for(n), 256, 0, c->stream>>>(nv.cols[0]->raw.get(), n1, n, bits, keys.get(), full.rows,
+                                                          flags.get());
+        FV_CUDA(cudaGetLastError());
+        c->count_launch(2);
         return flags;
     }
     // One probe loop per column, as in the reference (kernels.cpp:220-233).
