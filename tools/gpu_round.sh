@@ -26,6 +26,11 @@ if [ -z "${SKIP_BENCH:-}" ]; then
   echo "bench exit $?" >> "$OUT/bench.err"
 fi
 
+if [ -z "${SKIP_OPS:-}" ]; then
+  timeout 1200 python tools/bench_ops.py --out "$OUT/ops.json" > "$OUT/ops.log" 2>&1
+  timeout 900 python tools/bench_io.py --out "$OUT/io.json" > "$OUT/io.log" 2>&1
+fi
+
 if [ -z "${SKIP_WORKLOADS:-}" ]; then
   timeout 1500 python tools/bench_workloads.py --out "$OUT/workloads.json" > "$OUT/workloads.log" 2>&1
   echo "workloads exit $?" >> "$OUT/workloads.log"

@@ -90,7 +90,8 @@ def main(src, dst):
             cap = full_capture(os.path.join(src, f))
             if cap:
                 json.dump(cap, open(os.path.join(dst, f.replace(".ncu-rep", ".json")), "w"), indent=1)
-    for f in ("bench.json", "membench.json", "workloads.json", "pytest_gpu.log", "smoke.log", "nproc.txt", "lscpu.txt"):
+    for f in ("bench.json", "membench.json", "workloads.json", "ops.json", "io.json", "sortbench.json",
+              "pytest_gpu.log", "smoke.log", "nproc.txt", "lscpu.txt"):
         if os.path.exists(os.path.join(src, f)):
             shutil.copy(os.path.join(src, f), os.path.join(dst, f))
     summary = {"round_dir": dst, "kernels": {}}
