@@ -8,6 +8,8 @@ same files.
                    i.e. the same work; process_s is the whole process, which
                    also pays CUDA context creation and teardown (~2 s, fixed).
 
+Each side: one warm-up run, then the median of 3 runs.
+
     python tools/bench_io.py [--out f.json]
 """
 import argparse
@@ -68,7 +70,9 @@ def main():
             for label, binary in (("fvlog", CLI), ("reference", REF)):
                 out = os.path.join(d, label)
                 run(binary, prog, facts, out, dump)  # warm (page cache, driver)
-                wall, evaluate_s, phases = run(binary, prog, facts, out, dump)
+                # median of 3 process runs (by wall time)
+                wall, evaluate_s, phases = sorted((run(binary, prog, facts, out, dump) for _ in range(3)),
+                                                  key=lambda r: r[0])[1]
                 if label == "fvlog":
                     io = sum(v for k, v in phases.items() if k in ("parse", "load facts", "dump"))
                     row[label] = {"process_s": round(wall, 3), "evaluate_s": round(evaluate_s, 4),
