@@ -835,19 +835,30 @@ __global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __r
 // per value (shared-nothing L2 atomics on a small counter array), scan, and
 // scatter each key to base[value] + atomicAdd(cursor[value]) — two reads and
 // one write of the keys instead of a histogram plus three onesweep passes.
-// Warps whose 32 keys share one value (DELTA arrives in probe-row order, so
-// hub rows are contiguous) take one atomic for all of them.
+// DELTA arrives in probe-row order, so a value's keys come in short runs
+// (interleaved by the join's per-warp appends): every warp aggregates equal
+// values with __match_any_sync and takes one atomic per distinct value, the
+// group's lanes writing consecutive slots. Warps whose 32 keys share one
+// value skip the match.
+#ifndef FV_GROUP_MATCH
+#define FV_GROUP_MATCH 1
+#endif
 
 __global__ void group_count_kernel(const u64* __restrict__ keys, u64 n, u32 shift, u32* __restrict__ cnt) {
     const u64 n_round = ceil_div(n, 32) * 32;
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n_round; i += u64(gridDim.x) * blockDim.x) {
         const bool valid = i < n;
-        const u32 g = valid ? static_cast<u32>(keys[i] >> shift) : 0u;
+        const u32 g = valid ? static_cast<u32>(keys[i] >> shift) : ~0u;
         const u32 g0 = __shfl_sync(0xffffffffu, g, 0);
-        if (__all_sync(0xffffffffu, valid && g == g0)) {
-            if (lane_id() == 0) atomicAdd(cnt + g0, 32u);
-        } else if (valid) {
-            atomicAdd(cnt + g, 1u);
+        if (__all_sync(0xffffffffu, g == g0)) {
+            if (lane_id() == 0 && valid) atomicAdd(cnt + g0, 32u);
+        } else {
+#if FV_GROUP_MATCH
+            const u32 peers = __match_any_sync(0xffffffffu, g);
+            if (valid && lane_id() == __ffs(peers) - 1) atomicAdd(cnt + g, static_cast<u32>(__popc(peers)));
+#else
+            if (valid) atomicAdd(cnt + g, 1u);
+#endif
         }
     }
 }
@@ -860,15 +871,24 @@ __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 sh
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n_round; i += u64(gridDim.x) * blockDim.x) {
         const bool valid = i < n;
         const u64 key = valid ? keys[i] : 0;
-        const u32 g = static_cast<u32>(key >> shift);
+        const u32 g = valid ? static_cast<u32>(key >> shift) : ~0u;
         const u32 g0 = __shfl_sync(0xffffffffu, g, 0);
         u64 pos;
-        if (__all_sync(0xffffffffu, valid && g == g0)) {
+        if (__all_sync(0xffffffffu, g == g0)) {
             u32 b = 0;
-            if (lane == 0) b = atomicAdd(cursor + g0, 32u);
-            pos = base[g0] + __shfl_sync(0xffffffffu, b, 0) + lane;
+            if (lane == 0 && valid) b = atomicAdd(cursor + g0, 32u);
+            pos = valid ? base[g0] + __shfl_sync(0xffffffffu, b, 0) + lane : 0;
         } else {
+#if FV_GROUP_MATCH
+            const u32 peers = __match_any_sync(0xffffffffu, g);
+            const u32 leader = __ffs(peers) - 1;
+            u32 b = 0;
+            if (valid && lane == leader) b = atomicAdd(cursor + g, static_cast<u32>(__popc(peers)));
+            b = __shfl_sync(0xffffffffu, b, leader);
+            pos = valid ? base[g] + b + __popc(peers & ((1u << lane) - 1)) : 0;
+#else
             pos = valid ? base[g] + atomicAdd(cursor + g, 1u) : 0;
+#endif
         }
         if (valid) {
             if (c0) {  // unpacked straight into SoA columns
