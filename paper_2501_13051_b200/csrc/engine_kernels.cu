@@ -139,6 +139,30 @@ __device__ __forceinline__ void append_new(u64* __restrict__ out, u64* counter, 
     if (is_new) out[base + __popc(m & lanemask_lt())] = key;
 }
 
+// Warp-aggregated append of every item flagged in `mask` (bit k: key[k] is
+// new) with ONE counter atomic per warp for all items: the counter is a single
+// global word that every warp of the grid hits, so its atomic rate, not the
+// key set, caps the join when each item takes its own atomic.
+template <int N>
+__device__ __forceinline__ void append_new_items(u64* __restrict__ out, u64* counter, u32 mask, const u64 (&key)[N]) {
+    const u32 lane = lane_id();
+    const u32 cnt = __popc(mask);
+    u32 incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<u32>(o)) incl += y;
+    }
+    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+    if (!total) return;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(reinterpret_cast<unsigned long long*>(counter), static_cast<unsigned long long>(total));
+    u64 pos = __shfl_sync(0xffffffffu, base, 31) + (incl - cnt);
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+        if ((mask >> k) & 1u) out[pos++] = key[k];
+}
+
 // Write one output row (values computed from slots) at position pos.
 __device__ __forceinline__ void write_row(const OutSpec& spec, u64 pos, u64 i, u64 p) {
     if (spec.key_mode) {
@@ -178,6 +202,12 @@ constexpr int kMatSparseSpan = 8 * kMatTile;
 #define FV_MAT_SET_SLOTS (2 * kMatTile)
 #endif
 constexpr int kMatSetSlots = FV_MAT_SET_SLOTS;  // tile-local set; load <= 1/2 at the default size
+#ifndef FV_MAT_APPEND_CTA
+#define FV_MAT_APPEND_CTA 0
+#endif
+#ifndef FV_MAT_BATCH_CAS
+#define FV_MAT_BATCH_CAS 1
+#endif
 constexpr int kMatSetProbes = 16;               // bounded: an unplaced key is simply probed globally
 
 __device__ __forceinline__ u64 upper_bound_u64(const u64* __restrict__ a, u64 len, u64 x) {
@@ -276,8 +306,9 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
         }
         if (lane == 31) s_warp[warp] = x;
         __syncthreads();
-        u32 carry = 0;
-        for (u32 w = 0; w < warp; ++w) carry = max(carry, s_warp[w]);
+        // carry-in = max over the earlier warps: one shared read per lane
+        // and a warp max-reduction instead of a serial loop over them.
+        u32 carry = __reduce_max_sync(0xffffffffu, lane < warp ? s_warp[lane] : 0u);
         const u32 prev = __shfl_up_sync(0xffffffffu, x, 1);
         if (lane > 0) carry = max(carry, prev);
 #pragma unroll
@@ -339,17 +370,17 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
         if (REMOTE) {
             // Rows owned by another rank go to the routing pool (one
             // warp-aggregated append each) instead of the local key set.
+            u32 remote_mask = 0;
 #pragma unroll
             for (int k = 0; k < kMatItems; ++k) {
-                bool remote = false;
                 if ((keep_mask >> k) & 1u) {
                     const u32 c0 = static_cast<u32>(spec.n_out >= 2 ? key[k] >> spec.shift : key[k]);
-                    remote = static_cast<u32>((static_cast<u64>(hash32(c0)) * spec.remote_world) >> 32) !=
-                             spec.remote_rank;
+                    if (static_cast<u32>((static_cast<u64>(hash32(c0)) * spec.remote_world) >> 32) != spec.remote_rank)
+                        remote_mask |= 1u << k;
                 }
-                append_new(spec.keys[0], spec.d_count, remote, key[k]);
-                if (remote) keep_mask &= ~(1u << k);
             }
+            append_new_items(spec.keys[0], spec.d_count, remote_mask, key);
+            keep_mask &= ~remote_mask;
         }
         if (spec.probe_count) {
             const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
@@ -373,12 +404,56 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
         }
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) sv[k] = ((keep_mask >> k) & 1u) ? __ldcg(spec.ht_slots + hs[k]) : 0;
+#if FV_MAT_BATCH_CAS
+        // Every claim of an empty first slot is issued before any result is
+        // read (the CASes are as independent as the loads); collisions with
+        // another key fall back to the probe loop.
+        u32 new_mask = 0, slow_mask = 0;
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k) {
+            if (!((keep_mask >> k) & 1u) || sv[k] == key[k]) {
+                keep_mask &= ~(1u << k);
+            } else if (sv[k] == kEmptySlot) {
+                sv[k] = atomicCAS(reinterpret_cast<unsigned long long*>(spec.ht_slots + hs[k]), ~0ull,
+                                  static_cast<unsigned long long>(key[k]));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k) {
+            if (!((keep_mask >> k) & 1u)) continue;
+            if (sv[k] == kEmptySlot) new_mask |= 1u << k;          // claimed
+            else if (sv[k] != key[k]) slow_mask |= 1u << k;        // another key there
+        }
+#pragma unroll
+        for (int k = 0; k < kMatItems; ++k)
+            if (((slow_mask >> k) & 1u) &&
+                keyset_insert_probe_from(spec.ht_slots, spec.ht_mask, key[k], (hs[k] + 1) & spec.ht_mask))
+                new_mask |= 1u << k;
+#if FV_MAT_APPEND_CTA
+        {
+            u32 tot;
+            const u32 excl = block_excl_u32(__popc(new_mask), s_warp, &tot);
+            if (tid == 0)
+                s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(spec.new_count),
+                                         static_cast<unsigned long long>(tot))
+                             : 0;
+            __syncthreads();
+            u64 pos = s_base + excl;
+#pragma unroll
+            for (int k = 0; k < kMatItems; ++k)
+                if ((new_mask >> k) & 1u) spec.new_keys[pos++] = key[k];
+        }
+#else
+        append_new_items(spec.new_keys, spec.new_count, new_mask, key);
+#endif
+#else
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) {
             const bool keep = (keep_mask >> k) & 1u;
             const bool is_new = keep && keyset_insert_from(spec.ht_slots, spec.ht_mask, key[k], hs[k], sv[k]);
             append_new(spec.new_keys, spec.new_count, is_new, key[k]);
         }
+#endif
         return;
     }
     if (!COMPACT) {
