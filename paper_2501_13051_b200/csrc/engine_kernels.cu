@@ -852,16 +852,18 @@ __global__ void fingerprint_kernel(Cols8 c, u32 arity, u64 n, unsigned long long
 namespace {
 
 #ifndef FV_INSERT_ITEMS
-#define FV_INSERT_ITEMS 1
+#define FV_INSERT_ITEMS 4
 #endif
 #ifdef FV_INSERT_MINB
 #define FV_INSERT_BOUNDS __launch_bounds__(256, FV_INSERT_MINB)
 #else
 #define FV_INSERT_BOUNDS
 #endif
-// One key per thread: the probe is a latency-bound random load, and 20
-// registers give full occupancy (the partitioned C2 insert: 167.6 ms at 8
-// keys/thread and 64 registers, 119 ms at 2, 97 ms at 1).
+// Four keys per thread. With one counter atomic and one CAS round trip per
+// item, one key per thread was best (partitioned C2: 167.6 ms at 8, 97 at 1);
+// with the claims batched and one append atomic per warp for all items, more
+// items keep more independent loads in flight (8-rank C2 on one GPU, all
+// ranks' inserts under ncu: 113 ms at 1 key/thread, 96 at 2, 76 at 4, 74 at 8).
 constexpr int kInsertItems = FV_INSERT_ITEMS;
 __global__ void FV_INSERT_BOUNDS hash_insert_keys_kernel(const u64* __restrict__ keys, u64 n,
                                                          u64* __restrict__ slots, u64 mask, u32 bits,
@@ -877,12 +879,31 @@ __global__ void FV_INSERT_BOUNDS hash_insert_keys_kernel(const u64* __restrict__
     }
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) sv[k] = (base + u64(k) * blockDim.x < n) ? __ldcg(slots + hs[k]) : 0;
+    // As in the fused join: claims of empty first slots issued together,
+    // collisions through the probe loop, one counter atomic per warp.
+    u32 new_mask = 0, slow_mask = 0, cas_mask = 0;
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
-        const bool valid = base + u64(k) * blockDim.x < n;
-        const bool is_new = valid && keyset_insert_from(slots, mask, key[k], hs[k], sv[k]);
-        if (new_keys) append_new(new_keys, new_count, is_new, key[k]);
+        if (base + u64(k) * blockDim.x >= n || sv[k] == key[k]) continue;
+        if (sv[k] == kEmptySlot) {
+            sv[k] = atomicCAS(reinterpret_cast<unsigned long long*>(slots + hs[k]), ~0ull,
+                              static_cast<unsigned long long>(key[k]));
+            cas_mask |= 1u << k;
+        } else {
+            slow_mask |= 1u << k;
+        }
     }
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        if (!((cas_mask >> k) & 1u)) continue;
+        if (sv[k] == kEmptySlot) new_mask |= 1u << k;
+        else if (sv[k] != key[k]) slow_mask |= 1u << k;
+    }
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k)
+        if (((slow_mask >> k) & 1u) && keyset_insert_probe_from(slots, mask, key[k], (hs[k] + 1) & mask))
+            new_mask |= 1u << k;
+    if (new_keys) append_new_items(new_keys, new_count, new_mask, key);
 }
 
 // One tile of consecutive old slots per block (not grid-stride): blocks run
