@@ -914,11 +914,15 @@ public:
         ns.mask = cap - 1;
         ns.count = r.keys.count;
         ns.group_bits = r.keys.capacity() ? r.keys.group_bits : initial_group_bits();
-        FV_CUDA(cudaMemsetAsync(ns.slots.get(), 0xff, 8 * cap, c_->stream));
         // The old table holds FULL's keys and the ones found new so far this
         // iteration (a relation's keys only ever enter through its table):
-        // move them all in one streaming pass over its slots.
-        if (r.keys.capacity()) engine_hash_rehash(c_, r.keys, ns);
+        // move them all in one streaming pass over its slots — windowed in
+        // shared memory when the layout is unchanged (every new slot written
+        // once, no memset), else memset + atomic rehash.
+        if (!(grow_windowed_ && engine_hash_grow(c_, r.keys, ns))) {
+            FV_CUDA(cudaMemsetAsync(ns.slots.get(), 0xff, 8 * cap, c_->stream));
+            if (r.keys.capacity()) engine_hash_rehash(c_, r.keys, ns);
+        }
         r.keys = std::move(ns);
     }
 
@@ -1049,6 +1053,11 @@ private:
     const int forced_group_ = [] {
         const char* e = std::getenv("FVLOG_KEYSET_GROUP");
         return e ? std::atoi(e) : -1;
+    }();
+    // FVLOG_GROW=rehash: key-set growth by memset + atomic rehash only.
+    const bool grow_windowed_ = [] {
+        const char* e = std::getenv("FVLOG_GROW");
+        return !(e && std::string(e) == "rehash");
     }();
     u32 world_ = 1, rank_ = 0;
 };

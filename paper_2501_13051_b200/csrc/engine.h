@@ -275,6 +275,10 @@ void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_ke
 // landing at random; a layout change (group_bits) re-scatters them
 // (to.count is not touched).
 void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to);
+// Growth by a power-of-two factor with the same layout bits: writes every
+// slot of `to` (no memset needed) from `from`'s keys. False when it does not
+// apply or its overflow list filled up; `to` must then be reset and rehashed.
+bool engine_hash_grow(Ctx* c, const KeySet& from, KeySet& to);
 // Distinct rows of lexicographically sorted packed keys -> SoA columns
 // (arity <= FV_MAX_ARITY); returns the distinct count.
 u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift,

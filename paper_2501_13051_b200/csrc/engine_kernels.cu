@@ -924,6 +924,85 @@ __global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __r
             keyset_insert_probe_from(to, mask, key[k], keyset_home(keyset_line_hash(key[k], bits), key[k], bits, mask));
 }
 
+// Growth without a memset or global atomics. With the new capacity F times
+// the old (same layout bits), a key's new home is its old home + j * old
+// capacity for some j < F, so the keys of one tile of old slots [a, a + T)
+// land in the F windows [a + j * old, a + j * old + T), which partition the
+// new table. A block builds each of its windows in shared memory (linear
+// probing with shared atomics) and streams it out whole, empty slots
+// included. Keys that cannot be placed inside their window — their home lies
+// in an earlier tile (displaced across the tile boundary) or their probe run
+// reaches the window's end — go to an overflow list that a plain insert
+// places afterwards, when every slot has been written.
+constexpr int kGrowItems = 8;
+constexpr int kGrowBlock = 256;
+constexpr u32 kGrowTile = kGrowItems * kGrowBlock;
+__global__ void __launch_bounds__(kGrowBlock) hash_grow_kernel(const u64* __restrict__ from, u64 old_cap,
+                                                               u32 log_old, u32 factor, u64* __restrict__ to,
+                                                               u64 new_mask, u32 bits, u64* __restrict__ overflow,
+                                                               u64 overflow_cap, u64* overflow_count) {
+    __shared__ unsigned long long win[kGrowTile];
+    const u64 a = u64(blockIdx.x) * kGrowTile;
+    u64 key[kGrowItems];
+    u32 local[kGrowItems];
+    u32 jj[kGrowItems];
+    u32 spill = 0;  // bit k: key k goes to the overflow list
+#pragma unroll
+    for (int k = 0; k < kGrowItems; ++k) {
+        const u64 i = a + u64(k) * kGrowBlock + threadIdx.x;
+        key[k] = i < old_cap ? __ldcs(from + i) : kEmptySlot;
+        local[k] = 0;
+        jj[k] = 0;
+        if (key[k] == kEmptySlot) continue;
+        const u64 h = keyset_home(keyset_line_hash(key[k], bits), key[k], bits, new_mask);
+        const u64 lo = h & (old_cap - 1);
+        jj[k] = static_cast<u32>(h >> log_old);
+        if (lo < a || lo >= a + kGrowTile) spill |= 1u << k;
+        else local[k] = static_cast<u32>(lo - a);
+    }
+    for (u32 j = 0; j < factor; ++j) {
+        for (u32 i = threadIdx.x; i < kGrowTile; i += kGrowBlock) win[i] = ~0ull;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kGrowItems; ++k) {
+            if (key[k] == kEmptySlot || jj[k] != j || ((spill >> k) & 1u)) continue;
+            u32 q = local[k];
+            while (true) {
+                if (atomicCAS(win + q, ~0ull, static_cast<unsigned long long>(key[k])) == ~0ull) break;
+                if (++q == kGrowTile) {  // run leaves the window
+                    spill |= 1u << k;
+                    break;
+                }
+            }
+        }
+        __syncthreads();
+        const u64 w0 = a + (u64(j) << log_old);
+        for (u32 i = threadIdx.x; i < kGrowTile && a + i < old_cap; i += kGrowBlock) __stcs(to + w0 + i, static_cast<u64>(win[i]));
+        __syncthreads();
+    }
+    // Overflow keys (rare: about one per tile). The count keeps growing past
+    // the list's capacity so the host can see that it must fall back.
+    const u32 lane = lane_id();
+    const u32 cnt = __popc(spill);
+    u32 incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<u32>(o)) incl += y;
+    }
+    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+    if (!total) return;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(reinterpret_cast<unsigned long long*>(overflow_count), static_cast<unsigned long long>(total));
+    u64 pos = __shfl_sync(0xffffffffu, base, 31) + (incl - cnt);
+#pragma unroll
+    for (int k = 0; k < kGrowItems; ++k)
+        if ((spill >> k) & 1u) {
+            if (pos < overflow_cap) overflow[pos] = key[k];
+            ++pos;
+        }
+}
+
 // ---- grouping of one-word keys by their first column (counting sort) ----------------
 //
 // Levels-mode DELTA only has to be grouped by column 0 for its join index
@@ -1144,6 +1223,34 @@ void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to) {
         from.slots.get(), n, to.slots.get(), to.mask, to.group_bits);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
+}
+
+bool engine_hash_grow(Ctx* c, const KeySet& from, KeySet& to) {
+    const u64 old_cap = from.capacity(), new_cap = to.capacity();
+    if (!old_cap || new_cap <= old_cap || from.group_bits != to.group_bits || old_cap % kGrowTile) return false;
+    const u64 factor = new_cap / old_cap;
+    u32 log_old = 0;
+    while ((u64(1) << log_old) < old_cap) ++log_old;
+    // Overflow list: a few keys per tile are expected; more (a pathological
+    // clustering) falls back to the memset + atomic rehash.
+    const u64 ov_cap = std::max<u64>(u64(1) << 16, old_cap / 64);
+    DBuf<u64> ov(c, ov_cap);
+    u64* d = c->d_scalars + 36;
+    FV_CUDA(cudaMemsetAsync(d, 0, 8, c->stream));
+    {
+        // Algorithmic bytes: the old table read once, the new one written once.
+        ProfScope prof(c, "hash_grow", double(old_cap) * 8.0 + double(new_cap) * 8.0);
+        hash_grow_kernel<<<static_cast<unsigned>(old_cap / kGrowTile), kGrowBlock, 0, c->stream>>>(
+            from.slots.get(), old_cap, log_old, static_cast<u32>(factor), to.slots.get(), to.mask, to.group_bits,
+            ov.get(), ov_cap, d);
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+    }
+    u64 n_ov = 0;
+    c->read_scalars(d, &n_ov, 1);
+    if (n_ov > ov_cap) return false;  // nothing of `to` is relied on: the caller redoes it
+    if (n_ov) engine_hash_insert(c, ov.get(), n_ov, to, nullptr, nullptr);
+    return true;
 }
 
 static void build_run_hash(Ctx* c, JoinIndex& idx);

@@ -283,6 +283,27 @@ def test_join_orders_match_reference(ctx, order, monkeypatch):
             assert matches(st.dump(rel).reshape(-1), exp["dump"]), (order, case["name"], rel)
 
 
+@pytest.mark.parametrize("grow", ["windowed", "rehash"])
+def test_keyset_growth_paths_match_reference(ctx, grow, monkeypatch):
+    # Key-set growth: windowed shared-memory rebuild (default) or memset +
+    # atomic rehash (FVLOG_GROW=rehash); both must give the reference's sets.
+    # C1 at full size grows its key set six times (2^16 -> 2^30 slots).
+    monkeypatch.setenv("FVLOG_GROW", grow)
+    for case in load_golden("engine.json"):
+        text, facts = golden_cases.program_and_facts(case)
+        st = E.evaluate_program(text, facts, ctx=ctx)
+        got = [(s.index, s.relation, s.delta_rows, s.full_rows, s.merges) for s in st.stats()]
+        assert got == [tuple(s) for s in case["stats"]], (grow, case["name"])
+        for rel, exp in case["relations"].items():
+            assert matches(st.dump(rel).reshape(-1), exp["dump"]), (grow, case["name"], rel)
+    g = _large().get("C1")
+    if g:
+        st = E.evaluate_program(W.TC_PROGRAM, {"edge": W.tc_uniform(10_000, 50_000, 1)}, ctx=ctx)
+        assert st.rows("reach") == g["rows"]
+        assert st.delta_counts()["reach"] == g["deltas"]
+        assert str(st.fingerprint("reach")) == g["fingerprint"]
+
+
 @pytest.mark.parametrize("group", ["0", "1"])
 def test_keyset_layouts_match_reference(ctx, group, monkeypatch):
     # FVLOG_KEYSET_GROUP forces the key-set home layout (0: every key
