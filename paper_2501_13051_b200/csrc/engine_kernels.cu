@@ -918,10 +918,23 @@ __global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __r
         const u64 i = base + u64(k) * blockDim.x;
         key[k] = i < n ? __ldcs(from + i) : kEmptySlot;
     }
+    // Keys are distinct: a key only has to find an empty slot. All first-slot
+    // loads, then all claims, are in flight together; the rest probe on.
+    u64 hs[kRehashItems], sv[kRehashItems];
+#pragma unroll
+    for (int k = 0; k < kRehashItems; ++k) {
+        hs[k] = keyset_home(keyset_line_hash(key[k], bits), key[k], bits, mask);
+        sv[k] = key[k] != kEmptySlot ? __ldcg(to + hs[k]) : 0;
+    }
 #pragma unroll
     for (int k = 0; k < kRehashItems; ++k)
-        if (key[k] != kEmptySlot)
-            keyset_insert_probe_from(to, mask, key[k], keyset_home(keyset_line_hash(key[k], bits), key[k], bits, mask));
+        if (key[k] != kEmptySlot && sv[k] == kEmptySlot)
+            sv[k] = atomicCAS(reinterpret_cast<unsigned long long*>(to + hs[k]), ~0ull,
+                              static_cast<unsigned long long>(key[k]));
+#pragma unroll
+    for (int k = 0; k < kRehashItems; ++k)
+        if (key[k] != kEmptySlot && sv[k] != kEmptySlot)
+            keyset_insert_probe_from(to, mask, key[k], (hs[k] + 1) & mask);
 }
 
 // Growth without a memset or global atomics. With the new capacity F times
