@@ -31,6 +31,10 @@ if [ -z "${SKIP_OPS:-}" ]; then
   timeout 900 python tools/bench_io.py --out "$OUT/io.json" > "$OUT/io.log" 2>&1
 fi
 
+if [ -z "${SKIP_OPS:-}" ]; then
+  timeout 900 python tools/bench_sharded.py --worlds 2,4,8 --out "$OUT/sharded.json" > "$OUT/sharded.log" 2>&1
+fi
+
 if [ -z "${SKIP_WORKLOADS:-}" ]; then
   timeout 1500 python tools/bench_workloads.py --out "$OUT/workloads.json" > "$OUT/workloads.log" 2>&1
   echo "workloads exit $?" >> "$OUT/workloads.log"
@@ -47,7 +51,11 @@ if [ -z "${SKIP_NCU:-}" ]; then
         --clock-control none --csv --log-file "$OUT/launches_$CFG.csv" \
         python tools/bench_workloads.py --configs $CFG --steps 1 --warmup 0 --no-reference > /dev/null 2>&1
   done
-  for KS in ${NCU_KERNELS:-materialize_kernel:6 group_scatter_kernel:10 hash_rehash_kernel:1}; do
+  # The partitioned engine's kernels: C2 over 8 virtual ranks on this GPU.
+  timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+      --clock-control none --csv --log-file "$OUT/launches_sharded8.csv" \
+      python tools/bench_sharded.py --worlds 8 --reps 1 > "$OUT/sharded_ncu.log" 2>&1
+  for KS in ${NCU_KERNELS:-materialize_kernel:6 group_scatter_kernel:10 hash_grow_kernel:3}; do
     K=${KS%%:*}; SKIP=${KS##*:}
     timeout 900 $NCU --set full --clock-control none --import-source on -k "regex:$K" \
         --launch-skip $SKIP -c ${NCU_COUNT:-1} -f -o "$OUT/full_$K" \

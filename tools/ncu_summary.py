@@ -34,6 +34,8 @@ PROFILER_TO_KERNEL = {
     "unpack_keys": "unpack_keys_kernel",
     "pack_keys": "pack_kernel",
     "join_probe_count": "probe_count_kernel",
+    "hash_grow": "hash_grow_kernel",
+    "hash_rehash": "hash_rehash_kernel",
 }
 
 FULL_METRICS = [
@@ -82,7 +84,9 @@ def main(src, dst):
     for f in sorted(os.listdir(src)):
         if f.startswith("launches_") and f.endswith(".csv"):
             ks, tot = summarise(os.path.join(src, f))
-            json.dump({"source": f"ncu launch list of one {f[9:-4]} fixpoint (tools/bench_workloads.py)",
+            src_txt = ("ncu launch list of C2 over 8 virtual ranks, all ranks (tools/bench_sharded.py)"
+                       if "sharded" in f else f"ncu launch list of one {f[9:-4]} fixpoint (tools/bench_workloads.py)")
+            json.dump({"source": src_txt,
                        "total_kernel_ms": tot, "kernels": ks},
                       open(os.path.join(dst, f.replace(".csv", ".json")), "w"), indent=1)
     for f in sorted(os.listdir(src)):
@@ -90,7 +94,7 @@ def main(src, dst):
             cap = full_capture(os.path.join(src, f))
             if cap:
                 json.dump(cap, open(os.path.join(dst, f.replace(".ncu-rep", ".json")), "w"), indent=1)
-    for f in ("bench.json", "membench.json", "workloads.json", "ops.json", "io.json", "sortbench.json",
+    for f in ("bench.json", "membench.json", "workloads.json", "ops.json", "io.json", "sortbench.json", "sharded.json",
               "pytest_gpu.log", "smoke.log", "nproc.txt", "lscpu.txt"):
         if os.path.exists(os.path.join(src, f)):
             shutil.copy(os.path.join(src, f), os.path.join(dst, f))
