@@ -296,6 +296,9 @@ public:
         } else {
             // Sorted copy keyed on `col` (ties by the remaining columns).
             const u32 arity = static_cast<u32>(base->cols.size());
+            if (trace_)
+                std::fprintf(stderr, "[fvlog]   sorted copy on col %u: %llu rows x %u cols\n", col,
+                             static_cast<unsigned long long>(base->n), arity);
             std::vector<const u32*> order_cols{base->cols[col].get()};
             for (u32 j = 0; j < arity; ++j)
                 if (j != col) order_cols.push_back(base->cols[j].get());
@@ -569,8 +572,14 @@ public:
                     spec.remote_rank = rank_;
                     FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
                 }
-                for (u64 t0 = 0; t0 < T; t0 += kFusedChunk) {
-                    const u64 t1 = std::min(T, t0 + kFusedChunk);
+                // A chunk's outputs bound the keys it can add to the local
+                // key set, which sizes the table (4x the bound). Routed runs
+                // keep only ~1/world of them, so their chunks shrink by the
+                // world size: per-rank tables sized for 2^28 new keys would
+                // be mostly empty and every growth would stream them.
+                const u64 chunk = route ? std::max<u64>(u64(1) << 24, kFusedChunk / world_) : kFusedChunk;
+                for (u64 t0 = 0; t0 < T; t0 += chunk) {
+                    const u64 t1 = std::min(T, t0 + chunk);
                     hash_reserve(hr, *sink, t1 - t0);
                     spec.ht_slots = hr.keys.slots.get();
                     spec.ht_mask = hr.keys.mask;
