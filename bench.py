@@ -346,6 +346,35 @@ def run_fvlog(args):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e_value = float(e2e_tuples) / (e2e_ms / 1000.0) if args_steps_e2e else None
 
+    # ---- untimed: key-set probe count of one fixpoint (FVLOG_TRACE) ----
+    # The fused join is bound by random key-set accesses, not by streaming
+    # bytes: count its probes on one extra, untimed step (the engine's trace
+    # counts them) to put its live duration against the measured random-load
+    # ceiling of tools/membench.cu.
+    probe_stats = None
+    if world == 1 and not args.partitioned:
+        os.environ["FVLOG_TRACE"] = "1"
+        sys.stderr.flush()
+        saved = os.dup(2)
+        with tempfile.TemporaryFile() as tmp:
+            os.dup2(tmp.fileno(), 2)
+            try:
+                st = step_resident()
+                del st
+                ctx.synchronize()
+            finally:
+                os.dup2(saved, 2)
+                os.close(saved)
+                del os.environ["FVLOG_TRACE"]
+            tmp.seek(0)
+            cands = probes = 0
+            for ln in tmp.read().decode(errors="replace").splitlines():
+                f = ln.split()
+                if "fused" in f and "dedup:" in f and len(f) >= 7:
+                    cands += int(f[3])
+                    probes += int(f[6])
+        probe_stats = (cands, probes)
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -366,6 +395,19 @@ def run_fvlog(args):
                     "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": top["bytes"] / top["launches"],
                     "avg_launch_ms": top["ms"] / top["launches"]}
+    random_access = None
+    join = next((k for k in kernels if k["name"] == "join_dedup"), None)
+    if probe_stats and join and probe_stats[1]:
+        mb = os.path.join(ROOT, "profiles", "r1", "membench.json")
+        ceiling = json.load(open(mb)).get("rand_load_gaccess_s") if os.path.exists(mb) else None
+        rate = probe_stats[1] / (join["ms"] / args.steps / 1000.0) / 1e9
+        random_access = {"kernel": "join_dedup", "candidates_per_step": probe_stats[0],
+                         "keyset_probes_per_step": probe_stats[1], "achieved_gprobes_s": round(rate, 2),
+                         "ceiling_gloads_s": ceiling,
+                         "frac": round(rate / ceiling, 3) if ceiling else None,
+                         "ceiling_source": "random 8-byte loads into an 8 GB table, tools/membench.cu on a B200 "
+                                           "(profiles/r1/membench.json)",
+                         "probe_count_source": "one extra untimed step with FVLOG_TRACE=1"}
     step_ms = t_max / args.steps
     total_kernel_ms = sum(k["ms"] for k in kernels)
     line = {
@@ -387,6 +429,7 @@ def run_fvlog(args):
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),
         "roofline": roofline,
+        "random_access": random_access,
         "kernels": [{"name": k["name"], "launches": k["launches"], "ms_per_step": k["ms"] / args.steps,
                      "share": round(k["ms"] / total_kernel_ms, 4) if total_kernel_ms else None,
                      "gbs": round(k["bytes"] / (k["ms"] / 1000.0) / 1e9, 1) if k["ms"] else None}
