@@ -1246,7 +1246,10 @@ bool engine_hash_grow(Ctx* c, const KeySet& from, KeySet& to) {
     while ((u64(1) << log_old) < old_cap) ++log_old;
     // Overflow list: a few keys per tile are expected; more (a pathological
     // clustering) falls back to the memset + atomic rehash.
-    const u64 ov_cap = std::max<u64>(u64(1) << 16, old_cap / 64);
+    // FVLOG_GROW_OVERFLOW_CAP (tests): a tiny list forces the fallback.
+    const char* forced = std::getenv("FVLOG_GROW_OVERFLOW_CAP");
+    const long long forced_cap = forced ? std::atoll(forced) : -1ll;
+    const u64 ov_cap = forced_cap > 0 ? static_cast<u64>(forced_cap) : std::max<u64>(u64(1) << 16, old_cap / 64);
     DBuf<u64> ov(c, ov_cap);
     u64* d = c->d_scalars + 36;
     FV_CUDA(cudaMemsetAsync(d, 0, 8, c->stream));

@@ -283,12 +283,18 @@ def test_join_orders_match_reference(ctx, order, monkeypatch):
             assert matches(st.dump(rel).reshape(-1), exp["dump"]), (order, case["name"], rel)
 
 
-@pytest.mark.parametrize("grow", ["windowed", "rehash"])
+@pytest.mark.parametrize("grow", ["windowed", "rehash", "overflow"])
 def test_keyset_growth_paths_match_reference(ctx, grow, monkeypatch):
-    # Key-set growth: windowed shared-memory rebuild (default) or memset +
-    # atomic rehash (FVLOG_GROW=rehash); both must give the reference's sets.
-    # C1 at full size grows its key set six times (2^16 -> 2^30 slots).
-    monkeypatch.setenv("FVLOG_GROW", grow)
+    # Key-set growth: windowed shared-memory rebuild (default; its overflow
+    # list holds the few keys that leave their window), memset + atomic
+    # rehash (FVLOG_GROW=rehash), or the windowed pass abandoned because the
+    # overflow list filled up (a 1-entry list) and redone by the rehash.
+    # All must give the reference's sets. C1 at full size grows its key set
+    # several times (2^16 -> 2^30 slots).
+    if grow == "overflow":
+        monkeypatch.setenv("FVLOG_GROW_OVERFLOW_CAP", "1")
+    else:
+        monkeypatch.setenv("FVLOG_GROW", grow)
     for case in load_golden("engine.json"):
         text, facts = golden_cases.program_and_facts(case)
         st = E.evaluate_program(text, facts, ctx=ctx)
