@@ -947,14 +947,20 @@ __global__ void hash_rehash_kernel(const u64* __restrict__ from, u64 n, u64* __r
 // in an earlier tile (displaced across the tile boundary) or their probe run
 // reaches the window's end — go to an overflow list that a plain insert
 // places afterwards, when every slot has been written.
+#ifndef FV_GROW_VEC
+#define FV_GROW_VEC 1
+#endif
+#ifndef FV_GROW_MINB
+#define FV_GROW_MINB 1
+#endif
 constexpr int kGrowItems = 8;
 constexpr int kGrowBlock = 256;
 constexpr u32 kGrowTile = kGrowItems * kGrowBlock;
-__global__ void __launch_bounds__(kGrowBlock) hash_grow_kernel(const u64* __restrict__ from, u64 old_cap,
+__global__ void __launch_bounds__(kGrowBlock, FV_GROW_MINB) hash_grow_kernel(const u64* __restrict__ from, u64 old_cap,
                                                                u32 log_old, u32 factor, u64* __restrict__ to,
                                                                u64 new_mask, u32 bits, u64* __restrict__ overflow,
                                                                u64 overflow_cap, u64* overflow_count) {
-    __shared__ unsigned long long win[kGrowTile];
+    __shared__ __align__(16) unsigned long long win[kGrowTile];
     const u64 a = u64(blockIdx.x) * kGrowTile;
     u64 key[kGrowItems];
     u32 local[kGrowItems];
@@ -990,7 +996,13 @@ __global__ void __launch_bounds__(kGrowBlock) hash_grow_kernel(const u64* __rest
         }
         __syncthreads();
         const u64 w0 = a + (u64(j) << log_old);
+#if FV_GROW_VEC
+        // 16-byte streaming stores (windows start at multiples of the tile).
+        for (u32 i = 2 * threadIdx.x; i < kGrowTile; i += 2 * kGrowBlock)
+            __stcs(reinterpret_cast<ulonglong2*>(to + w0 + i), *reinterpret_cast<const ulonglong2*>(win + i));
+#else
         for (u32 i = threadIdx.x; i < kGrowTile && a + i < old_cap; i += kGrowBlock) __stcs(to + w0 + i, static_cast<u64>(win[i]));
+#endif
         __syncthreads();
     }
     // Overflow keys (rare: about one per tile). The count keeps growing past
