@@ -94,6 +94,13 @@ def main(src, dst):
             cap = full_capture(os.path.join(src, f))
             if cap:
                 json.dump(cap, open(os.path.join(dst, f.replace(".ncu-rep", ".json")), "w"), indent=1)
+            if f == "full_materialize_kernel.ncu-rep":
+                from ncu_stalls import stalls  # warp-stall samples per source line
+                try:
+                    json.dump(stalls(os.path.join(src, f)),
+                              open(os.path.join(dst, "stalls_materialize_kernel.json"), "w"), indent=1)
+                except Exception as e:  # noqa: BLE001 (capture without source counters)
+                    print("stalls:", e)
     for f in ("bench.json", "membench.json", "workloads.json", "ops.json", "io.json", "sortbench.json", "sharded.json",
               "pytest_gpu.log", "smoke.log", "nproc.txt", "lscpu.txt"):
         if os.path.exists(os.path.join(src, f)):
