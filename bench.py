@@ -352,7 +352,7 @@ def run_fvlog(args):
     # counts them) to put its live duration against the measured random-load
     # ceiling of tools/membench.cu.
     probe_stats = None
-    if world == 1 and not args.partitioned:
+    if world == 1 and not args.partitioned and not args.no_random_access:
         os.environ["FVLOG_TRACE"] = "1"
         sys.stderr.flush()
         saved = os.dup(2)
@@ -455,6 +455,8 @@ def main():
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
+    ap.add_argument("--no-random-access", action="store_true",
+                    help="skip the untimed traced step that counts key-set probes (profiling runs)")
     ap.add_argument("--reserve-gb", type=float, default=96.0, help="fv_ctx_reserve before warm-up")
     ap.add_argument("--partitioned", action="store_true",
                     help="N=1 only: run the hash-partitioned multi-GPU path over a 1-rank NCCL communicator")

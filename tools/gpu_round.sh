@@ -44,7 +44,7 @@ if [ -z "${SKIP_NCU:-}" ]; then
   NCU=/usr/local/cuda/bin/ncu
   timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       --clock-control none --csv --log-file "$OUT/launches.csv" \
-      python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > "$OUT/ncu_launch_bench.log" 2>&1
+      python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-random-access > "$OUT/ncu_launch_bench.log" 2>&1
   echo "ncu launches exit $?" >> "$OUT/ncu_launch_bench.log"
   for CFG in C1 C3 C4 C5; do
     timeout 600 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
@@ -59,7 +59,7 @@ if [ -z "${SKIP_NCU:-}" ]; then
     K=${KS%%:*}; SKIP=${KS##*:}
     timeout 900 $NCU --set full --clock-control none --import-source on -k "regex:$K" \
         --launch-skip $SKIP -c ${NCU_COUNT:-1} -f -o "$OUT/full_$K" \
-        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > "$OUT/ncu_full_$K.log" 2>&1
+        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-random-access > "$OUT/ncu_full_$K.log" 2>&1
     echo "ncu full $K exit $?" >> "$OUT/ncu_full_$K.log"
   done
 fi
