@@ -55,7 +55,7 @@ if [ -z "${SKIP_NCU:-}" ]; then
   timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       --clock-control none --csv --log-file "$OUT/launches_sharded8.csv" \
       python tools/bench_sharded.py --worlds 8 --reps 1 > "$OUT/sharded_ncu.log" 2>&1
-  for KS in ${NCU_KERNELS:-materialize_kernel:6 group_scatter_kernel:10 hash_grow_kernel:3}; do
+  for KS in ${NCU_KERNELS:-materialize_kernel:6 group_scatter_kernel:10 hash_grow_kernel:2}; do
     K=${KS%%:*}; SKIP=${KS##*:}
     timeout 900 $NCU --set full --clock-control none --import-source on -k "regex:$K" \
         --launch-skip $SKIP -c ${NCU_COUNT:-1} -f -o "$OUT/full_$K" \
