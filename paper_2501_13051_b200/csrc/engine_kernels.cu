@@ -208,7 +208,10 @@ constexpr int kMatSetSlots = FV_MAT_SET_SLOTS;  // tile-local set; load <= 1/2 a
 #ifndef FV_MAT_BATCH_CAS
 #define FV_MAT_BATCH_CAS 2  // 2: batched for the plain join only (the filtered variant spills: C3 32.9 vs 32.5 ms)
 #endif
-constexpr int kMatSetProbes = 16;               // bounded: an unplaced key is simply probed globally
+#ifndef FV_MAT_SET_PROBES
+#define FV_MAT_SET_PROBES 16  // measured: 4 slower (C2 93.5 vs 92.7 ms), 64 equal
+#endif
+constexpr int kMatSetProbes = FV_MAT_SET_PROBES;               // bounded: an unplaced key is simply probed globally
 
 __device__ __forceinline__ u64 upper_bound_u64(const u64* __restrict__ a, u64 len, u64 x) {
     u64 lo = 0, hi = len;
