@@ -306,6 +306,7 @@ fv_status fv_version_from_columns(fv_ctx* ctx, uint32_t arity, const uint32_t* c
                                   uint64_t n, fv_version** out) {
     FV_API_BEGIN(ctx)
     FV_REQUIRE(out, FV_ERR_INVALID, "fv_version_from_columns: null out");
+    FV_REQUIRE(arity <= FV_MAX_ARITY, FV_ERR_ARITY, "fv_version_from_columns: arity exceeds FV_MAX_ARITY");
     std::vector<DBuf<u32>> dcols;
     for (u32 j = 0; j < arity; ++j) {
         FV_REQUIRE(cols && (cols[j] || n == 0), FV_ERR_INVALID, "fv_version_from_columns: null column");
@@ -320,6 +321,7 @@ fv_status fv_version_decompose(fv_ctx* ctx, uint32_t arity, const uint32_t* rows
                                fv_version** out) {
     FV_API_BEGIN(ctx)
     FV_REQUIRE(out && (rows || n == 0 || arity == 0), FV_ERR_INVALID, "fv_version_decompose: null argument");
+    FV_REQUIRE(arity <= FV_MAX_ARITY, FV_ERR_ARITY, "fv_version_decompose: arity exceeds FV_MAX_ARITY");
     std::vector<std::vector<u32>> cols(arity, std::vector<u32>(n));
     for (u64 i = 0; i < n; ++i)
         for (u32 j = 0; j < arity; ++j) cols[j][i] = rows[i * arity + j];

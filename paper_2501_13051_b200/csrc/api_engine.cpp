@@ -485,8 +485,11 @@ fv_status fv_state_stat(const fv_state* s, uint64_t i, uint64_t* iteration, cons
 fv_status fv_state_dump_sorted(const fv_state* s, const char* rel, uint32_t* rows_out) {
     FV_API_BEGIN(s ? s->ctx : nullptr)
     FV_REQUIRE(s && rel, FV_ERR_INVALID, "fv_state_dump_sorted: null argument");
-    auto rows = fv::dump_sorted(*s->st, rel);
-    if (rows_out && !rows.empty()) std::memcpy(rows_out, rows.data(), rows.size() * sizeof(u32));
+    if (rows_out) {
+        fv::dump_sorted_into(*s->st, rel, rows_out);
+    } else {
+        if (!s->st->relations.count(rel)) fv::fail(FV_ERR_RANGE, std::string("unknown relation '") + rel + "'");
+    }
     FV_API_END
 }
 

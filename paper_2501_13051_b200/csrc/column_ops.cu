@@ -424,10 +424,16 @@ std::unique_ptr<Version> version_empty(Ctx* c, u32 arity) {
 }
 
 std::unique_ptr<Version> version_from_device(Ctx* c, std::vector<DBuf<u32>>&& cols, u64 n) {
+    // Every row operator keeps per-column pointers in FV_MAX_ARITY-sized
+    // arrays (ColPtrs, RunsArgs): a wider version is rejected here, at its
+    // only constructor, instead of overrunning them later.
+    if (cols.size() > FV_MAX_ARITY)
+        fail(FV_ERR_ARITY, "version arity " + std::to_string(cols.size()) + " exceeds FV_MAX_ARITY");
     auto v = std::make_unique<Version>();
     v->ctx = c;
     v->arity = static_cast<u32>(cols.size());
-    v->rows = n;
+    // Version::rows() is 0 for a version without columns (P/include/colog/relation.hpp:31).
+    v->rows = cols.empty() ? 0 : n;
     for (auto& col : cols) v->cols.push_back(column_build(c, std::move(col), n));
     return v;
 }
@@ -602,6 +608,7 @@ std::unique_ptr<Version> dedup_rows(Ctx* c, const Version& v) {
 
 bool has_duplicate_rows(Ctx* c, const Version& v) {
     if (v.rows < 2) return false;
+    if (v.arity > FV_MAX_ARITY) fail(FV_ERR_ARITY, "has_duplicate_rows: arity exceeds FV_MAX_ARITY");
     std::vector<const u32*> cp(v.arity);
     for (u32 j = 0; j < v.arity; ++j) cp[j] = v.cols[j]->raw.get();
     DBuf<u32> perm = lexicographic_order(c, cp.data(), v.arity, v.rows);
@@ -614,6 +621,7 @@ bool has_duplicate_rows(Ctx* c, const Version& v) {
 
 DBuf<u8> deduplicate(Ctx* c, const Version& nv, const Version& full) {
     if (nv.arity != full.arity) fail(FV_ERR_ARITY, "deduplicate: arity mismatch");
+    if (nv.arity > FV_MAX_ARITY) fail(FV_ERR_ARITY, "deduplicate: arity exceeds FV_MAX_ARITY");
     const u64 n = nv.rows;
     DBuf<u8> flags(c, n);
     if (n == 0) return flags;

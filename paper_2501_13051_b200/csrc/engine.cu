@@ -1425,6 +1425,8 @@ std::vector<std::unique_ptr<EvalState>> evaluate_sharded(Ctx* base, u32 world, c
                     out[r] = evaluate(ctxs[r], decls, plans, facts);
                 } catch (...) {
                     errs[r] = std::current_exception();
+                    // Peers blocked in a collective would otherwise wait forever.
+                    group[r]->abort();
                 }
             });
         for (auto& t : threads) t.join();
@@ -1441,6 +1443,9 @@ std::vector<std::unique_ptr<EvalState>> evaluate_sharded(Ctx* base, u32 world, c
             ctx_delete(ctxs[r]);
         }
     }
+    // The first failure is the cause; the others are the aborts it triggered.
+    const int first = group[0]->first_failed();
+    if (first >= 0 && errs[first]) std::rethrow_exception(errs[first]);
     for (auto& e : errs)
         if (e) std::rethrow_exception(e);
     return out;
@@ -1498,16 +1503,31 @@ const RelState& find_rel(const EvalState& s, const std::string& rel) {
 
 }  // namespace
 
-std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel) {
+void dump_sorted_into(const EvalState& s, const std::string& rel, u32* rows_out) {
     const RelState& r = find_rel(s, rel);
+    Ctx* c = s.ctx;
     DevVersion tmp;
     const DevVersion& src = sorted_rows(s, r, tmp);
     const u64 n = r.rows();
-    std::vector<u32> rows(n * r.arity), col(n);
-    for (u32 j = 0; j < r.arity; ++j) {
-        src.cols[j].download(col.data(), n);
-        for (u64 i = 0; i < n; ++i) rows[i * r.arity + j] = col[i];
+    if (!n) return;
+    // Bounded staging: rows are interleaved and copied out in 2^26-row chunks.
+    const u64 chunk = std::min<u64>(n, u64(1) << 26);
+    DBuf<u32> buf(c, chunk * r.arity);
+    for (u64 off = 0; off < n; off += chunk) {
+        const u64 m = std::min(chunk, n - off);
+        std::vector<const u32*> cols;
+        for (u32 j = 0; j < r.arity; ++j) cols.push_back(src.cols[j].get() + off);
+        engine_interleave(c, cols, m, buf.get());
+        FV_CUDA(cudaMemcpyAsync(rows_out + off * r.arity, buf.get(), 4 * m * r.arity, cudaMemcpyDeviceToHost,
+                                c->stream));
     }
+    c->sync();
+}
+
+std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel) {
+    const RelState& r = find_rel(s, rel);
+    std::vector<u32> rows(r.rows() * r.arity);
+    dump_sorted_into(s, rel, rows.data());
     return rows;
 }
 

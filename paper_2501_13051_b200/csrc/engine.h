@@ -210,6 +210,10 @@ void check_plans(const std::vector<RelationDecl>& decls, const std::vector<Plan>
 
 // Lexicographically sorted row-major dump of FULL (host).
 std::vector<u32> dump_sorted(const EvalState& s, const std::string& rel);
+// The same rows written straight into a caller's host buffer (rows x arity
+// u32): sorted and interleaved on the device, one D2H copy per chunk (pinned
+// buffers copy at PCIe / C2C rate).
+void dump_sorted_into(const EvalState& s, const std::string& rel, u32* rows_out);
 // dump_relation text (integer mode) of the sorted rows, formatted on the device.
 std::string dump_sorted_text(const EvalState& s, const std::string& rel);
 u64 fingerprint(const EvalState& s, const std::string& rel);
@@ -294,6 +298,8 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
                        u32* col1 = nullptr);
 // Distinct rows of sorted packed keys into fresh word buffers; returns the count.
 u64 engine_unique_words(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, std::vector<DBuf<u64>>& out);
+// SoA columns -> row-major rows out[i * arity + j] (device buffer).
+void engine_interleave(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32* out);
 // Keys -> SoA columns (one word per row, arity <= 2).
 void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, const std::vector<u32*>& cols);
 

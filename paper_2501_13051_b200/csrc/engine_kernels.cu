@@ -1143,6 +1143,17 @@ __global__ void unpack_keys_kernel(const u64* __restrict__ keys, u64 n, u32 arit
     }
 }
 
+// SoA columns -> row-major rows (the dump layout), one row per thread.
+__global__ void interleave_kernel(Cols8 c, u32 arity, u64 n, u32* __restrict__ out) {
+    GRID_STRIDE(i, n) {
+#pragma unroll
+        for (int j = 0; j < FV_MAX_ARITY; ++j) {
+            if (j >= static_cast<int>(arity)) break;
+            out[i * arity + j] = c.p[j][i];
+        }
+    }
+}
+
 // Distinct rows of sorted packed keys, unpacked into SoA columns (one
 // look-back compaction: a row is kept when any word differs from its
 // predecessor's).
@@ -1326,6 +1337,18 @@ void engine_unpack_keys(Ctx* c, const u64* keys, u64 n, u32 arity, u32 shift, co
     ProfScope prof(c, "unpack_keys", double(n) * (8.0 + 4.0 * arity));
     unpack_keys_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, n, arity, shift, cols[0],
                                                             arity == 2 ? cols[1] : nullptr);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void engine_interleave(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32* out) {
+    if (!n) return;
+    const u32 arity = static_cast<u32>(cols.size());
+    if (arity == 0 || arity > FV_MAX_ARITY) fail(FV_ERR_ARITY, "interleave: arity out of range");
+    Cols8 cp{};
+    for (u32 j = 0; j < arity; ++j) cp.p[j] = cols[j];
+    ProfScope prof(c, "dump_interleave", 8.0 * double(n) * arity);
+    interleave_kernel<<<grid_for(n), 256, 0, c->stream>>>(cp, arity, n, out);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }

@@ -197,8 +197,18 @@ int run(Ctx* c, const RunConfig& cfg, std::ostream& out, std::ostream& err) {
         auto plans = fe::compile(prog);
         const auto decls = fe::declarations(prog);
         check_plans(decls, plans);
+        // total_ms spans the host-fact upload too, like fv_evaluate and the
+        // reference's evaluate(), which seeds from host rows
+        // (P/src/runner.cpp:58-61); facts parsed on the device are already
+        // resident (their parse is the "load facts" phase, as the
+        // reference's TSV load is).
+        const auto t_up = std::chrono::steady_clock::now();
         DeviceEdb host_edb = upload_facts(c, decls, blocks);
+        c->sync();
+        const double upload_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_up).count();
         auto st = evaluate_device(c, decls, plans, {&host_edb, &file_edb});
+        st->elapsed_ms += upload_ms;
         phase("evaluate");
 
         if (cfg.print_stats)

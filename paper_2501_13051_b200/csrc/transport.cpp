@@ -129,6 +129,10 @@ struct LocalShared {
     std::condition_variable cv;
     int arrived = 0;
     u64 generation = 0;
+    // Set by the first rank that fails: every rank waiting in (or later
+    // reaching) a barrier throws instead of waiting for it forever.
+    bool aborted = false;
+    int first_failed = -1;
     std::vector<const u64*> counts;
     std::vector<const std::vector<ExchangeCol>*> cols;
     std::vector<const u64*> scnt, soff;
@@ -136,14 +140,23 @@ struct LocalShared {
 
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
+        if (aborted) fail(FV_ERR_INVALID, "in-process group aborted by another rank");
         const u64 gen = generation;
         if (++arrived == world) {
             arrived = 0;
             ++generation;
             cv.notify_all();
         } else {
-            cv.wait(lk, [&] { return generation != gen; });
+            cv.wait(lk, [&] { return generation != gen || aborted; });
+            if (generation == gen) fail(FV_ERR_INVALID, "in-process group aborted by another rank");
         }
+    }
+
+    void abort(int rank) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (first_failed < 0) first_failed = rank;
+        aborted = true;
+        cv.notify_all();
     }
 };
 
@@ -152,6 +165,8 @@ public:
     LocalTransport(std::shared_ptr<LocalShared> s, int rank) : s_(std::move(s)), rank_(rank) {}
     int rank() const override { return rank_; }
     int world() const override { return s_->world; }
+    void abort() override { s_->abort(rank_); }
+    int first_failed() const override { return s_->first_failed; }
 
     void exchange_counts(Ctx*, const u64* send_counts, u64* recv_counts) override {
         s_->counts[rank_] = send_counts;
@@ -167,19 +182,26 @@ public:
         s_->scnt[rank_] = scnt;
         s_->soff[rank_] = soff;
         s_->barrier();
-        for (size_t j = 0; j < cols.size(); ++j) {
-            for (int p = 0; p < s_->world; ++p) {
-                const ExchangeCol& src = (*s_->cols[p])[j];
-                const u64 n = s_->scnt[p][rank_];
-                if (n != rcnt[p]) fail(FV_ERR_INVALID, "local exchange: count mismatch");
-                if (!n) continue;
-                const char* from = static_cast<const char*>(src.send) + s_->soff[p][rank_] * src.elem;
-                char* to = static_cast<char*>(cols[j].recv) + roff[p] * cols[j].elem;
-                FV_CUDA(cudaMemcpyAsync(to, from, n * src.elem, cudaMemcpyDeviceToDevice, c->stream));
+        // Validate before touching any peer buffer, and report a mismatch
+        // only after the closing barrier: a rank must not unwind (and free
+        // the send buffers its peers are reading) while the exchange runs.
+        bool ok = true;
+        for (int p = 0; p < s_->world; ++p) ok = ok && s_->scnt[p][rank_] == rcnt[p];
+        if (ok) {
+            for (size_t j = 0; j < cols.size(); ++j) {
+                for (int p = 0; p < s_->world; ++p) {
+                    const ExchangeCol& src = (*s_->cols[p])[j];
+                    const u64 n = s_->scnt[p][rank_];
+                    if (!n) continue;
+                    const char* from = static_cast<const char*>(src.send) + s_->soff[p][rank_] * src.elem;
+                    char* to = static_cast<char*>(cols[j].recv) + roff[p] * cols[j].elem;
+                    FV_CUDA(cudaMemcpyAsync(to, from, n * src.elem, cudaMemcpyDeviceToDevice, c->stream));
+                }
             }
+            c->sync();
         }
-        c->sync();
         s_->barrier();  // peers may release their send buffers now
+        if (!ok) fail(FV_ERR_INVALID, "local exchange: count mismatch");
     }
 
     void allreduce_sum(Ctx*, u64* vals, int n) override {

@@ -36,6 +36,10 @@ public:
                                const u64* rcnt, const u64* roff) = 0;
     // Element-wise sum over ranks of n host values (in place).
     virtual void allreduce_sum(Ctx* c, u64* vals, int n) = 0;
+    // In-process groups: a failing rank releases its peers (their pending
+    // and later collectives throw) and the group remembers who failed first.
+    virtual void abort() {}
+    virtual int first_failed() const { return -1; }
 };
 
 // NCCL (one process per GPU). `id` is a 128-byte ncclUniqueId.

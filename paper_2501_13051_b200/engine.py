@@ -365,6 +365,17 @@ class State:
             check(self.l.fv_state_dump_sorted(self.h, rel.encode(), out.ctypes.data_as(u32p)), self.ctx.h)
         return out
 
+    def dump_into(self, rel: str, out: np.ndarray) -> int:
+        """Sorted rows of `rel` written into a caller-provided C-contiguous
+        u32 buffer of at least rows x arity elements (e.g. a pinned host
+        tensor's numpy view); returns the row count."""
+        a, n = self.relations()[rel]
+        if out.dtype != np.uint32 or not out.flags["C_CONTIGUOUS"] or out.size < n * a:
+            raise ValueError("dump_into: need a C-contiguous uint32 buffer of rows x arity elements")
+        if n:
+            check(self.l.fv_state_dump_sorted(self.h, rel.encode(), out.ctypes.data_as(u32p)), self.ctx.h)
+        return n
+
     def fingerprint(self, rel: str) -> int:
         v = C.c_uint64()
         check(self.l.fv_state_fingerprint(self.h, rel.encode(), C.byref(v)), self.ctx.h)

@@ -239,6 +239,27 @@ def test_decompose_reconstruct(C):
         C.Version.decompose([(1, 2, 3)], 2)
 
 
+def test_arity_beyond_max_is_rejected(C):
+    # a 9-column version must be an FV_ERR_ARITY, not a stack overrun.
+    rows = W.random_rows(5, 64, 9, 10)
+    with pytest.raises(_lib.ArityError):
+        C.Version.decompose(rows, 9)
+    with pytest.raises(_lib.ArityError):
+        C.Version.from_columns([rows[:, j] for j in range(9)])
+    with pytest.raises(_lib.ArityError):
+        C.Version.empty_version(9)
+    v = C.Version.decompose(W.random_rows(6, 64, 3, 10), 3)
+    with pytest.raises(_lib.ArityError):
+        C.project(v, np.arange(64), [0, 1, 2, 0, 1, 2, 0, 1, 2])
+
+
+def test_zero_column_version_has_no_rows(C):
+    # P/include/colog/relation.hpp:31: Version::rows() is 0 without columns.
+    v = C.Version.decompose(W.random_rows(7, 16, 2, 10), 2)
+    p = C.project(v, np.arange(16), [])
+    assert p.arity() == 0 and p.rows() == 0
+
+
 def test_dedup_rows_golden(C):
     for c in load_golden("dedup_rows.json"):
         rows = (np.asarray(c["rows"], np.uint32).reshape(-1, c["arity"]) if "rows" in c
