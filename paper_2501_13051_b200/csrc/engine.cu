@@ -108,9 +108,22 @@ struct HeadSink {
     DBuf<u64> keys;
     u64 cap = 0;
     u64 bound = 0;  // host upper bound of the device count
-    DBuf<u64> counter;
+    DBuf<u64> counter;   // [0] new keys, [1] overflow keys (block sets)
     u64 candidates = 0;  // rows offered to the key set this iteration
+    // Block sets: keys the set could not place (drained before every chunk).
+    DBuf<u64> ovf;
+    u64 ovf_cap = 0;
+    u64 chunk_blocks0 = 0, chunk_cands = 0;  // growth-ratio bookkeeping
 };
+
+// Block sets (BlockSet, engine.h): a relation falls back to a key set when
+// its directory would need more than kBlockSparseFactor x the bytes of the
+// equivalent key set and more than kBlockSparseMinBytes (FVLOG_SET=keyset
+// uses key sets throughout).
+constexpr double kBlockSparseFactor = 8.0;
+constexpr double kBlockSparseMinBytes = 1e9;
+constexpr u64 kBlockMinCap = u64(1) << 12;
+std::vector<const DevVersion*> levels_of(const RelState& r);
 
 // Key-set layout choice (KeySet::group_bits, see keyset_home in
 // engine_kernels.cu): group pairs of adjacent keys while a relation's
@@ -581,11 +594,20 @@ public:
                 for (u64 t0 = 0; t0 < T; t0 += chunk) {
                     const u64 t1 = std::min(T, t0 + chunk);
                     hash_reserve(hr, *sink, t1 - t0);
-                    spec.ht_slots = hr.keys.slots.get();
-                    spec.ht_mask = hr.keys.mask;
-                    spec.ht_group_bits = hr.keys.group_bits;
-                    // grouped layout <=> last iteration's candidates were all new
-                    spec.tile_set = hr.keys.group_bits == 0 ? 1u : 0u;
+                    if (hr.block_mode) {
+                        spec.ht_slots = nullptr;
+                        spec.bs = block_args(hr);
+                        spec.ovf_keys = sink->ovf.get();
+                        spec.ovf_count = sink->counter.get() + 1;
+                        spec.tile_set = block_tile_set_;
+                    } else {
+                        spec.bs = BlockSetArgs();
+                        spec.ht_slots = hr.keys.slots.get();
+                        spec.ht_mask = hr.keys.mask;
+                        spec.ht_group_bits = hr.keys.group_bits;
+                        // grouped layout <=> last iteration's candidates were all new
+                        spec.tile_set = hr.keys.group_bits == 0 ? 1u : 0u;
+                    }
                     spec.new_keys = sink->keys.get();
                     spec.new_count = sink->counter.get();
                     engine_materialize(c_, offsets.get(), n, T, starts.get(), spec, t0, t1);
@@ -879,8 +901,12 @@ public:
     // in the relation's key set at load factor <= 1/2 (rehash when needed).
     void hash_reserve(RelState& r, HeadSink& s, u64 extra) {
         if (!s.counter.get()) {
-            s.counter = DBuf<u64>(c_, 1);
-            FV_CUDA(cudaMemsetAsync(s.counter.get(), 0, 8, c_->stream));
+            s.counter = DBuf<u64>(c_, 2);
+            FV_CUDA(cudaMemsetAsync(s.counter.get(), 0, 16, c_->stream));
+        }
+        if (r.block_mode) {
+            block_reserve(r, s, extra);
+            if (r.block_mode) return;  // else: converted to a key set, reserve that
         }
         if (s.bound + extra > s.cap) {
             const u64 have = sink_count(s);
@@ -935,6 +961,157 @@ public:
         r.keys = std::move(ns);
     }
 
+    // ---- block-set dedup ---------------------------------------------------------
+
+    BlockSetArgs block_args(const RelState& r) const {
+        BlockSetArgs a;
+        a.dir = r.blocks.dir.get();
+        a.bits = r.blocks.bits.get();
+        a.mask = r.blocks.mask;
+        a.count = r.blocks.count.get();
+        a.limit = r.blocks.capacity() / 4 * 3;
+        a.shift = st_.key_shift;
+        a.arity = r.arity;
+        return a;
+    }
+
+    // Sink counters (new, overflow) and the block count in one sync; also
+    // updates the relation's new-blocks-per-candidate estimate.
+    void read_block_counters(RelState& r, HeadSink& s, u64* nw, u64* ov) {
+        FV_CUDA(cudaMemcpyAsync(c_->pinned, s.counter.get(), 16, cudaMemcpyDeviceToHost, c_->stream));
+        FV_CUDA(cudaMemcpyAsync(c_->pinned + 2, r.blocks.count.get(), 8, cudaMemcpyDeviceToHost, c_->stream));
+        c_->sync();
+        *nw = c_->pinned[0];
+        *ov = c_->pinned[1];
+        r.blocks.blocks = c_->pinned[2];
+        s.bound = std::max(s.bound, *nw);
+        if (s.chunk_cands) {
+            const double got = double(r.blocks.blocks - std::min(r.blocks.blocks, s.chunk_blocks0)) /
+                               double(s.chunk_cands);
+            r.blocks.ratio = std::max(r.blocks.ratio * 0.5, got);
+            s.chunk_cands = 0;
+        }
+    }
+
+    // Directory capacity for `need` blocks at load <= 1/2; false when that
+    // would make the set too sparse to pay (the caller converts it).
+    bool block_grow(RelState& r, u64 need, u64 live_keys) {
+        BlockSet& b = r.blocks;
+        if (b.capacity() && need <= b.capacity() / 2) return true;
+        u64 cap = kBlockMinCap;
+        while (cap < 2 * need) cap <<= 1;
+        // Sparse (about one row per block): the key set of the rows present
+        // is several times smaller; switch once the directory is large.
+        const double bytes = 136.0 * double(cap);
+        const double keyset_bytes = 8.0 * kKeysetGrowth * double(std::max<u64>(live_keys, 1));
+        if (force_blocks_ < 0 && bytes > block_sparse_bytes_ && bytes > kBlockSparseFactor * keyset_bytes)
+            return false;
+        BlockSet ns;
+        engine_blockset_alloc(c_, ns, cap, b.blocks);
+        ns.ratio = b.ratio;
+        if (b.capacity()) engine_blockset_grow(c_, b, ns);
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   %s block set -> %llu slots (%llu blocks)\n", r.name.c_str(),
+                         static_cast<unsigned long long>(cap), static_cast<unsigned long long>(b.blocks));
+        b = std::move(ns);
+        return true;
+    }
+
+    // Insert the overflow list (n keys) after growing the directory; repeats
+    // until the set placed every key.
+    void drain_overflow(RelState& r, HeadSink& s, u64 n) {
+        while (n) {
+            DBuf<u64> tmp(c_, n);
+            FV_CUDA(cudaMemcpyAsync(tmp.get(), s.ovf.get(), 8 * n, cudaMemcpyDeviceToDevice, c_->stream));
+            FV_CUDA(cudaMemsetAsync(s.counter.get() + 1, 0, 8, c_->stream));
+            // At least double the directory (n keys may share far fewer
+            // blocks; another round follows if they do not fit).
+            const u64 need = std::max(r.blocks.blocks + std::max<u64>(4096, std::min(n, r.blocks.blocks)),
+                                      r.blocks.capacity() / 2 + 1);
+            if (!block_grow(r, need, r.keys.count + s.bound + n)) {
+                // too sparse for blocks: the key set takes over, overflow keys included
+                convert_to_keyset(r, &s, tmp.get(), n);
+                return;
+            }
+            engine_blockset_insert(c_, tmp.get(), n, block_args(r), s.keys.get(), s.counter.get(), s.ovf.get(),
+                                   s.counter.get() + 1);
+            u64 nw;
+            read_block_counters(r, s, &nw, &n);
+        }
+    }
+
+    void block_reserve(RelState& r, HeadSink& s, u64 extra) {
+        if (s.bound + extra > s.cap) {
+            const u64 have = sink_count(s);
+            const u64 nc = std::max<u64>(have + extra, 2 * s.cap);
+            DBuf<u64> nk(c_, nc);
+            if (have) FV_CUDA(cudaMemcpyAsync(nk.get(), s.keys.get(), 8 * have, cudaMemcpyDeviceToDevice, c_->stream));
+            s.keys = std::move(nk);
+            s.cap = nc;
+        }
+        u64 nw = 0, ov = 0;
+        if (r.blocks.capacity()) read_block_counters(r, s, &nw, &ov);
+        if (ov) {
+            drain_overflow(r, s, ov);
+            if (!r.block_mode) return;
+        }
+        if (s.ovf_cap < extra) {
+            s.ovf = DBuf<u64>(c_, extra);
+            s.ovf_cap = extra;
+        }
+        s.bound = nw + extra;
+        const double ratio = block_ratio_ >= 0 ? block_ratio_ : r.blocks.ratio;
+        const u64 est = std::min<u64>(extra, static_cast<u64>(double(extra) * ratio) + (block_ratio_ >= 0 ? 0 : 1024));
+        if (!block_grow(r, r.blocks.blocks + est, r.keys.count + nw)) {
+            convert_to_keyset(r, &s, nullptr, 0);
+            return;
+        }
+        s.chunk_blocks0 = r.blocks.blocks;
+        s.chunk_cands = extra;
+    }
+
+    // Replace a relation's block set by a key set holding FULL's rows plus
+    // the keys this iteration already found new (sink) and `extra` pending
+    // keys (inserted with new-key detection).
+    void convert_to_keyset(RelState& r, HeadSink* s, const u64* extra, u64 n_extra) {
+        u64 nw = s ? sink_count(*s) : 0;
+        const u64 total = r.keys.count + nw + n_extra;
+        u64 cap = u64(1) << 16;
+        while (cap < kKeysetGrowth * total) cap <<= 1;
+        KeySet ns;
+        ns.slots = DBuf<u64>(c_, cap);
+        ns.mask = cap - 1;
+        ns.limit = cap / 2;
+        ns.count = r.keys.count;
+        ns.group_bits = initial_group_bits();
+        FV_CUDA(cudaMemsetAsync(ns.slots.get(), 0xff, 8 * cap, c_->stream));
+        std::vector<const DevVersion*> full;
+        if (r.levels_mode) full = levels_of(r);
+        else full.push_back(&r.full);
+        const u64 chunk = u64(1) << 27;
+        for (const DevVersion* v : full) {
+            for (u64 off = 0; off < v->n; off += chunk) {
+                const u64 m = std::min(chunk, v->n - off);
+                DBuf<u64> k(c_, m);
+                std::vector<const u32*> cols;
+                for (auto& col : v->cols) cols.push_back(col.get() + off);
+                u64* kp = k.get();
+                engine_pack_keys(c_, cols, m, st_.key_shift, &kp);
+                engine_hash_insert(c_, k.get(), m, ns, nullptr, nullptr);
+            }
+        }
+        if (nw) engine_hash_insert(c_, s->keys.get(), nw, ns, nullptr, nullptr);
+        if (n_extra) engine_hash_insert(c_, extra, n_extra, ns, s->keys.get(), s->counter.get());
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   %s block set (%llu blocks, %llu rows) -> key set of %llu slots\n",
+                         r.name.c_str(), static_cast<unsigned long long>(r.blocks.blocks),
+                         static_cast<unsigned long long>(total), static_cast<unsigned long long>(cap));
+        r.keys = std::move(ns);
+        r.block_mode = false;
+        r.blocks = BlockSet();
+        if (s) s->bound = nw + n_extra;
+    }
+
     u32 initial_group_bits() const { return forced_group_ >= 0 ? static_cast<u32>(forced_group_) : 1u; }
 
     // Re-lay the key set out with `bits` (same capacity): one pass over the
@@ -958,11 +1135,20 @@ public:
     u64 hash_finalize(RelState& r, HeadSink& s, CandPool& pool) {
         if (pool.n) {
             hash_reserve(r, s, pool.n);
-            engine_hash_insert(c_, pool.words[0].get(), pool.n, r.keys, s.keys.get(), s.counter.get());
+            if (r.block_mode)
+                engine_blockset_insert(c_, pool.words[0].get(), pool.n, block_args(r), s.keys.get(), s.counter.get(),
+                                       s.ovf.get(), s.counter.get() + 1);
+            else
+                engine_hash_insert(c_, pool.words[0].get(), pool.n, r.keys, s.keys.get(), s.counter.get());
             s.candidates += pool.n;
         }
+        if (r.block_mode && s.counter.get()) {
+            u64 nw, ov;
+            read_block_counters(r, s, &nw, &ov);
+            if (ov) drain_overflow(r, s, ov);
+        }
         const u64 nd = sink_count(s);
-        if (forced_group_ < 0 && r.keys.capacity() && s.candidates) {
+        if (!r.block_mode && forced_group_ < 0 && r.keys.capacity() && s.candidates) {
             const u32 want = double(s.candidates) <= group_ratio_ * double(std::max<u64>(nd, 1)) ? 1u : 0u;
             if (trace_)
                 std::fprintf(stderr, "[fvlog]   %s candidates/new = %.3f\n", r.name.c_str(),
@@ -1068,6 +1254,32 @@ private:
         const char* e = std::getenv("FVLOG_GROW");
         return !(e && std::string(e) == "rehash");
     }();
+    // FVLOG_SET=keyset: key sets only; =blocks: block sets even when sparse.
+    const int force_blocks_ = [] {
+        const char* e = std::getenv("FVLOG_SET");
+        return e ? (std::string(e) == "blocks" ? 1 : 0) : -1;
+    }();
+    // Tests: FVLOG_BLOCK_RATIO fixes the new-blocks-per-candidate estimate
+    // (0 provokes overflow lists), FVLOG_BLOCK_SPARSE_BYTES the directory
+    // size below which a sparse relation keeps its block set.
+    const double block_ratio_ = [] {
+        const char* e = std::getenv("FVLOG_BLOCK_RATIO");
+        return e ? std::atof(e) : -1.0;
+    }();
+    const double block_sparse_bytes_ = [] {
+        const char* e = std::getenv("FVLOG_BLOCK_SPARSE_BYTES");
+        return e ? std::atof(e) : kBlockSparseMinBytes;
+    }();
+    // FVLOG_BLOCK_TILE_SET=0: no tile-local dedup before the block-set probe.
+    const u32 block_tile_set_ = [] {
+        const char* e = std::getenv("FVLOG_BLOCK_TILE_SET");
+        return e ? static_cast<u32>(std::atoi(e) != 0) : 1u;
+    }();
+
+public:
+    bool blocks_enabled() const { return force_blocks_ != 0; }
+
+private:
     u32 world_ = 1, rank_ = 0;
 };
 
@@ -1322,6 +1534,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     for (auto& [name, r] : st->relations) {
         r->hash_mode = hash_ok && r->idb && r->arity <= 2 && (r->arity == 1 || 2 * st->key_shift < 64);
         r->levels_mode = r->hash_mode && !full_read.count(name);
+        r->block_mode = r->hash_mode && eng.blocks_enabled();
     }
 
     const bool trace = std::getenv("FVLOG_TRACE") != nullptr;

@@ -109,6 +109,37 @@ struct KeySet {
     u64 capacity() const { return slots.size(); }
 };
 
+// Blocked-bitmap set of packed row keys (binary or unary relations): the
+// relation's (a, b) value grid cut into 32 x 32-bit blocks, one 128-byte
+// bitmap per non-empty block (row a & 31 is the word, b & 31 the bit; unary:
+// 1024 consecutive values). A directory (open addressing, empty = all ones,
+// load <= 1/2) maps block ids to slots; bits[32 * slot ...] is that block's
+// bitmap. Relations whose tuples cluster in id space (components, trees,
+// dense closures) take a fraction of a byte per tuple instead of the key
+// set's 16-32, so a fixpoint's whole FULL fits in L2 and a membership test +
+// insert is one L2 atomic instead of a random DRAM line. The engine falls
+// back to a KeySet when a relation turns out sparse (< kBlockMinDensity
+// tuples per block).
+struct BlockSet {
+    DBuf<u64> dir;
+    DBuf<u32> bits;
+    DBuf<u64> count;  // device: blocks claimed
+    u64 mask = 0;
+    u64 blocks = 0;   // host copy of `count` (last read)
+    double ratio = 0.0;  // new blocks per candidate, recent maximum (growth estimate)
+    u64 capacity() const { return dir.size(); }
+};
+
+// Device view of a BlockSet (kernel argument).
+struct BlockSetArgs {
+    u64* dir = nullptr;
+    u32* bits = nullptr;
+    u64 mask = 0;
+    u64* count = nullptr;
+    u64 limit = 0;  // no new block is claimed once `count` reaches this
+    u32 shift = 0, arity = 2;
+};
+
 // A partition copy of a relation keyed on a column other than 0 (partitioned
 // evaluation only): the rows whose owner(hash(row[col])) is this rank.
 struct RelCopy {
@@ -137,6 +168,10 @@ struct RelState {
     // inserted straight from the join kernel; only new rows get sorted.
     bool hash_mode = false;
     KeySet keys;
+    // Hash mode with a BlockSet instead of `keys` (keys.count still counts
+    // FULL's rows); cleared when the relation proves sparse.
+    bool block_mode = false;
+    BlockSet blocks;
     // With hash dedup, a FULL no join reads is kept as levels: the past DELTAs
     // (one per iteration, grouped by column 0) plus the current `delta`,
     // concatenated and sorted only for dumps; otherwise it is `full`, merged
@@ -268,11 +303,28 @@ struct OutSpec {
     // Key mode, one word, no key set: drop tile-local repeats and append the
     // tile's distinct keys at keys[0][*d_count ...].
     u32 tile_dedup = 0;
+    // Block-set dedup (bs.dir != null, ht_slots null): insert into the
+    // relation's BlockSet; candidates it cannot place (claim limit reached,
+    // probe run too long) are appended to ovf_keys[*ovf_count ...] for the
+    // host to insert after growing the directory.
+    BlockSetArgs bs;
+    u64* ovf_keys = nullptr;
+    u64* ovf_count = nullptr;
 };
+
+FV_HD inline bool fused_set(const OutSpec& s) { return s.ht_slots != nullptr || s.bs.dir != nullptr; }
 
 // Insert n keys; the ones not yet present are appended to
 // new_keys[*d_new ...] (device counter, not reset here).
 void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_keys, u64* d_new);
+// BlockSet: allocate `cap` (power of two) empty slots; the count starts at `blocks`.
+void engine_blockset_alloc(Ctx* c, BlockSet& s, u64 cap, u64 blocks);
+// Move every block of `from` into the freshly allocated `to` (bitmaps copied whole).
+void engine_blockset_grow(Ctx* c, const BlockSet& from, BlockSet& to);
+// Insert n keys; new ones are appended to new_keys[*d_new ...] (when
+// new_keys), unplaceable ones to ovf[*d_ovf ...].
+void engine_blockset_insert(Ctx* c, const u64* keys, u64 n, const BlockSetArgs& s, u64* new_keys, u64* d_new,
+                            u64* ovf, u64* d_ovf);
 // Move every key of `from` into the (emptied) `to` by scanning from's slots
 // in order: with the same layout a key's home in `to` is its old slot plus a
 // multiple of from's capacity, so the inserts stream through L2 instead of

@@ -163,6 +163,93 @@ __device__ __forceinline__ void append_new_items(u64* __restrict__ out, u64* cou
         if ((mask >> k) & 1u) out[pos++] = key[k];
 }
 
+// ---- block set (BlockSet, engine.h) ------------------------------------------------
+
+// A longer probe run sends the key to the overflow list (the host grows the
+// directory and inserts it): the loop is bounded whatever the load.
+constexpr int kBlockMaxProbes = 64;
+
+// Block id and bit position (word << 5 | bit) of a packed row key.
+__device__ __forceinline__ u64 block_of(u64 key, u32 shift, u32 arity, u32* bitpos) {
+    if (arity == 2) {
+        const u64 a = key >> shift;
+        const u64 b = key & ((u64(1) << shift) - 1);
+        *bitpos = (static_cast<u32>(a & 31) << 5) | static_cast<u32>(b & 31);
+        return ((a >> 5) << 27) | (b >> 5);
+    }
+    *bitpos = static_cast<u32>(key & 1023);
+    return key >> 10;
+}
+__device__ __forceinline__ u64 block_home(u64 bid, u64 mask) { return mix64(bid) & mask; }
+
+// Directory slot of block `bid` given the first probed slot h (holding v);
+// claims an empty slot for a new block. ~0: no slot (overflow).
+// (Arguments by value: a reference into the kernel's parameter block would
+// force the whole OutSpec into local memory.)
+__device__ __forceinline__ u64 blockset_find(u64* dir, u64 mask, u64* count, u64 limit, u64 bid, u64 h, u64 v) {
+    for (int probe = 0; probe < kBlockMaxProbes; ++probe) {
+        if (v == bid) return h;
+        if (v == kEmptySlot) {
+            if (ld_relaxed_u64(count) >= limit) return ~u64(0);
+            const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(dir + h), ~0ull,
+                                       static_cast<unsigned long long>(bid));
+            if (prev == ~0ull) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(count), 1ull);
+                return h;
+            }
+            if (prev == bid) return h;
+        }
+        h = (h + 1) & mask;
+        v = __ldcg(dir + h);
+    }
+    return ~u64(0);
+}
+
+// Set-insert of N keys (bit k of `live`: key[k] is a candidate). All
+// directory loads are issued first, then all bitmap loads, then the atomics of
+// the bits found clear (repeats of present rows never issue an atomic).
+// Returns the new mask; keys that found no slot are flagged in *ovf_mask.
+template <int N>
+__device__ __forceinline__ u32 blockset_insert_items(const BlockSetArgs& s, u32 live, const u64 (&key)[N],
+                                                     u32* ovf_mask) {
+    u64 slot[N];
+    u32 bp[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        slot[k] = 0;
+        bp[k] = 0;
+        if ((live >> k) & 1u) slot[k] = block_of(key[k], s.shift, s.arity, &bp[k]);  // bid for now
+    }
+    u64 dv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) dv[k] = ((live >> k) & 1u) ? __ldcg(s.dir + block_home(slot[k], s.mask)) : 0;
+    u32 om = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        if (!((live >> k) & 1u)) continue;
+        const u64 bid = slot[k], h = block_home(bid, s.mask);
+        const u64 f = dv[k] == bid ? h : blockset_find(s.dir, s.mask, s.count, s.limit, bid, h, dv[k]);
+        if (f == ~u64(0)) {
+            om |= 1u << k;
+            live &= ~(1u << k);
+        }
+        slot[k] = f;
+    }
+    u32 wv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) wv[k] = ((live >> k) & 1u) ? __ldcg(s.bits + slot[k] * 32 + (bp[k] >> 5)) : 0;
+    u32 nm = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        if (!((live >> k) & 1u)) continue;
+        const u32 m = 1u << (bp[k] & 31);
+        if (wv[k] & m) continue;
+        if (!(atomicOr(s.bits + slot[k] * 32 + (bp[k] >> 5), m) & m)) nm |= 1u << k;
+    }
+    *ovf_mask = om;
+    return nm;
+}
+
 // Write one output row (values computed from slots) at position pos.
 __device__ __forceinline__ void write_row(const OutSpec& spec, u64 pos, u64 i, u64 p) {
     if (spec.key_mode) {
@@ -271,7 +358,7 @@ struct MatShared {
 
 // One output tile of the output-partitioned join expansion (see lbs_kernel in
 // column_ops.cu). All threads of the block call it for the same tile.
-template <bool COMPACT, bool REMOTE>
+template <bool COMPACT, bool REMOTE, bool BLOCKS>
 __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets, u64 o_begin, u64 total,
                                                  const u32* __restrict__ starts, const u64* __restrict__ tile_jlo,
                                                  const u64* __restrict__ tile_jhi, const OutSpec& spec, u64 t,
@@ -337,7 +424,7 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
             if (!COMPACT || pass_filters(spec.f, spec.n_filters, i, p)) keep_mask |= 1u << k;
         }
     }
-    if (spec.ht_slots || spec.tile_dedup) {
+    if ((BLOCKS ? spec.bs.dir != nullptr : spec.ht_slots != nullptr) || spec.tile_dedup) {
         // Fused dedup. First a tile-local key set in shared memory drops the
         // repeats inside the tile: consecutive outputs share the probe row's
         // head columns, so one derivation per tile and key reaches HBM (about
@@ -405,6 +492,15 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
                 if (keep_mask & (1u << k)) spec.keys[0][pos++] = key[k];
             return;
         }
+        if constexpr (BLOCKS) {
+            // Block-set dedup: survivors test-and-set their bit in FULL's
+            // blocked bitmap (L2-resident for clustered relations).
+            u32 ovf_mask;
+            const u32 new_mask = blockset_insert_items(spec.bs, keep_mask, key, &ovf_mask);
+            append_new_items(spec.new_keys, spec.new_count, new_mask, key);
+            append_new_items(spec.ovf_keys, spec.ovf_count, ovf_mask, key);
+            return;
+        } else {
 #pragma unroll
         for (int k = 0; k < kMatItems; ++k) sv[k] = ((keep_mask >> k) & 1u) ? __ldcg(spec.ht_slots + hs[k]) : 0;
         constexpr bool kBatchCas = FV_MAT_BATCH_CAS == 1 || (FV_MAT_BATCH_CAS == 2 && !COMPACT);
@@ -458,6 +554,7 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
             append_new(spec.new_keys, spec.new_count, is_new, key[k]);
         }
         }
+        }
         return;
     }
     if (!COMPACT) {
@@ -492,15 +589,18 @@ constexpr int kMatGroup = 1;  // measured: 1 is best on C1-C4 (FVLOG_MAT_GROUP o
 #ifndef FV_MAT_MIN_BLOCKS
 #define FV_MAT_MIN_BLOCKS 3
 #endif
-template <bool COMPACT, bool REMOTE>
-__global__ void __launch_bounds__(kMatBlock, FV_MAT_MIN_BLOCKS) materialize_kernel(const u64* __restrict__ offsets, u64 m,
+#ifndef FV_MAT_MIN_BLOCKS_BS
+#define FV_MAT_MIN_BLOCKS_BS 2
+#endif
+template <bool COMPACT, bool REMOTE, bool BLOCKS>
+__global__ void __launch_bounds__(kMatBlock, BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_MAT_MIN_BLOCKS) materialize_kernel(const u64* __restrict__ offsets, u64 m,
                                                                  u64 o_begin, u64 total,
                                                                  const u32* __restrict__ starts,
                                                                  const u64* __restrict__ tile_jlo,
                                                                  const u64* __restrict__ tile_jhi, u64 tiles,
                                                                  u32 group, OutSpec spec) {
     __shared__ MatShared sh;
-    const bool dedup = spec.ht_slots || spec.tile_dedup;
+    const bool dedup = (BLOCKS ? spec.bs.dir != nullptr : spec.ht_slots != nullptr) || spec.tile_dedup;
     const u64 t0 = u64(blockIdx.x) * group;
     const u64 t1 = min(t0 + group, tiles);
     for (u64 t = t0; t < t1; ++t) {
@@ -512,7 +612,7 @@ __global__ void __launch_bounds__(kMatBlock, FV_MAT_MIN_BLOCKS) materialize_kern
             if (threadIdx.x == 0) sh.set_fill = 0;
             __syncthreads();
         }
-        materialize_tile<COMPACT, REMOTE>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh);
+        materialize_tile<COMPACT, REMOTE, BLOCKS>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh);
     }
 }
 
@@ -909,6 +1009,46 @@ __global__ void FV_INSERT_BOUNDS hash_insert_keys_kernel(const u64* __restrict__
     if (new_keys) append_new_items(new_keys, new_count, new_mask, key);
 }
 
+// Block-set insert of n keys (pooled candidates, seeds, routed rows): four
+// keys per thread, the same batched path as the fused join.
+__global__ void blockset_insert_kernel(const u64* __restrict__ keys, u64 n, BlockSetArgs s,
+                                       u64* __restrict__ new_keys, u64* new_count, u64* __restrict__ ovf,
+                                       u64* ovf_count) {
+    constexpr int ITEMS = 4;
+    const u64 base = u64(blockIdx.x) * blockDim.x * ITEMS + threadIdx.x;
+    u64 key[ITEMS];
+    u32 live = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 i = base + u64(k) * blockDim.x;
+        key[k] = i < n ? keys[i] : 0;
+        if (i < n) live |= 1u << k;
+    }
+    u32 om;
+    const u32 nm = blockset_insert_items(s, live, key, &om);
+    if (new_keys) append_new_items(new_keys, new_count, nm, key);
+    append_new_items(ovf, ovf_count, om, key);
+}
+
+// Directory growth: every used old slot re-homed in the new directory, its
+// 128-byte bitmap moved with 16-byte vector loads/stores. Block ids are
+// distinct, so a block only has to find an empty slot.
+__global__ void blockset_grow_kernel(const u64* __restrict__ from_dir, const u32* __restrict__ from_bits, u64 n,
+                                     BlockSetArgs to) {
+    GRID_STRIDE(i, n) {
+        const u64 bid = __ldcs(from_dir + i);
+        if (bid == kEmptySlot) continue;
+        u64 h = block_home(bid, to.mask);
+        while (atomicCAS(reinterpret_cast<unsigned long long*>(to.dir + h), ~0ull,
+                         static_cast<unsigned long long>(bid)) != ~0ull)
+            h = (h + 1) & to.mask;
+        const uint4* src = reinterpret_cast<const uint4*>(from_bits + i * 32);
+        uint4* dst = reinterpret_cast<uint4*>(to.bits + h * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = __ldcs(src + q);
+    }
+}
+
 // One tile of consecutive old slots per block (not grid-stride): blocks run
 // roughly in index order, so the inserts of all resident blocks fall into a
 // few narrow windows of the new table that stay in L2.
@@ -1253,6 +1393,42 @@ void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_ke
     c->count_launch();
 }
 
+void engine_blockset_alloc(Ctx* c, BlockSet& s, u64 cap, u64 blocks) {
+    s.dir = DBuf<u64>(c, cap);
+    s.bits = DBuf<u32>(c, cap * 32);
+    s.count = DBuf<u64>(c, 1);
+    s.mask = cap - 1;
+    s.blocks = blocks;
+    FV_CUDA(cudaMemsetAsync(s.dir.get(), 0xff, 8 * cap, c->stream));
+    FV_CUDA(cudaMemsetAsync(s.bits.get(), 0, 128 * cap, c->stream));
+    FV_CUDA(cudaMemcpyAsync(s.count.get(), &blocks, 8, cudaMemcpyHostToDevice, c->stream));
+    c->sync();  // `blocks` is a host stack value
+}
+
+void engine_blockset_grow(Ctx* c, const BlockSet& from, BlockSet& to) {
+    const u64 n = from.capacity();
+    if (!n) return;
+    BlockSetArgs a;
+    a.dir = to.dir.get();
+    a.bits = to.bits.get();
+    a.mask = to.mask;
+    ProfScope prof(c, "blockset_grow", 136.0 * double(n) + 136.0 * double(to.blocks));
+    blockset_grow_kernel<<<grid_for(n), 256, 0, c->stream>>>(from.dir.get(), from.bits.get(), n, a);
+    FV_CUDA(cudaGetLastError());
+    FV_CUDA(cudaMemcpyAsync(to.count.get(), from.count.get(), 8, cudaMemcpyDeviceToDevice, c->stream));
+    c->count_launch();
+}
+
+void engine_blockset_insert(Ctx* c, const u64* keys, u64 n, const BlockSetArgs& s, u64* new_keys, u64* d_new,
+                            u64* ovf, u64* d_ovf) {
+    if (!n) return;
+    ProfScope prof(c, "blockset_insert", 16.0 * double(n));
+    const unsigned grid = static_cast<unsigned>(ceil_div(n, u64(256) * 4));
+    blockset_insert_kernel<<<grid, 256, 0, c->stream>>>(keys, n, s, new_keys, d_new, ovf, d_ovf);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
 void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to) {
     const u64 n = from.capacity();
     if (!n) return;
@@ -1453,37 +1629,46 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
         if (spec.f[k].op != kFilterConst) (spec.f[k].b.side ? side1 : side0) += 4;
     }
     const double row_bytes = spec.key_mode ? 8.0 * ((spec.n_out + 1) / 2) : 4.0 * spec.n_out;
-    const double out_bytes = spec.ht_slots ? 2.0 * row_bytes : row_bytes;
+    const double out_bytes = fused_set(spec) ? 2.0 * row_bytes : row_bytes;
     const double frac = double(outs) / double(total);  // a chunk reads its share of the probe rows
     DBuf<u64> rows(c, 2 * tiles);
     tile_rows_kernel<<<grid_for(tiles), 256, 0, c->stream>>>(offsets, m, o_begin, o_end, tiles, rows.get(),
                                                              rows.get() + tiles);
     FV_CUDA(cudaGetLastError());
     // The fused join + key-set dedup is profiled as "join_dedup".
-    ProfScope prof(c, spec.ht_slots ? "join_dedup" : "join_materialize",
+    ProfScope prof(c, fused_set(spec) ? "join_dedup" : "join_materialize",
                    frac * double(m) * (12.0 + side0) + double(outs) * (side1 + out_bytes));
     static const u32 env_group = [] {
         const char* e = std::getenv("FVLOG_MAT_GROUP");
         return e ? static_cast<u32>(std::atoi(e)) : 0u;
     }();
-    const u32 group = (spec.ht_slots || spec.tile_dedup) ? (env_group ? env_group : u32(kMatGroup)) : 1u;
+    const u32 group = (fused_set(spec) || spec.tile_dedup) ? (env_group ? env_group : u32(kMatGroup)) : 1u;
     const unsigned grid = static_cast<unsigned>(ceil_div(tiles, group));
     const u64* jlo = rows.get();
     const u64* jhi = rows.get() + tiles;
+    // Instantiations: filtered (COMPACT), partitioned routing (REMOTE) and
+    // block-set dedup (BLOCKS) each keep their own register budget.
+#define FV_MAT_LAUNCH(C_, R_, B_)                                                                         \
+    materialize_kernel<C_, R_, B_><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, jlo, \
+                                                                       jhi, tiles, group, spec)
+    const bool blocks = spec.bs.dir != nullptr;
+    const bool cmp = spec.n_filters != 0;
     if (spec.remote_world) {
-        if (spec.n_filters)
-            materialize_kernel<true, true><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, jlo,
-                                                                             jhi, tiles, group, spec);
-        else
-            materialize_kernel<false, true><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts,
-                                                                              jlo, jhi, tiles, group, spec);
-    } else if (spec.n_filters) {
-        materialize_kernel<true, false><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, jlo,
-                                                                          jhi, tiles, group, spec);
+        if (blocks) {
+            if (cmp) FV_MAT_LAUNCH(true, true, true);
+            else FV_MAT_LAUNCH(false, true, true);
+        } else {
+            if (cmp) FV_MAT_LAUNCH(true, true, false);
+            else FV_MAT_LAUNCH(false, true, false);
+        }
+    } else if (blocks) {
+        if (cmp) FV_MAT_LAUNCH(true, false, true);
+        else FV_MAT_LAUNCH(false, false, true);
     } else {
-        materialize_kernel<false, false><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, jlo,
-                                                                           jhi, tiles, group, spec);
+        if (cmp) FV_MAT_LAUNCH(true, false, false);
+        else FV_MAT_LAUNCH(false, false, false);
     }
+#undef FV_MAT_LAUNCH
     FV_CUDA(cudaGetLastError());
     c->count_launch(2);
 }

@@ -187,12 +187,17 @@ def _large():
     return json.load(open(p)) if os.path.exists(p) else {}
 
 
-def test_sg_c3_full_size_closed_form(ctx):
+def test_sg_c3_full_size_against_reference(ctx):
     st = E.evaluate_program(W.SG_PROGRAM, {"edge": W.sg_forest(244, 10)}, ctx=ctx)
     assert st.rows("sg") == W.sg_count(244, 10) == 340_637_176
     assert st.iterations == 11
-    # SG of a forest of identical trees: every tree contributes the same rows.
     assert sum(st.delta_counts()["sg"]) == 340_637_176
+    # The tuple set itself, not just its size: fingerprint and per-iteration
+    # deltas of the unmodified reference run over the forest's disjoint trees.
+    g = _large().get("C3")
+    if g and "fingerprint" in g:
+        assert str(st.fingerprint("sg")) == g["fingerprint"]
+        assert st.delta_counts()["sg"] == g["deltas"]
 
 
 def test_sg_beyond_c3_1e9_tuples(ctx):
@@ -291,6 +296,7 @@ def test_keyset_growth_paths_match_reference(ctx, grow, monkeypatch):
     # overflow list filled up (a 1-entry list) and redone by the rehash.
     # All must give the reference's sets. C1 at full size grows its key set
     # several times (2^16 -> 2^30 slots).
+    monkeypatch.setenv("FVLOG_SET", "keyset")
     if grow == "overflow":
         monkeypatch.setenv("FVLOG_GROW_OVERFLOW_CAP", "1")
     else:
@@ -310,11 +316,40 @@ def test_keyset_growth_paths_match_reference(ctx, grow, monkeypatch):
         assert str(st.fingerprint("reach")) == g["fingerprint"]
 
 
+@pytest.mark.parametrize("setmode", [
+    {"FVLOG_SET": "keyset"},                                  # key sets only (round-1 engine)
+    {"FVLOG_SET": "blocks"},                                  # block sets, never converted
+    {"FVLOG_SET": "blocks", "FVLOG_BLOCK_RATIO": "0"},        # directory never pre-grown: overflow lists drained
+    {"FVLOG_BLOCK_SPARSE_BYTES": "0"},                        # sparse relations convert to key sets mid-run
+    {"FVLOG_BLOCK_TILE_SET": "0"},                            # no tile-local dedup before the block set
+], ids=["keyset", "blocks", "blocks-overflow", "blocks-convert", "blocks-no-tile-set"])
+def test_dedup_sets_match_reference(ctx, setmode, monkeypatch):
+    # FULL's dedup structure for binary/unary IDB relations: a BlockSet
+    # (blocked bitmap, default) or a KeySet; every path must give the
+    # reference's sets and per-iteration stats, C1 included at full size.
+    for k, v in setmode.items():
+        monkeypatch.setenv(k, v)
+    for case in load_golden("engine.json"):
+        text, facts = golden_cases.program_and_facts(case)
+        st = E.evaluate_program(text, facts, ctx=ctx)
+        got = [(s.index, s.relation, s.delta_rows, s.full_rows, s.merges) for s in st.stats()]
+        assert got == [tuple(s) for s in case["stats"]], (setmode, case["name"])
+        for rel, exp in case["relations"].items():
+            assert matches(st.dump(rel).reshape(-1), exp["dump"]), (setmode, case["name"], rel)
+    g = _large().get("C1")
+    if g:
+        st = E.evaluate_program(W.TC_PROGRAM, {"edge": W.tc_uniform(10_000, 50_000, 1)}, ctx=ctx)
+        assert st.rows("reach") == g["rows"]
+        assert st.delta_counts()["reach"] == g["deltas"]
+        assert str(st.fingerprint("reach")) == g["fingerprint"]
+
+
 @pytest.mark.parametrize("group", ["0", "1"])
 def test_keyset_layouts_match_reference(ctx, group, monkeypatch):
     # FVLOG_KEYSET_GROUP forces the key-set home layout (0: every key
     # scattered, 1: adjacent key pairs share a sector); the default picks one
     # per relation from candidates per new row. Results must not depend on it.
+    monkeypatch.setenv("FVLOG_SET", "keyset")
     monkeypatch.setenv("FVLOG_KEYSET_GROUP", group)
     for case in load_golden("engine.json"):
         if case["name"] == "TC uniform 2000/10000":
