@@ -179,6 +179,11 @@ fv_status fv_project(const fv_version* v, const uint32_t* ids, uint64_t n_ids,
 /* join_probe_phase (kernels.cpp:59-81) over host probe values. */
 fv_status fv_join_probe_phase(fv_ctx* ctx, const uint32_t* probe_values, uint64_t n,
                               const fv_column* build, fv_match** out);
+/* A MatchVector given as host arrays (ranges + matched probe positions), for
+ * callers that hold one across the phases (join_total_size, join_offsets,
+ * join_write_phase take `const MatchVector&`, P/include/colog/kernels.hpp:82-96). */
+fv_status fv_match_create(fv_ctx* ctx, const uint32_t* starts, const uint32_t* counts,
+                          const uint32_t* matched, uint64_t n, fv_match** out);
 void fv_match_free(fv_match* m);
 uint64_t fv_match_size(const fv_match* m);
 /* ranges (start,count) and matched probe positions, host out. */

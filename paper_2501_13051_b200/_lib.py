@@ -115,6 +115,7 @@ _SIGNATURES = [
     ("fv_select_eq", st, [vp, C.c_uint32, C.POINTER(vp)]),
     ("fv_project", st, [vp, u32p, C.c_uint64, u32p, C.c_uint32, C.POINTER(vp)]),
     ("fv_join_probe_phase", st, [vp, u32p, C.c_uint64, vp, C.POINTER(vp)]),
+    ("fv_match_create", st, [vp, u32p, u32p, u32p, C.c_uint64, C.POINTER(vp)]),
     ("fv_match_free", None, [vp]),
     ("fv_match_size", C.c_uint64, [vp]),
     ("fv_match_read", st, [vp, u32p, u32p, u32p]),

@@ -466,6 +466,22 @@ fv_status fv_join_probe_phase(fv_ctx* ctx, const uint32_t* probe_values, uint64_
     FV_API_END
 }
 
+fv_status fv_match_create(fv_ctx* ctx, const uint32_t* starts, const uint32_t* counts,
+                          const uint32_t* matched, uint64_t n, fv_match** out) {
+    FV_API_BEGIN(ctx)
+    FV_REQUIRE(out && ((starts && counts && matched) || n == 0), FV_ERR_INVALID, "fv_match_create: null argument");
+    auto* m = new fv_match();
+    m->ctx = ctx;
+    m->m = std::make_unique<fv::Match>();
+    m->m->ctx = ctx->c;
+    m->m->m = n;
+    m->m->starts = fv::make_dbuf(ctx->c, starts, n);
+    m->m->counts = fv::make_dbuf(ctx->c, counts, n);
+    m->m->matched = fv::make_dbuf(ctx->c, matched, n);
+    *out = m;
+    FV_API_END
+}
+
 void fv_match_free(fv_match* m) {
     if (!m) return;
     m->ctx->c->activate();
