@@ -309,12 +309,15 @@ void fv_edb_free(fv_edb* e);
 fv_status fv_evaluate_program_edb(fv_ctx* ctx, const fv_program* p, const fv_edb* edb,
                                   fv_state** out);
 /* ---- Partitioned (multi-GPU) evaluation, SURVEY.md §8e -------------------
- * IDB relations are hash-partitioned by column (home: col 0, plus copies on
- * other probed columns), EDB relations replicated; each iteration routes
- * head rows to owner(hash(col 0)) with one all-to-all, forwards new Δ rows to
- * the other copies, and all-reduces |Δ| (termination) and the stats. Every
- * rank passes the full EDB. States hold the rank's home partition; stats are
- * global. */
+ * IDB relations are hash-partitioned by a home column chosen from the
+ * recursive rules (the column a rule carries from its DELTA atom to the head;
+ * col 0 otherwise), plus copies on other probed columns; EDB relations are
+ * replicated. Derivations whose rows are already at their owner (right-linear
+ * TC: all of them) stay local; the others route head rows to
+ * owner(hash(home col)) with one all-to-all per head per iteration. New Δ rows
+ * are forwarded to the other copies, |Δ| (termination) and the stats are
+ * all-reduced. Every rank passes the full EDB. States hold the rank's home
+ * partition; stats are global. */
 fv_status fv_nccl_unique_id(void* out128);
 /* One process per GPU: later evaluations on ctx run partitioned over NCCL. */
 fv_status fv_ctx_set_nccl(fv_ctx* ctx, int rank, int world, const void* id128);
@@ -325,8 +328,9 @@ fv_status fv_evaluate_program_sharded(fv_ctx* ctx, const fv_program* p, const fv
                                       uint32_t n_facts, uint32_t world, fv_state** states_out);
 fv_status fv_state_partition(const fv_state* s, int* rank, int* world);
 /* The static partitioning decisions for a program as JSON (host only):
- * {"relations": {name: {"idb": bool, "keyset": [cols]}}, "rules": [{"src_copy":
- * [...], "shuffle": [...], "replicated_out": bool}]}. *len = full length. */
+ * {"relations": {name: {"idb": bool, "home": col, "keyset": [cols]}}, "rules":
+ * [{"src_copy": [...], "shuffle": [...], "replicated_out": bool, "local_out":
+ * bool}]}. *len = full length. */
 fv_status fv_program_partition_plan(const fv_program* p, char* buf, size_t cap, size_t* len);
 /* owner(v) = floor(hash32(v) * world / 2^32): the rank owning value v. */
 uint32_t fv_owner(uint32_t v, uint32_t world);

@@ -396,10 +396,18 @@ fv_status fv_program_partition_plan(const fv_program* p, char* buf, size_t cap, 
     std::set<std::string> idb;
     for (auto& plan : mp->plans) idb.insert(plan.head);
     std::map<std::string, std::set<u32>> keyset;
+    std::map<std::string, u32> idb_arity;
+    for (auto& r : mp->prog.relations)
+        if (idb.count(r.name)) idb_arity[r.name] = static_cast<u32>(r.arity);
+    std::vector<std::pair<const fv::Plan*, long>> variants;
+    for (auto& plan : mp->plans)
+        for (size_t s = 0; s < plan.sources.size(); ++s)
+            if (idb.count(plan.sources[s].relation)) variants.emplace_back(&plan, static_cast<long>(s));
+    const auto home = fv::choose_home_cols(variants, idb_arity);
     std::ostringstream rules;
     rules << "[";
     for (size_t i = 0; i < mp->plans.size(); ++i) {
-        const auto dp = fv::dist_plan(mp->plans[i], idb);
+        const auto dp = fv::dist_plan(mp->plans[i], idb, home);
         for (size_t s = 0; s < dp.src_copy.size(); ++s) {
             const std::string& rel = mp->plans[i].sources[s].relation;
             if (idb.count(rel)) keyset[rel].insert(dp.src_copy[s]);
@@ -408,7 +416,8 @@ fv_status fv_program_partition_plan(const fv_program* p, char* buf, size_t cap, 
         for (size_t s = 0; s < dp.src_copy.size(); ++s) rules << (s ? "," : "") << dp.src_copy[s];
         rules << "],\"shuffle\":[";
         for (size_t k = 0; k < dp.shuffle.size(); ++k) rules << (k ? "," : "") << int(dp.shuffle[k]);
-        rules << "],\"replicated_out\":" << (dp.replicated_out ? "true" : "false") << "}";
+        rules << "],\"replicated_out\":" << (dp.replicated_out ? "true" : "false")
+              << ",\"local_out\":" << (dp.local_out ? "true" : "false") << "}";
     }
     rules << "]";
     std::ostringstream os;
@@ -417,8 +426,10 @@ fv_status fv_program_partition_plan(const fv_program* p, char* buf, size_t cap, 
     for (auto& r : mp->prog.relations) {
         const bool is_idb = idb.count(r.name) > 0;
         std::set<u32> ks = keyset[r.name];
-        if (is_idb) ks.insert(0);
-        os << (first ? "" : ",") << "\"" << r.name << "\":{\"idb\":" << (is_idb ? "true" : "false") << ",\"keyset\":[";
+        const u32 h = is_idb ? home.at(r.name) : 0;
+        if (is_idb) ks.insert(h);
+        os << (first ? "" : ",") << "\"" << r.name << "\":{\"idb\":" << (is_idb ? "true" : "false")
+           << ",\"home\":" << h << ",\"keyset\":[";
         bool f2 = true;
         for (u32 k : ks) {
             os << (f2 ? "" : ",") << k;

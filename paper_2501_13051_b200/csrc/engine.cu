@@ -133,14 +133,6 @@ std::vector<const DevVersion*> levels_of(const RelState& r);
 // measured equal; 1.5 switches TC one iteration too late).
 constexpr double kGroupedRatio = 1.1;
 
-// Partition column of plan source s (the copy it is read from when its
-// relation is partitioned): the probe column of the first join for source 0,
-// the hash column of its join for the others.
-u32 copy_for_source(const Plan& p, u32 s) {
-    if (s == 0) return p.joins.empty() ? 0 : p.joins[0].left.col;
-    return p.joins[s - 1].right_col;
-}
-
 }  // namespace
 
 // Delta-first join order for one semi-naive variant (engine decision, not
@@ -218,23 +210,113 @@ bool delta_first_plan(const Plan& p, u32 d, Plan& out, std::vector<u32>* order_o
     return true;
 }
 
-DistPlan dist_plan(const Plan& p, const std::set<std::string>& idb) {
-    DistPlan d;
-    for (u32 s = 0; s < p.sources.size(); ++s)
-        d.src_copy.push_back(idb.count(p.sources[s].relation) ? copy_for_source(p, s) : 0);
-    bool repl = !idb.count(p.sources[0].relation);
-    ColRef dkey{0, copy_for_source(p, 0)};
-    for (size_t k = 0; k < p.joins.size(); ++k) {
-        const PlanJoin& jn = p.joins[k];
-        const bool rpart = idb.count(p.sources[jn.right_source].relation) > 0;
-        const bool sh = rpart && !repl && !(dkey == jn.left);
-        d.shuffle.push_back(sh ? 1 : 0);
-        if (sh || (rpart && repl)) {
-            dkey = jn.left;
-            repl = false;
+namespace {
+
+// Union-find over a plan's column references (source, col): the variable
+// classes the plan's join keys, residual and self equalities induce.
+struct VarClasses {
+    std::vector<u32> base, parent;
+    explicit VarClasses(const Plan& p) {
+        const u32 ns = static_cast<u32>(p.sources.size());
+        base.assign(ns + 1, 0);
+        for (u32 s = 0; s < ns; ++s) base[s + 1] = base[s] + p.sources[s].arity;
+        parent.resize(base[ns]);
+        for (u32 i = 0; i < parent.size(); ++i) parent[i] = i;
+        for (const PlanJoin& j : p.joins) {
+            unite(node(j.left), base[j.right_source] + j.right_col);
+            for (auto& [l, rc] : j.residual_eq) unite(node(l), base[j.right_source] + rc);
         }
+        for (u32 s = 0; s < ns; ++s)
+            for (auto& [a, b] : p.sources[s].self_eqs) unite(base[s] + a, base[s] + b);
     }
-    d.replicated_out = repl;
+    u32 node(const ColRef& r) const { return base[r.source] + r.col; }
+    u32 find(u32 x) {
+        while (parent[x] != x) x = parent[x] = parent[parent[x]];
+        return x;
+    }
+    void unite(u32 a, u32 b) { parent[find(a)] = find(b); }
+    bool same(const ColRef& a, const ColRef& b) { return find(node(a)) == find(node(b)); }
+};
+
+}  // namespace
+
+std::map<std::string, u32> choose_home_cols(const std::vector<std::pair<const Plan*, long>>& variants,
+                                            const std::map<std::string, u32>& idb_arity) {
+    std::map<std::string, u32> home;
+    for (auto& [name, a] : idb_arity) home[name] = 0;
+    const char* e = std::getenv("FVLOG_HOME_COL");
+    if (e && std::string(e) == "0") return home;
+    std::map<std::string, std::vector<u32>> score;
+    for (auto& [p, d] : variants) {
+        if (d < 0 || p->sources[d].relation != p->head) continue;
+        const u32 a = p->head_arity;
+        if (a > 2) continue;  // packed-key routing covers columns 0 and 1
+        VarClasses vc(*p);
+        auto& sc = score[p->head];
+        sc.resize(a, 0);
+        for (u32 c = 0; c < a; ++c)
+            if (vc.same(p->output_cols[c], ColRef{static_cast<u32>(d), c})) ++sc[c];
+    }
+    for (auto& [name, sc] : score) {
+        u32 best = 0;
+        for (u32 c = 1; c < sc.size(); ++c)
+            if (sc[c] > sc[best]) best = c;
+        home[name] = best;
+    }
+    return home;
+}
+
+DistPlan dist_plan(const Plan& p, const std::set<std::string>& idb, const std::map<std::string, u32>& home) {
+    DistPlan d;
+    const u32 ns = static_cast<u32>(p.sources.size());
+    d.src_copy.assign(ns, 0);
+    auto is_idb = [&](u32 s) { return idb.count(p.sources[s].relation) > 0; };
+    auto home_of = [&](const std::string& rel) {
+        auto it = home.find(rel);
+        return it == home.end() ? 0u : it->second;
+    };
+    // `key`: column references whose value the intermediate is partitioned
+    // on (every row sits on owner(value)); empty while it is replicated.
+    std::set<ColRef> key;
+    auto extend = [&](const ColRef& a, const ColRef& b) {
+        if (key.count(a)) key.insert(b);
+        else if (key.count(b)) key.insert(a);
+    };
+    if (is_idb(0)) {
+        // Co-partitioned with the first join's right atom when that is
+        // partitioned too; otherwise the home copy serves any replicated join.
+        const bool co = !p.joins.empty() && is_idb(p.joins[0].right_source);
+        d.src_copy[0] = co ? p.joins[0].left.col : home_of(p.sources[0].relation);
+        key.insert(ColRef{0, d.src_copy[0]});
+    }
+    for (u32 s = 0; s < ns && !key.empty(); ++s)
+        for (auto& [a, b] : p.sources[s].self_eqs) extend(ColRef{s, a}, ColRef{s, b});
+    for (const PlanJoin& jn : p.joins) {
+        const u32 R = jn.right_source;
+        u8 sh = 0;
+        if (is_idb(R)) {
+            if (key.empty()) {
+                // Replicated intermediate x partitioned atom: read the home
+                // copy; the result is partitioned like it.
+                d.src_copy[R] = home_of(p.sources[R].relation);
+                key.insert(ColRef{R, d.src_copy[R]});
+            } else {
+                d.src_copy[R] = jn.right_col;
+                if (!key.count(jn.left)) {
+                    sh = 1;
+                    key.clear();
+                    key.insert(jn.left);
+                }
+            }
+        }
+        d.shuffle.push_back(sh);
+        if (key.empty()) continue;
+        extend(jn.left, ColRef{R, jn.right_col});
+        for (auto& [l, rc] : jn.residual_eq) extend(l, ColRef{R, rc});
+        for (auto& [a, b] : p.sources[R].self_eqs) extend(ColRef{R, a}, ColRef{R, b});
+    }
+    d.replicated_out = key.empty();
+    d.local_out = !key.empty() && key.count(p.output_cols[home_of(p.head)]) > 0;
     return d;
 }
 
@@ -258,9 +340,11 @@ public:
     bool partitioned(const RelState& r) const { return dist() && r.idb; }
     RelState& rel(const std::string& name) { return *st_.relations.at(name); }
 
-    DevVersion& vfull(RelState& r, u32 kc) { return kc ? r.copies.at(kc)->full : r.full; }
-    DevVersion& vdelta(RelState& r, u32 kc) { return kc ? r.copies.at(kc)->delta : r.delta; }
-    IndexMap& vindexes(RelState& r, u32 kc) { return kc ? r.copies.at(kc)->indexes : r.indexes; }
+    // Copy kc of a relation: its rows partitioned on column kc (the home
+    // copy when kc is the relation's home column; always on one GPU).
+    DevVersion& vfull(RelState& r, u32 kc) { return kc != r.home ? r.copies.at(kc)->full : r.full; }
+    DevVersion& vdelta(RelState& r, u32 kc) { return kc != r.home ? r.copies.at(kc)->delta : r.delta; }
+    IndexMap& vindexes(RelState& r, u32 kc) { return kc != r.home ? r.copies.at(kc)->indexes : r.indexes; }
 
     // FULL - DELTA of the home copy (see RelState::full_old).
     DevVersion& vold(RelState& r) { return r.old_is_full ? r.full : r.full_old; }
@@ -401,7 +485,7 @@ public:
     }
 
     // Route a candidate pool to owner(head col 0).
-    void route_pool(CandPool& pool) {
+    void route_pool(CandPool& pool, u32 home) {
         const u32 W = (pool.arity + 1) / 2;
         if (pool.words.empty()) pool.words.resize(W);
         std::vector<const u64*> in;
@@ -412,10 +496,14 @@ public:
             send.emplace_back(c_, pool.n);
             outp.push_back(send.back().get());
         }
+        // Packed keys: the home column is the high half (col 0) or the low
+        // half (col 1) of a binary key, the whole word of a unary one.
+        // (choose_home_cols only picks a non-zero home for arity <= 2).
         RouteKey rk;
         rk.word = pool.words[0].get();
         rk.shift = st_.key_shift;
-        rk.hi = pool.arity >= 2 ? 1 : 0;
+        rk.hi = pool.arity >= 2 && home == 0 ? 1 : 0;
+        if (pool.arity >= 2 && home == 1) rk.mask = (u64(1) << st_.key_shift) - 1;
         std::vector<u64> cnt(world_), off(world_);
         engine_route(c_, pool.n, rk, world_, {}, {}, in, outp, cnt.data(), off.data());
         std::vector<DBuf<u64>> recv;
@@ -484,7 +572,7 @@ public:
         auto slot0 = [&](const ColRef& r) { return SlotRef{v.ver[0]->cols[r.col].get(), 0}; };
         for (auto& [ga, gb] : plan.guard_neq)
             push(spec, Filter{slot0(plan.output_cols[ga]), slot0(plan.output_cols[gb]), kFilterNeq, 0});
-        if (v.D && dp.replicated_out) push(spec, owner_filter(slot0(plan.output_cols[0])));
+        if (v.D && dp.replicated_out) push(spec, owner_filter(slot0(plan.output_cols[rel(plan.head).home])));
         spec.key_mode = 1;
         spec.n_out = plan.head_arity;
         for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot0(plan.output_cols[h]);
@@ -526,7 +614,7 @@ public:
             build_index_on(*v.ver[R], jn.right_col, *tmp, &plan.sources[R]);
             idx = tmp.get();
         } else {
-            idx = &index(rr, rpart ? jn.right_col : 0, v.which[R], jn.right_col);
+            idx = &index(rr, rpart ? dp.src_copy[R] : 0, v.which[R], jn.right_col);
         }
         if (!D && idx->rows->n == 0) return;
         const u64 n = cur.n;
@@ -559,7 +647,7 @@ public:
         if (last) {
             for (auto& [ga, gb] : plan.guard_neq)
                 push(spec, Filter{slot_of(plan.output_cols[ga]), slot_of(plan.output_cols[gb]), kFilterNeq, 0});
-            if (D && dp.replicated_out) push(spec, owner_filter(slot_of(plan.output_cols[0])));
+            if (D && dp.replicated_out) push(spec, owner_filter(slot_of(plan.output_cols[rel(plan.head).home])));
             spec.key_mode = 1;
             spec.n_out = plan.head_arity;
             for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot_of(plan.output_cols[h]);
@@ -576,13 +664,14 @@ public:
                 }
                 // Partitioned: rows owned here are deduplicated in this
                 // kernel, the others are pooled for the all-to-all.
-                const bool route = D && !dp.replicated_out;
+                const bool route = D && !dp.replicated_out && !dp.local_out;
                 if (route) {
                     out.reserve(c_, T);
                     spec.keys[0] = out.words[0].get() + out.n;
                     spec.d_count = c_->d_scalars + 26;
                     spec.remote_world = world_;
                     spec.remote_rank = rank_;
+                    spec.remote_col = hr.home;
                     FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
                 }
                 // A chunk's outputs bound the keys it can add to the local
@@ -821,12 +910,12 @@ public:
     // when partitioned).
     void seed_copy(RelState& r, const DevVersion& v, u32 kc) {
         CandPool pool = seed_pool(r, v, kc);
-        if (kc == 0 && r.hash_mode) {
+        if (kc == r.home && r.hash_mode) {
             HeadSink sink;
             hash_finalize(r, sink, pool);
             return;
         }
-        dedup_merge(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool, kc == 0 ? &r : nullptr);
+        dedup_merge(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool, kc == r.home ? &r : nullptr);
     }
 
     CandPool seed_pool(RelState& r, const DevVersion& v, u32 kc) {
@@ -858,7 +947,7 @@ public:
     // Forward the new home Δ rows to the relation's other partition copies.
     void forward_delta(RelState& r) {
         for (u32 kc : r.keyset) {
-            if (kc == 0) continue;
+            if (kc == r.home) continue;
             std::vector<const u32*> in;
             std::vector<DBuf<u32>> send;
             std::vector<u32*> outp;
@@ -1485,18 +1574,25 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
                     std::vector<u8> old_src(order.size());
                     for (size_t i = 0; i < order.size(); ++i) old_src[i] = old_by_rule[order[i]];
                     reordered.push_back(std::move(rp));
-                    dplans.push_back(dist_plan(reordered.back(), idb));
-                    variants.push_back({&reordered.back(), 0, dplans.size() - 1, std::move(old_src)});
+                    variants.push_back({&reordered.back(), 0, variants.size(), std::move(old_src)});
                 } else {
-                    dplans.push_back(dist_plan(p, idb));
-                    variants.push_back({&p, static_cast<long>(s), dplans.size() - 1, old_by_rule});
+                    variants.push_back({&p, static_cast<long>(s), variants.size(), old_by_rule});
                 }
                 any = true;
             }
-        if (!any) {
-            dplans.push_back(dist_plan(p, idb));
-            variants.push_back({&p, -1, dplans.size() - 1, {}});
-        }
+        if (!any) variants.push_back({&p, -1, variants.size(), {}});
+    }
+    // Partitioned runs: home columns from the executed variants, then each
+    // variant's static partitioning decisions.
+    {
+        std::map<std::string, u32> idb_arity;
+        for (auto& [name, r] : st->relations)
+            if (r->idb) idb_arity[name] = r->arity;
+        std::vector<std::pair<const Plan*, long>> pv;
+        for (auto& v : variants) pv.emplace_back(v.plan, v.delta_source);
+        const std::map<std::string, u32> home = eng.dist() ? choose_home_cols(pv, idb_arity) : std::map<std::string, u32>();
+        for (auto& [name, col] : home) st->relations.at(name)->home = col;
+        for (auto& v : variants) dplans.push_back(dist_plan(*v.plan, idb, home));
     }
     for (auto& v : variants)
         for (size_t s = 0; s < v.plan->sources.size(); ++s) {
@@ -1507,7 +1603,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     // Partition copies each IDB relation needs (static in the executed variant plans).
     if (eng.dist()) {
         for (auto& [name, r] : st->relations)
-            if (r->idb) r->keyset.insert(0);
+            if (r->idb) r->keyset.insert(r->home);
         for (auto& v : variants) {
             const Plan& p = *v.plan;
             const DistPlan& dp = dplans[v.plan_index];
@@ -1518,7 +1614,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         }
         for (auto& [name, r] : st->relations)
             for (u32 kc : r->keyset)
-                if (kc != 0) {
+                if (kc != r->home) {
                     auto cp = std::make_unique<RelCopy>();
                     cp->full.cols.resize(r->arity);
                     cp->delta.cols.resize(r->arity);
@@ -1578,7 +1674,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         std::vector<u64> counts;  // per head: |Δ|, |FULL| (local, then global)
         for (auto& [name, pool] : pooled) {
             RelState& r = *st->relations.at(name);
-            if (eng.dist()) eng.route_pool(pool);
+            if (eng.dist()) eng.route_pool(pool, r.home);
             const u64 nd = r.hash_mode ? eng.hash_finalize(r, sinks[name], pool) : eng.dedup_merge_home(r, pool);
             if (eng.dist()) eng.forward_delta(r);
             counts.push_back(nd);

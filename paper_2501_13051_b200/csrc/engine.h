@@ -151,7 +151,8 @@ struct RelState {
     std::string name;
     u32 arity = 0;
     bool idb = false;
-    // Home copy: all rows (single GPU) or the rows owned by hash(col 0).
+    // Home copy: all rows (single GPU) or the rows owned by hash(col home).
+    u32 home = 0;
     DevVersion full, delta;
     // FULL before the last merge (= FULL minus DELTA), kept when some variant
     // reads it (exactly-once semi-naive variants); old_is_full when the last
@@ -161,7 +162,8 @@ struct RelState {
     DevVersion full_old;
     // (0 = full, 1 = delta, col) -> index; invalidated when the version changes
     IndexMap indexes;
-    // Partitioned evaluation: extra copies keyed on other probed columns.
+    // Partitioned evaluation: extra copies keyed on other probed columns
+    // (never on `home`: the home copy is full/delta above).
     std::map<u32, std::unique_ptr<RelCopy>> copies;
     std::set<u32> keyset;  // partition columns this relation is needed on
     // Hash dedup (arity <= 2): the key set of the home FULL. Candidates are
@@ -228,17 +230,33 @@ std::vector<std::unique_ptr<EvalState>> evaluate_sharded(Ctx* c, u32 world, cons
                                                          const std::vector<Plan>& plans,
                                                          const std::vector<FactsBlock>& facts);
 
+// Home partition column per IDB relation (partitioned evaluation): the
+// column the relation's home copy (key set / levels / sorted FULL) is hash-
+// partitioned on. Chosen from the recursive variants: the column whose
+// variable the rule carries unchanged from its DELTA atom to the head — for
+// right-linear TC, reach(x, z) :- edge(x, y), reach(y, z), column 1 (z): every
+// head row is then derived on the rank that owns it, and no candidate crosses
+// the interconnect. Relations of arity > 2 and relations with no such column
+// use column 0. FVLOG_HOME_COL=0 forces column 0 everywhere.
+// `variants`: (plan, delta source) of every executed variant.
+std::map<std::string, u32> choose_home_cols(const std::vector<std::pair<const Plan*, long>>& variants,
+                                            const std::map<std::string, u32>& idb_arity);
+
 // Static partitioning decisions for one rule plan (partitioned evaluation):
 //   src_copy[s]      partition column source s is read from (IDB sources)
 //   shuffle[k]       shuffle the intermediate by joins[k].left before step k
 //   replicated_out   the derivation only touches replicated (EDB) relations:
 //                    its head rows are owner-filtered instead of routed
+//   local_out        the intermediate is partitioned on the variable of the
+//                    head's home column: every head row is already at its
+//                    owner (no routing, no filter)
 struct DistPlan {
     std::vector<u32> src_copy;
     std::vector<u8> shuffle;
     bool replicated_out = false;
+    bool local_out = false;
 };
-DistPlan dist_plan(const Plan& p, const std::set<std::string>& idb);
+DistPlan dist_plan(const Plan& p, const std::set<std::string>& idb, const std::map<std::string, u32>& home);
 
 // Validate plan structure against the declarations (throws FV_ERR_PLAN).
 void check_plans(const std::vector<RelationDecl>& decls, const std::vector<Plan>& plans);
@@ -300,6 +318,7 @@ struct OutSpec {
     // remote_rank are appended to keys[0][*d_count ...] (to be routed)
     // instead of probing the local key set. remote_world = 0: all local.
     u32 remote_world = 0, remote_rank = 0;
+    u32 remote_col = 0;  // head column whose owner decides (the home column)
     // Key mode, one word, no key set: drop tile-local repeats and append the
     // tile's distinct keys at keys[0][*d_count ...].
     u32 tile_dedup = 0;
@@ -389,9 +408,10 @@ u64 engine_fingerprint(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 a
 // or the high/low half of a packed key word.
 struct RouteKey {
     const u32* col = nullptr;   // u32 column, or
-    const u64* word = nullptr;  // packed key word: v = hi ? word >> shift : word
+    const u64* word = nullptr;  // packed key word: v = hi ? word >> shift : word & mask
     u32 shift = 0;
     u32 hi = 0;
+    u64 mask = ~u64(0);
 };
 // Group n rows by destination rank: u32 columns `c32` and u64 columns `c64`
 // are scattered into the matching *_out buffers (capacity n) so that rows for

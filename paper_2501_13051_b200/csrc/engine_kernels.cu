@@ -464,8 +464,10 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
 #pragma unroll
             for (int k = 0; k < kMatItems; ++k) {
                 if ((keep_mask >> k) & 1u) {
-                    const u32 c0 = static_cast<u32>(spec.n_out >= 2 ? key[k] >> spec.shift : key[k]);
-                    if (static_cast<u32>((static_cast<u64>(hash32(c0)) * spec.remote_world) >> 32) != spec.remote_rank)
+                    const u32 hv = static_cast<u32>(spec.n_out < 2 ? key[k]
+                                                    : spec.remote_col ? key[k] & ((u64(1) << spec.shift) - 1)
+                                                                      : key[k] >> spec.shift);
+                    if (static_cast<u32>((static_cast<u64>(hash32(hv)) * spec.remote_world) >> 32) != spec.remote_rank)
                         remote_mask |= 1u << k;
                 }
             }
@@ -1329,7 +1331,7 @@ constexpr u32 kGroupMaxPerValue = 512;  // ... and at most this many keys per va
 __device__ __forceinline__ u32 route_dest(const RouteKey& k, u64 i, u32 world) {
     u32 v;
     if (k.col) v = k.col[i];
-    else v = static_cast<u32>(k.hi ? (k.word[i] >> k.shift) : k.word[i]);
+    else v = static_cast<u32>(k.hi ? (k.word[i] >> k.shift) : (k.word[i] & k.mask));
     return static_cast<u32>((static_cast<u64>(hash32(v)) * world) >> 32);
 }
 

@@ -47,6 +47,7 @@ def simulate(text, facts, rank, world):
     arity = dict(prog.relations())
     idb = {p.head_relation for p in plans}
     own = lambda v: E.owner(int(v), world)  # noqa: E731
+    home_col = {rel: pp["relations"][rel]["home"] for rel in idb}
     state = {}
     for rel, a in arity.items():
         rows = {tuple(int(x) for x in r) for r in np.asarray(facts.get(rel, np.zeros((0, a))), np.int64).reshape(-1, a)}
@@ -99,20 +100,25 @@ def simulate(text, facts, rank, world):
                 if any(vals[a] == vals[b] for a, b in p.guard_neq):
                     continue
                 head = tuple(vals[: p.head_arity])
-                if dp["replicated_out"] and own(head[0]) != rank:
+                h = home_col[p.head_relation]
+                if dp["replicated_out"] and own(head[h]) != rank:
                     continue
+                if dp["local_out"]:
+                    # the plan claims the row was derived at its owner
+                    assert own(head[h]) == rank, (p.head_relation, head)
                 pooled[p.head_relation].append(head)
         counts = []
         for rel in sorted(pooled):
             b = [[] for _ in range(world)]
+            h = home_col[rel]
             for row in pooled[rel]:
-                b[own(row[0])].append(row)
-            home = state[rel][0]
+                b[own(row[h])].append(row)
+            home = state[rel][h]
             new = set(_alltoall(b, world)) - home["full"]
             home["full"] |= new
             home["delta"] = new
             for kc in pp["relations"][rel]["keyset"]:
-                if kc == 0:
+                if kc == h:
                     continue
                 b = [[] for _ in range(world)]
                 for row in new:
@@ -130,7 +136,7 @@ def simulate(text, facts, rank, world):
         if not any(g[0::2]):
             break
         it += 1
-    home = {rel: sorted(st[0]["full"]) for rel, st in state.items() if rel in idb}
+    home = {rel: sorted(st[home_col[rel]]["full"]) for rel, st in state.items() if rel in idb}
     return {"iterations": it + 1, "stats": stats, "home": home}
 
 
@@ -138,7 +144,11 @@ def _worker(rank, world, port, cases, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        q.put((rank, [simulate(text, facts, rank, world) for _, text, facts in cases]))
+        try:
+            q.put((rank, [simulate(text, facts, rank, world) for _, text, facts in cases]))
+        except Exception as e:  # noqa: BLE001 — reported by the parent
+            import traceback
+            q.put((rank, "".join(traceback.format_exception(e))))
     finally:
         dist.destroy_process_group()
 
@@ -169,6 +179,8 @@ def test_partitioned_protocol_gloo_world2():
     for p in procs:
         p.start()
     results = dict(q.get(timeout=600) for _ in range(world))
+    for r, res in results.items():
+        assert not isinstance(res, str), f"rank {r}: {res}"
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -187,3 +199,21 @@ def test_partitioned_protocol_gloo_world2():
             assert not set(rows0) & set(rows1), (name, rel)  # disjoint home partitions
             exp = {tuple(int(x) for x in r) for r in rels[names.index(rel)].tolist()}
             assert set(rows0) | set(rows1) == exp, (name, rel)
+
+
+def test_home_columns_make_tc_exchange_free():
+    """The planner's home column for right-linear TC is column 1 and its
+    recursive rule is local_out (no routing); left-linear TC keeps column 0,
+    also local; SG has no carried column and routes (column 0)."""
+    sys.path.insert(0, ROOT)
+    from paper_2501_13051_b200 import engine as E, workloads as W
+    pp = E.compile_program(W.TC_PROGRAM).partition_plan()
+    assert pp["relations"]["reach"]["home"] == 1
+    assert pp["relations"]["reach"]["keyset"] == [1]  # no partition copies
+    assert all(r["local_out"] or r["replicated_out"] for r in pp["rules"])
+    left = E.compile_program("reach(x, y) :- edge(x, y).\nreach(x, z) :- reach(x, y), edge(y, z).\n")
+    pl = left.partition_plan()
+    assert pl["relations"]["reach"]["home"] == 0 and pl["rules"][1]["local_out"]
+    sg = E.compile_program(W.SG_PROGRAM).partition_plan()
+    assert sg["relations"]["sg"]["home"] == 0
+    assert any(not r["local_out"] and not r["replicated_out"] for r in sg["rules"])

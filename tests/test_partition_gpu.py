@@ -51,7 +51,12 @@ def _check(single, shards, text):
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_sharded_equals_single_gpu(ctx, world):
+@pytest.mark.parametrize("home", ["rules", "col0"])
+def test_sharded_equals_single_gpu(ctx, world, home, monkeypatch):
+    # "rules": home columns chosen from the recursive rules (TC: col 1,
+    # exchange-free); "col0": every IDB relation homed on column 0 (routed).
+    if home == "col0":
+        monkeypatch.setenv("FVLOG_HOME_COL", "0")
     for name, text, facts in CASES:
         single = E.evaluate_program(text, facts, ctx=ctx)
         shards = E.evaluate_program_sharded(text, facts, world, ctx=ctx)
@@ -108,3 +113,58 @@ def test_nccl_transport_single_rank(monkeypatch):
         single = E.evaluate_program(text, facts, ctx=plain)
         part = E.evaluate_program(text, facts, ctx=ctx)
         _check(single, [part], name)
+
+
+def _nccl_rank(rank, world, uid, cases, q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        from paper_2501_13051_b200 import colog, engine as E2
+        ctx = colog.Context(rank)
+        E2.set_nccl(ctx, rank, world, uid)
+        out = []
+        for name, text, facts in cases:
+            st = E2.evaluate_program(text, facts, ctx=ctx)
+            out.append({rel: st.dump(rel) for rel in st.relations()} | {
+                "__stats": [(s.index, s.relation, s.delta_rows, s.full_rows) for s in st.stats()],
+                "__iterations": st.iterations})
+        q.put((rank, out))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        q.put((rank, "".join(traceback.format_exception(e))))
+
+
+def test_nccl_two_processes(ctx):
+    """Two processes, one GPU each, one NCCL communicator: the real multi-GPU
+    path (routing all-to-alls over NVLink, Δ forwarding, all-reduced stats).
+    The union of the two home partitions must equal the single-GPU result."""
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    world = 2
+    uid = E.nccl_unique_id()
+    cases = [c for c in CASES if c[0] in ("TC uniform", "SG tree", "CSPA", "LUBM", "probe on col 1")]
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    procs = [mpc.Process(target=_nccl_rank, args=(r, world, uid, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=900) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for r, v in res.items():
+        assert not isinstance(v, str), f"rank {r}: {v}"
+    for k, (name, text, facts) in enumerate(cases):
+        single = E.evaluate_program(text, facts, ctx=ctx)
+        stats = [(s.index, s.relation, s.delta_rows, s.full_rows) for s in single.stats()]
+        idb = {s.relation for s in single.stats()}
+        for r in range(world):
+            assert res[r][k]["__stats"] == stats and res[r][k]["__iterations"] == single.iterations, name
+        for rel in single.relations():
+            if rel not in idb:
+                continue
+            got = np.concatenate([res[r][k][rel] for r in range(world)])
+            got = got[np.lexsort(got.T[::-1])] if got.size else got
+            assert np.array_equal(got, single.dump(rel)), (name, rel)
