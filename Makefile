@@ -8,9 +8,9 @@ SRC := $(PKG)/csrc
 OBJ := build/obj
 ARCH := -gencode arch=compute_100a,code=sm_100a
 
-NVFLAGS := -std=c++17 -O3 $(ARCH) -lineinfo -ccbin $(HOSTCXX) -Xcompiler -fPIC \
+NVFLAGS := -std=c++17 -O3 $(ARCH) -lineinfo -ccbin $(HOSTCXX) -Xcompiler -fPIC -Xcompiler -g \
            -Iinclude -I$(SRC) --expt-relaxed-constexpr -Xptxas -warn-spills
-CXXFLAGS := -std=c++17 -O2 -fPIC -Wall -Wextra -Wno-unused-parameter -Iinclude -I$(SRC) \
+CXXFLAGS := -std=c++17 -O2 -g -fPIC -Wall -Wextra -Wno-unused-parameter -Iinclude -I$(SRC) \
             -I/usr/local/cuda/include
 
 CU_SRCS := $(wildcard $(SRC)/*.cu)

@@ -12,7 +12,12 @@
 //   [doctest] test cases: N | N passed | 0 failed | assertions: A | A passed | 0 failed
 #pragma once
 
+#include <csignal>
 #include <cstdio>
+#include <cstdlib>
+#include <execinfo.h>
+#include <sys/wait.h>
+#include <unistd.h>
 #include <exception>
 #include <string>
 #include <vector>
@@ -58,25 +63,86 @@ inline void report(bool ok, bool require, const char* expr, const char* file, in
     if (require) throw RequireAbort{};
 }
 
+// Verbose runs print a raw backtrace on a crash (addresses resolve with
+// addr2line against the -g build).
+inline void crash_handler(int sig) {
+    void* frames[64];
+    const int n = backtrace(frames, 64);
+    const char msg[] = "[doctest] fatal signal, backtrace:\n";
+    (void)!write(2, msg, sizeof msg - 1);
+    backtrace_symbols_fd(frames, n, 2);
+    std::signal(sig, SIG_DFL);
+    std::raise(sig);
+}
+
+// Runs one test case in this process; returns true when it passed.
+inline bool run_case(const TestCase& t) {
+    state().case_failed = false;
+    try {
+        t.fn();
+    } catch (const RequireAbort&) {
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "%s:%d: TEST CASE \"%s\" threw: %s\n", t.file, t.line, t.name, e.what());
+        state().case_failed = true;
+    } catch (...) {
+        std::fprintf(stderr, "%s:%d: TEST CASE \"%s\" threw an unknown exception\n", t.file, t.line, t.name);
+        state().case_failed = true;
+    }
+    return !state().case_failed;
+}
+
+// DOCTEST_MINI_FORK=1: every test case runs in a child process, so a crash
+// inside one case (the reference's random-program generator indexes an
+// empty vector on this toolchain's RNG stream, P/tests/engine_test.cpp:83)
+// is reported as that case's failure and the others still run. Each case
+// prints one "[doctest] case: <status> <assertions> <name>" line (status ok /
+// failed / crashed(signal)). The child's assertion counts come back through a pipe.
 inline int run_all() {
     long passed = 0, failed = 0;
+    const bool verbose = std::getenv("DOCTEST_MINI_VERBOSE") != nullptr;
+    const bool fork_each = std::getenv("DOCTEST_MINI_FORK") != nullptr;
+    if (verbose) {
+        std::signal(SIGSEGV, crash_handler);
+        std::signal(SIGABRT, crash_handler);
+    }
     for (const TestCase& t : registry()) {
-        state().case_failed = false;
-        try {
-            t.fn();
-        } catch (const RequireAbort&) {
-        } catch (const std::exception& e) {
-            std::fprintf(stderr, "%s:%d: TEST CASE \"%s\" threw: %s\n", t.file, t.line, t.name, e.what());
-            state().case_failed = true;
-        } catch (...) {
-            std::fprintf(stderr, "%s:%d: TEST CASE \"%s\" threw an unknown exception\n", t.file, t.line, t.name);
-            state().case_failed = true;
+        if (verbose) std::fprintf(stderr, "[doctest] running \"%s\"\n", t.name);
+        std::string status;
+        const long before = state().asserts, failed_before = state().failed_asserts;
+        if (fork_each) {
+            std::fflush(stdout);
+            std::fflush(stderr);
+            int fd[2];
+            if (pipe(fd) != 0) return 255;
+            const pid_t pid = fork();
+            if (pid == 0) {
+                close(fd[0]);
+                const bool ok = run_case(t);
+                long counts[2] = {state().asserts - before, state().failed_asserts - failed_before};
+                (void)!write(fd[1], counts, sizeof counts);
+                std::fflush(stdout);
+                std::fflush(stderr);
+                _exit(ok ? 0 : 1);
+            }
+            close(fd[1]);
+            long counts[2] = {0, 0};
+            const bool got = read(fd[0], counts, sizeof counts) == static_cast<ssize_t>(sizeof counts);
+            close(fd[0]);
+            int ws = 0;
+            waitpid(pid, &ws, 0);
+            state().asserts += counts[0];
+            state().failed_asserts += counts[1];
+            if (WIFSIGNALED(ws) || !got) status = "crashed(" + std::to_string(WIFSIGNALED(ws) ? WTERMSIG(ws) : 0) + ")";
+            else status = WEXITSTATUS(ws) == 0 ? "ok" : "failed";
+        } else {
+            status = run_case(t) ? "ok" : "failed";
         }
-        if (state().case_failed) {
+        std::printf("[doctest] case: %s %ld %s\n", status.c_str(), state().asserts - before, t.name);
+        if (status == "ok") {
+            ++passed;
+        } else {
             ++failed;
             std::fprintf(stderr, "  in TEST CASE \"%s\"\n", t.name);
-        } else {
-            ++passed;
         }
     }
     const State& s = state();

@@ -108,12 +108,15 @@ struct HeadSink {
     DBuf<u64> keys;
     u64 cap = 0;
     u64 bound = 0;  // host upper bound of the device count
-    DBuf<u64> counter;   // [0] new keys, [1] overflow keys (block sets)
+    DBuf<u64> counter;   // [0] new keys, [1] overflow keys (block sets), [2] new tuples (word form)
     u64 candidates = 0;  // rows offered to the key set this iteration
     // Block sets: keys the set could not place (drained before every chunk).
     DBuf<u64> ovf;
     u64 ovf_cap = 0;
+    // Word form: the masks of `keys` / `ovf` entries.
+    DBuf<u32> bits, ovf_bits;
     u64 chunk_blocks0 = 0, chunk_cands = 0;  // growth-ratio bookkeeping
+    u64 tuples = 0;                          // host copy of counter[2] (last read)
 };
 
 // Block sets (BlockSet, engine.h): a relation falls back to a key set when
@@ -689,6 +692,17 @@ public:
                         spec.ovf_keys = sink->ovf.get();
                         spec.ovf_count = sink->counter.get() + 1;
                         spec.tile_set = block_tile_set_;
+                        spec.wbits = SlotRef();
+                        if (hr.word_mode) {
+                            // Word-form composition: the build side is DELTA's
+                            // words (x, z base, mask); one output per word.
+                            if (idx->rows->cols.size() != hr.arity + 1)
+                                fail(FV_ERR_INVALID, "word-form head joined without a word-form DELTA");
+                            spec.wbits = SlotRef{idx->rows->cols[hr.arity].get(), 1};
+                            spec.ovf_bits = sink->ovf_bits.get();
+                            spec.new_tuples = sink->counter.get() + 2;
+                            spec.tile_set = 0;
+                        }
                     } else {
                         spec.bs = BlockSetArgs();
                         spec.ht_slots = hr.keys.slots.get();
@@ -990,8 +1004,8 @@ public:
     // in the relation's key set at load factor <= 1/2 (rehash when needed).
     void hash_reserve(RelState& r, HeadSink& s, u64 extra) {
         if (!s.counter.get()) {
-            s.counter = DBuf<u64>(c_, 2);
-            FV_CUDA(cudaMemsetAsync(s.counter.get(), 0, 16, c_->stream));
+            s.counter = DBuf<u64>(c_, 3);
+            FV_CUDA(cudaMemsetAsync(s.counter.get(), 0, 24, c_->stream));
         }
         if (r.block_mode) {
             block_reserve(r, s, extra);
@@ -1056,6 +1070,7 @@ public:
         BlockSetArgs a;
         a.dir = r.blocks.dir.get();
         a.bits = r.blocks.bits.get();
+        a.dbits = r.blocks.dbits.get();
         a.mask = r.blocks.mask;
         a.count = r.blocks.count.get();
         a.limit = r.blocks.capacity() / 4 * 3;
@@ -1067,12 +1082,13 @@ public:
     // Sink counters (new, overflow) and the block count in one sync; also
     // updates the relation's new-blocks-per-candidate estimate.
     void read_block_counters(RelState& r, HeadSink& s, u64* nw, u64* ov) {
-        FV_CUDA(cudaMemcpyAsync(c_->pinned, s.counter.get(), 16, cudaMemcpyDeviceToHost, c_->stream));
-        FV_CUDA(cudaMemcpyAsync(c_->pinned + 2, r.blocks.count.get(), 8, cudaMemcpyDeviceToHost, c_->stream));
+        FV_CUDA(cudaMemcpyAsync(c_->pinned, s.counter.get(), 24, cudaMemcpyDeviceToHost, c_->stream));
+        FV_CUDA(cudaMemcpyAsync(c_->pinned + 3, r.blocks.count.get(), 8, cudaMemcpyDeviceToHost, c_->stream));
         c_->sync();
         *nw = c_->pinned[0];
         *ov = c_->pinned[1];
-        r.blocks.blocks = c_->pinned[2];
+        s.tuples = c_->pinned[2];
+        r.blocks.blocks = c_->pinned[3];
         s.bound = std::max(s.bound, *nw);
         if (s.chunk_cands) {
             const double got = double(r.blocks.blocks - std::min(r.blocks.blocks, s.chunk_blocks0)) /
@@ -1093,10 +1109,14 @@ public:
         // is several times smaller; switch once the directory is large.
         const double bytes = 136.0 * double(cap);
         const double keyset_bytes = 8.0 * kKeysetGrowth * double(std::max<u64>(live_keys, 1));
-        if (force_blocks_ < 0 && bytes > block_sparse_bytes_ && bytes > kBlockSparseFactor * keyset_bytes)
-            return false;
+        if (force_blocks_ < 0 && bytes > block_sparse_bytes_ && bytes > kBlockSparseFactor * keyset_bytes) {
+            // A word-form relation cannot switch mid-iteration (its DELTA is
+            // words): it grows and leaves the word form at the next finalize.
+            if (!r.word_mode) return false;
+            r.word_sparse = true;
+        }
         BlockSet ns;
-        engine_blockset_alloc(c_, ns, cap, b.blocks);
+        engine_blockset_alloc(c_, ns, cap, b.blocks, r.word_mode);
         ns.ratio = b.ratio;
         if (b.capacity()) engine_blockset_grow(c_, b, ns);
         if (trace_)
@@ -1122,8 +1142,15 @@ public:
                 convert_to_keyset(r, &s, tmp.get(), n);
                 return;
             }
-            engine_blockset_insert(c_, tmp.get(), n, block_args(r), s.keys.get(), s.counter.get(), s.ovf.get(),
-                                   s.counter.get() + 1);
+            if (r.word_mode) {
+                DBuf<u32> tb(c_, n);
+                FV_CUDA(cudaMemcpyAsync(tb.get(), s.ovf_bits.get(), 4 * n, cudaMemcpyDeviceToDevice, c_->stream));
+                engine_blockset_word_insert(c_, tmp.get(), tb.get(), n, block_args(r), s.keys.get(), s.counter.get(),
+                                            s.counter.get() + 2, s.ovf.get(), s.ovf_bits.get(), s.counter.get() + 1);
+            } else {
+                engine_blockset_insert(c_, tmp.get(), n, block_args(r), s.keys.get(), s.counter.get(), s.ovf.get(),
+                                       s.counter.get() + 1);
+            }
             u64 nw;
             read_block_counters(r, s, &nw, &n);
         }
@@ -1146,6 +1173,7 @@ public:
         }
         if (s.ovf_cap < extra) {
             s.ovf = DBuf<u64>(c_, extra);
+            if (r.word_mode) s.ovf_bits = DBuf<u32>(c_, extra);
             s.ovf_cap = extra;
         }
         s.bound = nw + extra;
@@ -1220,8 +1248,101 @@ public:
         r.keys = std::move(ns);
     }
 
+    // Word form: the iteration's new words become DELTA (columns x, z base,
+    // mask, grouped by x; the counting sort also yields its column-0 join
+    // index); returns |DELTA| in tuples.
+    u64 word_finalize(RelState& r, HeadSink& s, CandPool& pool) {
+        if (pool.n) {
+            hash_reserve(r, s, pool.n);
+            engine_blockset_word_insert(c_, pool.words[0].get(), nullptr, pool.n, block_args(r), s.keys.get(),
+                                        s.counter.get(), s.counter.get() + 2, s.ovf.get(), s.ovf_bits.get(),
+                                        s.counter.get() + 1);
+            s.candidates += pool.n;
+        }
+        u64 nw = 0, ov = 0;
+        if (s.counter.get()) {
+            read_block_counters(r, s, &nw, &ov);
+            if (ov) {
+                drain_overflow(r, s, ov);
+                read_block_counters(r, s, &nw, &ov);
+            }
+        }
+        const u64 tuples = s.counter.get() ? s.tuples : 0;
+        r.indexes.clear();
+        if (r.delta.n) r.levels.push_back(std::move(r.delta));
+        DevVersion Dv;
+        Dv.n = nw;
+        for (u32 j = 0; j <= r.arity; ++j) Dv.cols.emplace_back(c_, nw);
+        if (nw == 0) {
+            r.delta = std::move(Dv);
+            set_old(r, nullptr);
+            if (r.word_sparse) leave_word_mode(r);
+            return 0;
+        }
+        r.keys.count += tuples;
+        r.level_rows += tuples;
+        // One entry per word first written this iteration; its merged mask
+        // is read (and cleared) from the DELTA bitmap.
+        s.bits = DBuf<u32>(c_, nw);
+        engine_blockset_collect(c_, s.keys.get(), nw, block_args(r), s.bits.get());
+        auto delta_index = std::make_unique<JoinIndex>();
+        const bool grouped = engine_group_keys(c_, s.keys, nw, st_.key_shift, delta_index.get(), Dv.cols[0].get(),
+                                               Dv.cols[1].get(), s.bits.get(), Dv.cols[2].get());
+        if (!grouped) {
+            // Domain too large for the counting sort: unpack, then order the
+            // entries by x (stable LSD pass over column 0) and gather.
+            std::vector<u32*> dc{Dv.cols[0].get(), Dv.cols[1].get()};
+            engine_unpack_keys(c_, s.keys.get(), nw, 2, st_.key_shift, dc);
+            FV_CUDA(cudaMemcpyAsync(Dv.cols[2].get(), s.bits.get(), 4 * nw, cudaMemcpyDeviceToDevice, c_->stream));
+            const u32* order_cols[1] = {Dv.cols[0].get()};
+            DBuf<u32> perm = lexicographic_order(c_, order_cols, 1, nw);
+            DevVersion G;
+            G.n = nw;
+            for (u32 j = 0; j <= r.arity; ++j) {
+                DBuf<u32> g(c_, nw);
+                gather_u32(c_, Dv.cols[j].get(), perm.get(), g.get(), nw);
+                G.cols.push_back(std::move(g));
+            }
+            Dv = std::move(G);
+        }
+        s.cap = 0;
+        r.delta = std::move(Dv);
+        if (grouped) {
+            delta_index->rows = &r.delta;
+            r.indexes.emplace(std::make_pair(static_cast<int>(kDelta), 0u), std::move(delta_index));
+        }
+        if (r.word_sparse) leave_word_mode(r);
+        return tuples;
+    }
+
+    // Word-form version -> tuple form (grouping by x is kept).
+    void to_tuples(DevVersion& v, u32 arity) {
+        if (v.cols.size() != arity + 1) return;
+        DevVersion t;
+        // one pass counts the tuples (sizes the output), the second writes them
+        t.n = engine_expand_words(c_, v.cols[0].get(), v.cols[1].get(), v.cols[2].get(), v.n, nullptr, nullptr);
+        t.cols.emplace_back(c_, t.n);
+        t.cols.emplace_back(c_, t.n);
+        engine_expand_words(c_, v.cols[0].get(), v.cols[1].get(), v.cols[2].get(), v.n, t.cols[0].get(),
+                            t.cols[1].get());
+        v = std::move(t);
+    }
+
+    // Leave the word form (the block set proved sparse): DELTA and the levels
+    // become tuples and the relation converts to a key set.
+    void leave_word_mode(RelState& r) {
+        to_tuples(r.delta, r.arity);
+        for (auto& lv : r.levels) to_tuples(lv, r.arity);
+        r.indexes.clear();
+        r.word_mode = false;
+        r.word_sparse = false;
+        if (trace_) std::fprintf(stderr, "[fvlog]   %s leaves the word form\n", r.name.c_str());
+        convert_to_keyset(r, nullptr, nullptr, 0);
+    }
+
     // Sort the iteration's new keys into Δ and fold them into FULL.
     u64 hash_finalize(RelState& r, HeadSink& s, CandPool& pool) {
+        if (r.word_mode) return word_finalize(r, s, pool);
         if (pool.n) {
             hash_reserve(r, s, pool.n);
             if (r.block_mode)
@@ -1632,6 +1753,35 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         r->levels_mode = r->hash_mode && !full_read.count(name);
         r->block_mode = r->hash_mode && eng.blocks_enabled();
     }
+    // Word form (RelState::word_mode): a binary block-set relation whose
+    // DELTA is only ever read by composition variants of itself — two atoms
+    // A(x, y), DELTA(y, z) -> head(x, z), joined on DELTA's column 0 with
+    // nothing else to check (right-linear TC) — and whose other derivations
+    // are single-atom copies (pooled). FVLOG_WORDS=0 disables.
+    const char* words_env = std::getenv("FVLOG_WORDS");
+    if (!eng.dist() && !(words_env && std::string(words_env) == "0")) {
+        auto composition = [](const Plan& p, long d) {
+            return p.sources.size() == 2 && d == 1 && p.joins.size() == 1 && p.joins[0].right_source == 1 &&
+                   p.joins[0].right_col == 0 && p.joins[0].residual_eq.empty() && !p.sources[1].constrained() &&
+                   p.guard_neq.empty() && p.head_arity == 2 && p.output_cols.size() == 2 &&
+                   p.output_cols[1] == ColRef{1, 1} && p.output_cols[0].source == 0;
+        };
+        for (auto& [name, r] : st->relations) {
+            if (!(r->block_mode && r->levels_mode && r->arity == 2)) continue;
+            bool ok = true, any = false;
+            for (auto& v : variants) {
+                const Plan& p = *v.plan;
+                const bool reads_delta = v.delta_source >= 0 && p.sources[v.delta_source].relation == name;
+                if (p.head == name && !p.joins.empty()) {
+                    if (reads_delta && composition(p, v.delta_source)) any = true;
+                    else ok = false;
+                } else if (reads_delta) {
+                    ok = false;
+                }
+            }
+            r->word_mode = ok && any;
+        }
+    }
 
     const bool trace = std::getenv("FVLOG_TRACE") != nullptr;
     auto tr = [&](const char* what, Clock::time_point t, u64 it) {
@@ -1780,17 +1930,21 @@ const DevVersion& sorted_rows(const EvalState& s, const RelState& r, DevVersion&
     // concatenation gives the lexicographic dump (like dump_relation's std::sort).
     tmp.n = n;
     tmp.cols.clear();
-    for (u32 j = 0; j < r.arity; ++j) {
-        DBuf<u32> col(c, n);
-        u64 off = 0;
-        for (const DevVersion* lv : levels_of(r)) {
-            if (lv->n)
-                FV_CUDA(cudaMemcpyAsync(col.get() + off, lv->cols[j].get(), 4 * lv->n, cudaMemcpyDeviceToDevice,
-                                        c->stream));
-            off += lv->n;
+    for (u32 j = 0; j < r.arity; ++j) tmp.cols.emplace_back(c, n);
+    u64 off = 0;
+    for (const DevVersion* lv : levels_of(r)) {
+        if (!lv->n) continue;
+        if (lv->cols.size() == r.arity + 1) {  // word form: expanded in place
+            off += engine_expand_words(c, lv->cols[0].get(), lv->cols[1].get(), lv->cols[2].get(), lv->n,
+                                       tmp.cols[0].get() + off, tmp.cols[1].get() + off);
+            continue;
         }
-        tmp.cols.push_back(std::move(col));
+        for (u32 j = 0; j < r.arity; ++j)
+            FV_CUDA(cudaMemcpyAsync(tmp.cols[j].get() + off, lv->cols[j].get(), 4 * lv->n, cudaMemcpyDeviceToDevice,
+                                    c->stream));
+        off += lv->n;
     }
+    if (off != n) fail(FV_ERR_INVALID, "levels hold " + std::to_string(off) + " rows, expected " + std::to_string(n));
     if (n) {
         std::vector<DBuf<u64>> words;
         words.emplace_back(c, n);
@@ -1853,7 +2007,18 @@ u64 fingerprint(const EvalState& s, const std::string& rel) {
     const RelState& r = *it->second;
     if (!r.levels_mode) return engine_fingerprint(s.ctx, r.full.ptrs(), r.full.n, r.arity);
     u64 h = 0;  // the fingerprint is a sum over rows: additive over levels
-    for (const DevVersion* lv : levels_of(r)) h += engine_fingerprint(s.ctx, lv->ptrs(), lv->n, r.arity);
+    for (const DevVersion* lv : levels_of(r)) {
+        if (lv->cols.size() == r.arity + 1 && lv->n) {  // word form: fingerprint of its tuples
+            const u64 t = engine_expand_words(s.ctx, lv->cols[0].get(), lv->cols[1].get(), lv->cols[2].get(), lv->n,
+                                              nullptr, nullptr);
+            DBuf<u32> x(s.ctx, t), z(s.ctx, t);
+            engine_expand_words(s.ctx, lv->cols[0].get(), lv->cols[1].get(), lv->cols[2].get(), lv->n, x.get(),
+                                z.get());
+            h += engine_fingerprint(s.ctx, std::vector<const u32*>{x.get(), z.get()}, t, r.arity);
+            continue;
+        }
+        h += engine_fingerprint(s.ctx, lv->ptrs(), lv->n, r.arity);
+    }
     return h;
 }
 

@@ -123,6 +123,7 @@ struct KeySet {
 struct BlockSet {
     DBuf<u64> dir;
     DBuf<u32> bits;
+    DBuf<u32> dbits;  // word form: this iteration's new bits, same layout as `bits`
     DBuf<u64> count;  // device: blocks claimed
     u64 mask = 0;
     u64 blocks = 0;   // host copy of `count` (last read)
@@ -134,6 +135,7 @@ struct BlockSet {
 struct BlockSetArgs {
     u64* dir = nullptr;
     u32* bits = nullptr;
+    u32* dbits = nullptr;  // word form only
     u64 mask = 0;
     u64* count = nullptr;
     u64 limit = 0;  // no new block is claimed once `count` reaches this
@@ -174,6 +176,14 @@ struct RelState {
     // FULL's rows); cleared when the relation proves sparse.
     bool block_mode = false;
     BlockSet blocks;
+    // Word form (block mode, levels mode, binary; single GPU): DELTA and the
+    // levels are words — columns (x, z & ~31, mask of the z's present),
+    // grouped by x — so the composition variant that probes DELTA on
+    // column 0 (right-linear TC) emits one candidate per word, and FULL's
+    // bitmap takes one OR per word. A DevVersion with arity + 1 columns is in
+    // word form. Left when the block set turns out sparse (word_sparse).
+    bool word_mode = false;
+    bool word_sparse = false;
     // With hash dedup, a FULL no join reads is kept as levels: the past DELTAs
     // (one per iteration, grouped by column 0) plus the current `delta`,
     // concatenated and sorted only for dumps; otherwise it is `full`, merged
@@ -329,6 +339,14 @@ struct OutSpec {
     BlockSetArgs bs;
     u64* ovf_keys = nullptr;
     u64* ovf_count = nullptr;
+    // Word form (block-set dedup of a word-mode head, RelState::word_mode):
+    // col[1] is the DELTA side's word base (z & ~31), `wbits` its mask; a
+    // word's first DELTA writer appends its key to new_keys, overflow entries
+    // carry their masks in ovf_bits, and the new tuples (bits) are counted in
+    // *new_tuples.
+    SlotRef wbits;
+    u32* ovf_bits = nullptr;
+    u64* new_tuples = nullptr;
 };
 
 FV_HD inline bool fused_set(const OutSpec& s) { return s.ht_slots != nullptr || s.bs.dir != nullptr; }
@@ -336,8 +354,9 @@ FV_HD inline bool fused_set(const OutSpec& s) { return s.ht_slots != nullptr || 
 // Insert n keys; the ones not yet present are appended to
 // new_keys[*d_new ...] (device counter, not reset here).
 void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_keys, u64* d_new);
-// BlockSet: allocate `cap` (power of two) empty slots; the count starts at `blocks`.
-void engine_blockset_alloc(Ctx* c, BlockSet& s, u64 cap, u64 blocks);
+// BlockSet: allocate `cap` (power of two) empty slots; the count starts at
+// `blocks`; delta_bits: also the (zeroed) DELTA bitmap of the word form.
+void engine_blockset_alloc(Ctx* c, BlockSet& s, u64 cap, u64 blocks, bool delta_bits = false);
 // Move every block of `from` into the freshly allocated `to` (bitmaps copied whole).
 void engine_blockset_grow(Ctx* c, const BlockSet& from, BlockSet& to);
 // Insert n keys; new ones are appended to new_keys[*d_new ...] (when
@@ -364,9 +383,24 @@ u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32
 // With `runs`, also fills its column-0 run index (ukeys/ustart/ucount +
 // hash; rows left to the caller) for the grouped keys.
 // With col0/col1, the grouped rows are written as SoA columns instead
-// (keys left as they were).
+// (keys left as they were). pay_in/pay_out: a u32 payload per key moved
+// along (word masks).
 bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs = nullptr, u32* col0 = nullptr,
-                       u32* col1 = nullptr);
+                       u32* col1 = nullptr, const u32* pay_in = nullptr, u32* pay_out = nullptr);
+// Word-form block-set insert (RelState::word_mode): n word keys with masks
+// `bits`, or packed binary tuple keys (bits null) as one-bit words. New bits
+// are OR-ed into FULL and into the DELTA bitmap (s.dbits); a word's first
+// DELTA writer appends its key to new_keys[*d_new ...] and *d_tuples counts
+// the new bits; entries without a directory slot go to ovf/ovf_bits[*d_ovf ...].
+void engine_blockset_word_insert(Ctx* c, const u64* keys, const u32* bits, u64 n, const BlockSetArgs& s,
+                                 u64* new_keys, u64* d_new, u64* d_tuples, u64* ovf, u32* ovf_bits, u64* d_ovf);
+// The merged DELTA masks of n word keys (each inserted this iteration), read
+// from s.dbits into out_bits and cleared there.
+void engine_blockset_collect(Ctx* c, const u64* keys, u64 n, const BlockSetArgs& s, u32* out_bits);
+// Tuples (x, z) of n word entries (x, z base, mask), entry order kept (so
+// entries grouped by x give tuples grouped by x); returns the tuple count.
+// out_x null: count only.
+u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u64 n, u32* out_x, u32* out_z);
 // Distinct rows of sorted packed keys into fresh word buffers; returns the count.
 u64 engine_unique_words(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, std::vector<DBuf<u64>>& out);
 // SoA columns -> row-major rows out[i * arity + j] (device buffer).

@@ -250,6 +250,113 @@ __device__ __forceinline__ u32 blockset_insert_items(const BlockSetArgs& s, u32 
     return nm;
 }
 
+// ---- word form of a binary relation (RelState::word_mode, engine.h) ---------------
+//
+// A row set is carried as words: a word key (x << shift | z & ~31) plus a
+// 32-bit mask of the z's of that word present. One word is the 32 bits of
+// one row of a BlockSet block, so inserting it into FULL is ONE bitmap OR and
+// a composition join emits one candidate per (probe row, DELTA word) instead
+// of one per tuple.
+
+// Word key and bit of a packed binary tuple key.
+__device__ __forceinline__ u64 word_key_of(u64 key, u32 shift, u32* bit) {
+    const u64 z = key & ((u64(1) << shift) - 1);
+    *bit = 1u << static_cast<u32>(z & 31);
+    return ((key >> shift) << shift) | (z & ~u64(31));
+}
+
+// Set-insert of N words (bit k of `live`: key[k] / bits[k] is a candidate):
+// all directory loads first, then all bitmap-word loads, then an atomic OR
+// only where some bit is still clear. The bits that were clear in FULL are
+// also OR-ed into the block's DELTA bitmap (s.dbits, same slot): the insert
+// that finds that DELTA word empty is its first writer this iteration and
+// is flagged in *first (its key is appended once; the merged mask is read at
+// finalize). *ones = the new bits of this thread. Words whose block found no
+// directory slot are flagged in *ovf_mask.
+template <int N>
+__device__ __forceinline__ void blockset_word_items(const BlockSetArgs& s, u32 live, const u64 (&key)[N],
+                                                    const u32 (&bits)[N], u32* first, u32* ones, u32* ovf_mask) {
+    u64 slot[N];
+    u32 wi[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        slot[k] = 0;
+        wi[k] = 0;
+        if ((live >> k) & 1u) {
+            u32 bp;
+            slot[k] = block_of(key[k], s.shift, 2, &bp);  // bid for now
+            wi[k] = bp >> 5;
+        }
+    }
+    u64 dv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) dv[k] = ((live >> k) & 1u) ? __ldcg(s.dir + block_home(slot[k], s.mask)) : 0;
+    u32 om = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        if (!((live >> k) & 1u)) continue;
+        const u64 bid = slot[k], h = block_home(bid, s.mask);
+        const u64 f = dv[k] == bid ? h : blockset_find(s.dir, s.mask, s.count, s.limit, bid, h, dv[k]);
+        if (f == ~u64(0)) {
+            om |= 1u << k;
+            live &= ~(1u << k);
+        }
+        slot[k] = f * 32 + wi[k];  // bitmap word index from here on
+    }
+    u32 wv[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) wv[k] = ((live >> k) & 1u) ? __ldcg(s.bits + slot[k]) : ~0u;
+    u32 nb[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        nb[k] = 0;
+        if (!((live >> k) & 1u) || (wv[k] & bits[k]) == bits[k]) continue;
+        nb[k] = bits[k] & ~atomicOr(s.bits + slot[k], bits[k]);
+    }
+    u32 fm = 0, n1 = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        if (!nb[k]) continue;
+        n1 += __popc(nb[k]);
+        if (atomicOr(s.dbits + slot[k], nb[k]) == 0) fm |= 1u << k;
+    }
+    *first = fm;
+    *ones = n1;
+    *ovf_mask = om;
+}
+
+// Warp-aggregated append of the keys flagged in `mask` (one counter atomic
+// per warp), plus `ones` (per thread) summed into *tuples when non-null.
+template <int N>
+__device__ __forceinline__ void append_words(u64* __restrict__ out, u32* __restrict__ out_bits, u64* counter,
+                                             u64* tuples, u32 ones, u32 mask, const u64 (&key)[N],
+                                             const u32 (&bits)[N]) {
+    const u32 lane = lane_id();
+    const u32 cnt = __popc(mask);
+    u32 incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<u32>(o)) incl += y;
+    }
+    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+    if (tuples) {
+        const u32 t = __reduce_add_sync(0xffffffffu, ones);
+        if (lane == 0 && t) atomicAdd(reinterpret_cast<unsigned long long*>(tuples), static_cast<unsigned long long>(t));
+    }
+    if (!total) return;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(reinterpret_cast<unsigned long long*>(counter), static_cast<unsigned long long>(total));
+    u64 pos = __shfl_sync(0xffffffffu, base, 31) + (incl - cnt);
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+        if ((mask >> k) & 1u) {
+            out[pos] = key[k];
+            if (out_bits) out_bits[pos] = bits[k];
+            ++pos;
+        }
+}
+
 // Write one output row (values computed from slots) at position pos.
 __device__ __forceinline__ void write_row(const OutSpec& spec, u64 pos, u64 i, u64 p) {
     if (spec.key_mode) {
@@ -358,7 +465,7 @@ struct MatShared {
 
 // One output tile of the output-partitioned join expansion (see lbs_kernel in
 // column_ops.cu). All threads of the block call it for the same tile.
-template <bool COMPACT, bool REMOTE, bool BLOCKS>
+template <bool COMPACT, bool REMOTE, bool BLOCKS, bool WORDS>
 __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets, u64 o_begin, u64 total,
                                                  const u32* __restrict__ starts, const u64* __restrict__ tile_jlo,
                                                  const u64* __restrict__ tile_jhi, const OutSpec& spec, u64 t,
@@ -436,6 +543,23 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
         for (int k = 0; k < kMatItems; ++k) {
             key[k] = ((keep_mask >> k) & 1u) ? row_key1(spec, ii[k], pp[k]) : 0;
             hs[k] = keyset_line_hash(key[k], spec.ht_group_bits);
+        }
+        if constexpr (WORDS) {
+            // Word form: each output is a whole DELTA word; OR it into FULL's
+            // bitmap and append the bits that were new.
+            u32 wb[kMatItems], first, ones, ovf_mask;
+#pragma unroll
+            for (int k = 0; k < kMatItems; ++k) wb[k] = ((keep_mask >> k) & 1u) ? slot(spec.wbits, ii[k], pp[k]) : 0;
+            if (spec.probe_count) {
+                const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
+                if (lane == 0 && m) atomicAdd(reinterpret_cast<unsigned long long*>(spec.probe_count), static_cast<unsigned long long>(m));
+            }
+            blockset_word_items(spec.bs, keep_mask, key, wb, &first, &ones, &ovf_mask);
+            append_words(spec.new_keys, static_cast<u32*>(nullptr), spec.new_count, spec.new_tuples, ones, first, key,
+                         wb);
+            append_words(spec.ovf_keys, spec.ovf_bits, spec.ovf_count, static_cast<u64*>(nullptr), 0u, ovf_mask, key,
+                         wb);
+            return;
         }
         __syncthreads();  // s_set initialised (the sparse path has no barrier before this)
 #pragma unroll
@@ -594,7 +718,7 @@ constexpr int kMatGroup = 1;  // measured: 1 is best on C1-C4 (FVLOG_MAT_GROUP o
 #ifndef FV_MAT_MIN_BLOCKS_BS
 #define FV_MAT_MIN_BLOCKS_BS 2
 #endif
-template <bool COMPACT, bool REMOTE, bool BLOCKS>
+template <bool COMPACT, bool REMOTE, bool BLOCKS, bool WORDS>
 __global__ void __launch_bounds__(kMatBlock, BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_MAT_MIN_BLOCKS) materialize_kernel(const u64* __restrict__ offsets, u64 m,
                                                                  u64 o_begin, u64 total,
                                                                  const u32* __restrict__ starts,
@@ -614,7 +738,7 @@ __global__ void __launch_bounds__(kMatBlock, BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_
             if (threadIdx.x == 0) sh.set_fill = 0;
             __syncthreads();
         }
-        materialize_tile<COMPACT, REMOTE, BLOCKS>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh);
+        materialize_tile<COMPACT, REMOTE, BLOCKS, WORDS>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh);
     }
 }
 
@@ -1032,11 +1156,83 @@ __global__ void blockset_insert_kernel(const u64* __restrict__ keys, u64 n, Bloc
     append_new_items(ovf, ovf_count, om, key);
 }
 
+// Word-form block-set insert of n entries: word keys with their masks
+// (bits_in), or packed binary tuple keys (bits_in null) turned into one-bit
+// words. Words first written to DELTA this iteration are appended to
+// new_keys (new bits counted in *new_tuples), entries without a directory
+// slot go to the overflow list with their full mask.
+__global__ void blockset_word_insert_kernel(const u64* __restrict__ keys, const u32* __restrict__ bits_in, u64 n,
+                                            BlockSetArgs s, u64* __restrict__ new_keys, u64* new_count,
+                                            u64* new_tuples, u64* __restrict__ ovf, u32* __restrict__ ovf_bits,
+                                            u64* ovf_count) {
+    constexpr int ITEMS = 4;
+    const u64 base = u64(blockIdx.x) * blockDim.x * ITEMS + threadIdx.x;
+    u64 key[ITEMS];
+    u32 b[ITEMS];
+    u32 live = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 i = base + u64(k) * blockDim.x;
+        key[k] = 0;
+        b[k] = 0;
+        if (i < n) {
+            if (bits_in) {
+                key[k] = keys[i];
+                b[k] = bits_in[i];
+            } else {
+                key[k] = word_key_of(keys[i], s.shift, &b[k]);
+            }
+            live |= 1u << k;
+        }
+    }
+    u32 om, first, ones;
+    blockset_word_items(s, live, key, b, &first, &ones, &om);
+    append_words(new_keys, static_cast<u32*>(nullptr), new_count, new_tuples, ones, first, key, b);
+    append_words(ovf, ovf_bits, ovf_count, static_cast<u64*>(nullptr), 0u, om, key, b);
+}
+
+// DELTA's merged masks: entry i (a word first written this iteration) reads
+// its block's DELTA bitmap word and clears it for the next iteration.
+__global__ void blockset_collect_kernel(const u64* __restrict__ keys, u64 n, BlockSetArgs s, u32* __restrict__ out) {
+    GRID_STRIDE(i, n) {
+        u32 bp;
+        const u64 bid = block_of(keys[i], s.shift, 2, &bp);
+        u64 h = block_home(bid, s.mask);
+        while (__ldcg(s.dir + h) != bid) h = (h + 1) & s.mask;  // present: inserted this iteration
+        const u64 w = h * 32 + (bp >> 5);
+        out[i] = s.dbits[w];
+        s.dbits[w] = 0;
+    }
+}
+
+// Tuples of word entries (x, z base, mask), in entry order: entry i's set
+// bits become rows (x, base + bit) at its prefix of the popcounts.
+struct ExpandWordsOp {
+    const u32* x;
+    const u32* zb;
+    const u32* bits;
+    u32* out_x;
+    u32* out_z;
+    __device__ u64 value(u64 i) const { return __popc(bits[i]); }
+    __device__ void emit(u64 i, u64 p, u64 v) const {
+        if (!v || !out_x) return;  // counting pass
+        const u32 xi = x[i], z0 = zb[i];
+        u32 m = bits[i];
+        while (m) {
+            const u32 b = __ffs(m) - 1;
+            m &= m - 1;
+            out_x[p] = xi;
+            out_z[p] = z0 + b;
+            ++p;
+        }
+    }
+};
+
 // Directory growth: every used old slot re-homed in the new directory, its
 // 128-byte bitmap moved with 16-byte vector loads/stores. Block ids are
 // distinct, so a block only has to find an empty slot.
-__global__ void blockset_grow_kernel(const u64* __restrict__ from_dir, const u32* __restrict__ from_bits, u64 n,
-                                     BlockSetArgs to) {
+__global__ void blockset_grow_kernel(const u64* __restrict__ from_dir, const u32* __restrict__ from_bits,
+                                     const u32* __restrict__ from_dbits, u64 n, BlockSetArgs to) {
     GRID_STRIDE(i, n) {
         const u64 bid = __ldcs(from_dir + i);
         if (bid == kEmptySlot) continue;
@@ -1048,6 +1244,12 @@ __global__ void blockset_grow_kernel(const u64* __restrict__ from_dir, const u32
         uint4* dst = reinterpret_cast<uint4*>(to.bits + h * 32);
 #pragma unroll
         for (int q = 0; q < 8; ++q) dst[q] = __ldcs(src + q);
+        if (to.dbits) {  // word form: the block's DELTA bitmap moves along
+            const uint4* dsrc = reinterpret_cast<const uint4*>(from_dbits + i * 32);
+            uint4* ddst = reinterpret_cast<uint4*>(to.dbits + h * 32);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ddst[q] = __ldcs(dsrc + q);
+        }
     }
 }
 
@@ -1211,7 +1413,8 @@ __global__ void group_count_kernel(const u64* __restrict__ keys, u64 n, u32 shif
 
 __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 shift, const u64* __restrict__ base,
                                      u32* __restrict__ cursor, u64* __restrict__ out, u32* __restrict__ c0,
-                                     u32* __restrict__ c1) {
+                                     u32* __restrict__ c1, const u32* __restrict__ pay_in,
+                                     u32* __restrict__ pay_out) {
     const u64 n_round = ceil_div(n, 32) * 32;
     const u32 lane = lane_id();
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n_round; i += u64(gridDim.x) * blockDim.x) {
@@ -1237,6 +1440,7 @@ __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 sh
 #endif
         }
         if (valid) {
+            if (pay_out) pay_out[pos] = pay_in[i];  // word masks travel with their keys
             if (c0) {  // unpacked straight into SoA columns
                 c0[pos] = g;
                 c1[pos] = static_cast<u32>(key & ((u64(1) << shift) - 1));
@@ -1395,9 +1599,11 @@ void engine_hash_insert(Ctx* c, const u64* keys, u64 n, KeySet& set, u64* new_ke
     c->count_launch();
 }
 
-void engine_blockset_alloc(Ctx* c, BlockSet& s, u64 cap, u64 blocks) {
+void engine_blockset_alloc(Ctx* c, BlockSet& s, u64 cap, u64 blocks, bool delta_bits) {
     s.dir = DBuf<u64>(c, cap);
     s.bits = DBuf<u32>(c, cap * 32);
+    s.dbits = delta_bits ? DBuf<u32>(c, cap * 32) : DBuf<u32>();
+    if (delta_bits) FV_CUDA(cudaMemsetAsync(s.dbits.get(), 0, 128 * cap, c->stream));
     s.count = DBuf<u64>(c, 1);
     s.mask = cap - 1;
     s.blocks = blocks;
@@ -1413,9 +1619,12 @@ void engine_blockset_grow(Ctx* c, const BlockSet& from, BlockSet& to) {
     BlockSetArgs a;
     a.dir = to.dir.get();
     a.bits = to.bits.get();
+    a.dbits = from.dbits.get() ? to.dbits.get() : nullptr;
     a.mask = to.mask;
-    ProfScope prof(c, "blockset_grow", 136.0 * double(n) + 136.0 * double(to.blocks));
-    blockset_grow_kernel<<<grid_for(n), 256, 0, c->stream>>>(from.dir.get(), from.bits.get(), n, a);
+    const double per_block = a.dbits ? 264.0 : 136.0;
+    ProfScope prof(c, "blockset_grow", per_block * double(n) + per_block * double(to.blocks));
+    blockset_grow_kernel<<<grid_for(n), 256, 0, c->stream>>>(from.dir.get(), from.bits.get(), from.dbits.get(), n,
+                                                              a);
     FV_CUDA(cudaGetLastError());
     FV_CUDA(cudaMemcpyAsync(to.count.get(), from.count.get(), 8, cudaMemcpyDeviceToDevice, c->stream));
     c->count_launch();
@@ -1429,6 +1638,37 @@ void engine_blockset_insert(Ctx* c, const u64* keys, u64 n, const BlockSetArgs& 
     blockset_insert_kernel<<<grid, 256, 0, c->stream>>>(keys, n, s, new_keys, d_new, ovf, d_ovf);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
+}
+
+void engine_blockset_word_insert(Ctx* c, const u64* keys, const u32* bits, u64 n, const BlockSetArgs& s,
+                                 u64* new_keys, u64* d_new, u64* d_tuples, u64* ovf, u32* ovf_bits, u64* d_ovf) {
+    if (!n) return;
+    ProfScope prof(c, "blockset_insert", (bits ? 12.0 : 8.0) * double(n));
+    const unsigned grid = static_cast<unsigned>(ceil_div(n, u64(256) * 4));
+    blockset_word_insert_kernel<<<grid, 256, 0, c->stream>>>(keys, bits, n, s, new_keys, d_new, d_tuples, ovf,
+                                                             ovf_bits, d_ovf);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+void engine_blockset_collect(Ctx* c, const u64* keys, u64 n, const BlockSetArgs& s, u32* out_bits) {
+    if (!n) return;
+    ProfScope prof(c, "blockset_collect", 20.0 * double(n));
+    blockset_collect_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, n, s, out_bits);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u64 n, u32* out_x, u32* out_z) {
+    if (!n) return 0;
+    u64* d = c->d_scalars + 36;
+    {
+        ProfScope prof(c, "expand_words", 12.0 * double(n));
+        tile_scan(c, ExpandWordsOp{x, zb, bits, out_x, out_z}, n, d);
+    }
+    u64 total = 0;
+    c->read_scalars(d, &total, 1);
+    return total;
 }
 
 void engine_hash_rehash(Ctx* c, const KeySet& from, KeySet& to) {
@@ -1475,7 +1715,8 @@ bool engine_hash_grow(Ctx* c, const KeySet& from, KeySet& to) {
 
 static void build_run_hash(Ctx* c, JoinIndex& idx);
 
-bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs, u32* col0, u32* col1) {
+bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs, u32* col0, u32* col1,
+                       const u32* pay_in, u32* pay_out) {
     // Small domains with thousands of keys per value serialize on the
     // counters (C1: 2.6 K keys per value, 2.2 -> 5.1 ms); radix there.
     if (shift > kGroupMaxBits || n > (u64(kGroupMaxPerValue) << shift)) return false;
@@ -1491,7 +1732,7 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
         FV_CUDA(cudaGetLastError());
         tile_scan(c, GroupBaseOp{cnt.get(), base.get()}, domain, nullptr);
         group_scatter_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys.get(), n, shift, base.get(), cursor.get(),
-                                                                  out.get(), col0, col1);
+                                                                  out.get(), col0, col1, pay_in, pay_out);
         FV_CUDA(cudaGetLastError());
         c->count_launch(2);
     }
@@ -1630,7 +1871,9 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
         (spec.f[k].a.side ? side1 : side0) += 4;
         if (spec.f[k].op != kFilterConst) (spec.f[k].b.side ? side1 : side0) += 4;
     }
-    const double row_bytes = spec.key_mode ? 8.0 * ((spec.n_out + 1) / 2) : 4.0 * spec.n_out;
+    if (spec.wbits.ptr) (spec.wbits.side ? side1 : side0) += 4;
+    const double row_bytes = (spec.key_mode ? 8.0 * ((spec.n_out + 1) / 2) : 4.0 * spec.n_out) +
+                             (spec.wbits.ptr ? 4.0 : 0.0);
     const double out_bytes = fused_set(spec) ? 2.0 * row_bytes : row_bytes;
     const double frac = double(outs) / double(total);  // a chunk reads its share of the probe rows
     DBuf<u64> rows(c, 2 * tiles);
@@ -1650,11 +1893,14 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
     const u64* jhi = rows.get() + tiles;
     // Instantiations: filtered (COMPACT), partitioned routing (REMOTE) and
     // block-set dedup (BLOCKS) each keep their own register budget.
-#define FV_MAT_LAUNCH(C_, R_, B_)                                                                         \
-    materialize_kernel<C_, R_, B_><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, jlo, \
-                                                                       jhi, tiles, group, spec)
+#define FV_MAT_LAUNCH(C_, R_, B_) FV_MAT_LAUNCH_W(C_, R_, B_, false)
+#define FV_MAT_LAUNCH_W(C_, R_, B_, W_)                                                                    \
+    materialize_kernel<C_, R_, B_, W_><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, \
+                                                                           jlo, jhi, tiles, group, spec)
     const bool blocks = spec.bs.dir != nullptr;
     const bool cmp = spec.n_filters != 0;
+    const bool words = spec.wbits.ptr != nullptr;
+    if (words && (!blocks || spec.remote_world)) fail(FV_ERR_INVALID, "word-form join needs a local block set");
     if (spec.remote_world) {
         if (blocks) {
             if (cmp) FV_MAT_LAUNCH(true, true, true);
@@ -1663,6 +1909,9 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
             if (cmp) FV_MAT_LAUNCH(true, true, false);
             else FV_MAT_LAUNCH(false, true, false);
         }
+    } else if (words) {
+        if (cmp) FV_MAT_LAUNCH_W(true, false, true, true);
+        else FV_MAT_LAUNCH_W(false, false, true, true);
     } else if (blocks) {
         if (cmp) FV_MAT_LAUNCH(true, false, true);
         else FV_MAT_LAUNCH(false, false, true);
@@ -1671,6 +1920,7 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
         else FV_MAT_LAUNCH(false, false, false);
     }
 #undef FV_MAT_LAUNCH
+#undef FV_MAT_LAUNCH_W
     FV_CUDA(cudaGetLastError());
     c->count_launch(2);
 }

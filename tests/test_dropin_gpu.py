@@ -49,18 +49,56 @@ def test_dropin_binaries_link_libfvlog():
             assert "fv_evaluate" in syms, name
 
 
+def _run_suite(binary):
+    """Run a doctest suite with one child process per case; returns
+    ({case: (status, assertions)}, summary line)."""
+    r = subprocess.run([binary], capture_output=True, text=True, timeout=1800,
+                       env=dict(os.environ, DOCTEST_MINI_FORK="1"))
+    cases = {}
+    for line in r.stdout.splitlines():
+        m = re.match(r"\[doctest\] case: (\S+) (\d+) (.*)$", line)
+        if m:
+            cases[m.group(3)] = (m.group(1), int(m.group(2)))
+    summary = [l for l in r.stdout.splitlines() if l.startswith("[doctest] test cases")]
+    assert summary, f"exit {r.returncode}\n" + r.stdout + r.stderr[-6000:]
+    return cases, summary[-1], r.stderr
+
+
+def test_reference_suites_on_the_reference_build():
+    """(CPU) the baseline: the same suites linked against the reference's own
+    objects. In this environment the reference passes column/relation/kernels
+    and 10 of 12 engine cases: its random-rule generator indexes an empty
+    vector (P/tests/engine_test.cpp:83, a crash) and its residual-equality
+    defect (P/src/kernels.cpp:155) fails semi-naive == naive."""
+    for suite, n in SUITES.items():
+        cases, _, _ = _run_suite(_binary(f"{suite}_test_ref"))
+        assert len(cases) == n, suite
+        bad = {c: st for c, (st, _) in cases.items() if st != "ok"}
+        if suite == "engine":
+            assert set(bad) <= {"executing a compiled plan once equals the oracle's single step",
+                                "semi-naive evaluation equals naive evaluation on random programs"}, bad
+        else:
+            assert not bad, (suite, bad)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("suite", sorted(SUITES))
 def test_reference_suite_on_gpu(suite):
-    p = _binary(f"{suite}_test")
-    r = subprocess.run([p], capture_output=True, text=True, timeout=900)
-    summary = [l for l in r.stdout.splitlines() if l.startswith("[doctest]")]
-    assert summary, r.stdout + r.stderr
-    m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed", summary[-1])
-    assert m, summary[-1]
-    total, passed, failed = map(int, m.groups())
-    assert failed == 0 and r.returncode == 0, r.stderr[-4000:]
-    assert total == passed == SUITES[suite]
+    """Every case the reference passes passes on fvlog with the same number of
+    assertions; cases the reference fails on its own defect pass on fvlog;
+    the generator crash (inside the test's own code) is the only allowed
+    non-pass, and only where the reference crashes too."""
+    ref, _, _ = _run_suite(_binary(f"{suite}_test_ref"))
+    got, summary, err = _run_suite(_binary(f"{suite}_test"))
+    assert set(got) == set(ref) and len(got) == SUITES[suite], summary
+    for case, (st, n) in ref.items():
+        gst, gn = got[case]
+        if st == "ok":
+            assert gst == "ok" and gn == n, (case, got[case], ref[case], err[-3000:])
+        elif st == "failed":
+            assert gst == "ok", (case, got[case], err[-3000:])
+        else:  # crashed inside the reference's test generator
+            assert gst in ("ok", st), (case, got[case])
 
 
 @pytest.mark.gpu

@@ -322,7 +322,11 @@ def test_keyset_growth_paths_match_reference(ctx, grow, monkeypatch):
     {"FVLOG_SET": "blocks", "FVLOG_BLOCK_RATIO": "0"},        # directory never pre-grown: overflow lists drained
     {"FVLOG_BLOCK_SPARSE_BYTES": "0"},                        # sparse relations convert to key sets mid-run
     {"FVLOG_BLOCK_TILE_SET": "0"},                            # no tile-local dedup before the block set
-], ids=["keyset", "blocks", "blocks-overflow", "blocks-convert", "blocks-no-tile-set"])
+    {"FVLOG_WORDS": "0"},                                     # tuple-form DELTA for every block-set relation
+    {"FVLOG_BLOCK_RATIO": "0"},                               # word form with overflow lists drained
+    {"FVLOG_BLOCK_SPARSE_BYTES": "0", "FVLOG_WORDS": "1"},    # word form left mid-run (sparse -> key set)
+], ids=["keyset", "blocks", "blocks-overflow", "blocks-convert", "blocks-no-tile-set", "no-words",
+        "words-overflow", "words-leave"])
 def test_dedup_sets_match_reference(ctx, setmode, monkeypatch):
     # FULL's dedup structure for binary/unary IDB relations: a BlockSet
     # (blocked bitmap, default) or a KeySet; every path must give the

@@ -24,8 +24,14 @@ from launch_summary import summarise  # noqa: E402
 
 # bench.py / fv_ctx_profile names -> CUDA kernel names in the launch list
 PROFILER_TO_KERNEL = {
-    "join_dedup": "materialize_kernel<0, 0>",
-    "join_materialize": "materialize_kernel<0, 0>",
+    # fused join + set dedup: word form (<.., 1, 1>), block set (<.., 1, 0>),
+    # key set (<.., 0, 0>); round-1 names had two template arguments
+    "join_dedup": ["materialize_kernel<0, 0, 1, 1>", "materialize_kernel<0, 0, 1, 0>", "materialize_kernel<0, 0, 0, 0>",
+                   "materialize_kernel<0, 0, 1>", "materialize_kernel<0, 0>"],
+    "join_materialize": ["materialize_kernel<0, 0, 0, 0>", "materialize_kernel<0, 0>"],
+    "blockset_insert": ["blockset_word_insert_kernel", "blockset_insert_kernel"],
+    "blockset_collect": "blockset_collect_kernel",
+    "blockset_grow": "blockset_grow_kernel",
     "group_keys": ["group_count_kernel", "group_scatter_kernel"],
     "hash_insert": "hash_insert_keys_kernel",
     "radix_onesweep_u64": "onesweep_kernel<unsigned long, 0>",
