@@ -514,9 +514,11 @@ def run_fvlog(args):
         st = R.step_resident(w)
         del st
     launches0 = R.ctx.kernel_launches()
+    syncs0 = R.ctx.host_syncs()
     sampler = ClockSampler(R.device)
     t_max, st = R.timed(args.steps, lambda: R.step_resident(w), sampler)
     launches = R.ctx.kernel_launches() - launches0
+    syncs = R.ctx.host_syncs() - syncs0
     derived = st.derived_tuples()
     iterations = st.iterations
     value = derived * args.steps / (t_max / 1000.0)
@@ -636,6 +638,8 @@ def run_fvlog(args):
         "e2e": e2e,
         "e2e_with_dump": e2e_dump,
         "gpu_launches": int(launches),
+        "host_syncs": {"per_step": syncs / args.steps, "per_iteration": round(syncs / args.steps / iterations, 2),
+                       "what": "stream syncs + scalar readbacks on the engine context (fv_ctx_host_syncs)"},
         "clocks": sampler.summary(),
         "roofline": roofline_of(kernels, prof_steps),
         "random_access": random_access,

@@ -77,6 +77,10 @@ fv_status fv_ctx_synchronize(fv_ctx* ctx);
 fv_status fv_ctx_reserve(fv_ctx* ctx, uint64_t bytes);
 /* Number of kernels this context has launched so far (profiling evidence). */
 uint64_t fv_ctx_kernel_launches(const fv_ctx* ctx);
+/* Host synchronisations (stream syncs + scalar readbacks) issued on ctx so
+ * far: the host round trips a fixpoint makes (north_star: ~one scalar per
+ * iteration). */
+uint64_t fv_ctx_host_syncs(const fv_ctx* ctx);
 /* Per-kernel-class timing with CUDA events recorded on the context stream
  * around every launch (enable = 1 clears previous entries). Each entry:
  * launches, summed device milliseconds, summed algorithmic bytes (inputs

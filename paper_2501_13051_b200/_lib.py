@@ -77,6 +77,7 @@ _SIGNATURES = [
     ("fv_last_error", C.c_char_p, [vp]),
     ("fv_ctx_synchronize", st, [vp]),
     ("fv_ctx_kernel_launches", C.c_uint64, [vp]),
+    ("fv_ctx_host_syncs", C.c_uint64, [vp]),
     ("fv_gather_volume", C.c_uint64, []),
     ("fv_reset_gather_volume", None, []),
     ("fv_array_size", C.c_uint64, [vp]),

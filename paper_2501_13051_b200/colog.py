@@ -59,6 +59,10 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self._lib.fv_ctx_kernel_launches(self.h))
 
+    def host_syncs(self) -> int:
+        """Host synchronisations issued on this context so far."""
+        return int(self._lib.fv_ctx_host_syncs(self.h))
+
     def close(self):
         if getattr(self, "h", None):
             self._lib.fv_ctx_destroy(self.h)

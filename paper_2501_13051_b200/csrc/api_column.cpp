@@ -123,6 +123,8 @@ fv_status fv_ctx_synchronize(fv_ctx* ctx) {
 
 uint64_t fv_ctx_kernel_launches(const fv_ctx* ctx) { return ctx ? ctx->c->launches : 0; }
 
+uint64_t fv_ctx_host_syncs(const fv_ctx* ctx) { return ctx ? ctx->c->syncs : 0; }
+
 fv_status fv_ctx_profile(fv_ctx* ctx, int enable) {
     FV_API_BEGIN(ctx)
     FV_REQUIRE(ctx, FV_ERR_INVALID, "fv_ctx_profile: null ctx");

@@ -113,10 +113,18 @@ struct HeadSink {
     // Block sets: keys the set could not place (drained before every chunk).
     DBuf<u64> ovf;
     u64 ovf_cap = 0;
-    // Word form: the masks of `keys` / `ovf` entries.
-    DBuf<u32> bits, ovf_bits;
+    // Word form: the merged masks of `keys` (at finalize), the masks of `ovf`
+    // entries, the bitmap word index of each `keys` entry (recorded at
+    // append; valid while the directory generation is still gen0).
+    DBuf<u32> bits, ovf_bits, widx;
+    u64 gen0 = ~u64(0);
     u64 chunk_blocks0 = 0, chunk_cands = 0;  // growth-ratio bookkeeping
     u64 tuples = 0;                          // host copy of counter[2] (last read)
+    // Counters (new, overflow, tuples, blocks) already read with another
+    // scalar (the join's output count, or known zero for a fresh sink):
+    // the next read_block_counters uses them instead of a sync.
+    bool pre = false;
+    u64 pre_vals[4] = {0, 0, 0, 0};
 };
 
 // Block sets (BlockSet, engine.h): a relation falls back to a key set when
@@ -432,9 +440,10 @@ public:
         if (s.n_filters >= static_cast<u32>(kMaxFilters)) fail(FV_ERR_PLAN, "rule needs more than 8 filters");
         s.f[s.n_filters++] = x;
     }
-    Filter owner_filter(const SlotRef& s) const {
+    Filter owner_filter(const SlotRef& s, u32 oshift) const {
         Filter f{s, {}, kFilterOwner, rank_};
         f.world = world_;
+        f.oshift = oshift;
         return f;
     }
 
@@ -488,7 +497,7 @@ public:
     }
 
     // Route a candidate pool to owner(head col 0).
-    void route_pool(CandPool& pool, u32 home) {
+    void route_pool(CandPool& pool, u32 home, u32 oshift) {
         const u32 W = (pool.arity + 1) / 2;
         if (pool.words.empty()) pool.words.resize(W);
         std::vector<const u64*> in;
@@ -507,6 +516,7 @@ public:
         rk.shift = st_.key_shift;
         rk.hi = pool.arity >= 2 && home == 0 ? 1 : 0;
         if (pool.arity >= 2 && home == 1) rk.mask = (u64(1) << st_.key_shift) - 1;
+        rk.oshift = oshift;
         std::vector<u64> cnt(world_), off(world_);
         engine_route(c_, pool.n, rk, world_, {}, {}, in, outp, cnt.data(), off.data());
         std::vector<DBuf<u64>> recv;
@@ -575,7 +585,10 @@ public:
         auto slot0 = [&](const ColRef& r) { return SlotRef{v.ver[0]->cols[r.col].get(), 0}; };
         for (auto& [ga, gb] : plan.guard_neq)
             push(spec, Filter{slot0(plan.output_cols[ga]), slot0(plan.output_cols[gb]), kFilterNeq, 0});
-        if (v.D && dp.replicated_out) push(spec, owner_filter(slot0(plan.output_cols[rel(plan.head).home])));
+        if (v.D && dp.replicated_out) {
+            const RelState& h = rel(plan.head);
+            push(spec, owner_filter(slot0(plan.output_cols[h.home]), h.owner_shift));
+        }
         spec.key_mode = 1;
         spec.n_out = plan.head_arity;
         for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot0(plan.output_cols[h]);
@@ -628,8 +641,23 @@ public:
         DBuf<u64> offsets(c_, n + 1);
         exclusive_scan_counts(c_, counts.get(), offsets.get(), n);
         FV_CUDA(cudaMemcpyAsync(c_->pinned, offsets.get() + n, 8, cudaMemcpyDeviceToHost, c_->stream));
+        // The fused dedup's set counters ride on the same sync (its first
+        // chunk then needs no read of its own).
+        HeadSink* pre = nullptr;
+        if (k + 1 == nj && sink && sink->counter.get()) {
+            RelState& hr = rel(plan.head);
+            if (hr.block_mode && hr.blocks.capacity()) {
+                pre = sink;
+                FV_CUDA(cudaMemcpyAsync(c_->pinned + 8, sink->counter.get(), 24, cudaMemcpyDeviceToHost, c_->stream));
+                FV_CUDA(cudaMemcpyAsync(c_->pinned + 11, hr.blocks.count.get(), 8, cudaMemcpyDeviceToHost, c_->stream));
+            }
+        }
         c_->sync();
         const u64 T = c_->pinned[0];
+        if (pre && T) {  // consumed by the first chunk's hash_reserve below
+            pre->pre = true;
+            for (int q = 0; q < 4; ++q) pre->pre_vals[q] = c_->pinned[8 + q];
+        }
         counts.reset();
         if (trace_)
             std::fprintf(stderr, "[fvlog]   %s join %zu/%zu delta@%ld probe=%llu outputs=%llu\n", plan.head.c_str(), k, nj,
@@ -650,7 +678,10 @@ public:
         if (last) {
             for (auto& [ga, gb] : plan.guard_neq)
                 push(spec, Filter{slot_of(plan.output_cols[ga]), slot_of(plan.output_cols[gb]), kFilterNeq, 0});
-            if (D && dp.replicated_out) push(spec, owner_filter(slot_of(plan.output_cols[rel(plan.head).home])));
+            if (D && dp.replicated_out) {
+                const RelState& h = rel(plan.head);
+                push(spec, owner_filter(slot_of(plan.output_cols[h.home]), h.owner_shift));
+            }
             spec.key_mode = 1;
             spec.n_out = plan.head_arity;
             for (u32 h = 0; h < plan.head_arity; ++h) spec.col[h] = slot_of(plan.output_cols[h]);
@@ -675,6 +706,7 @@ public:
                     spec.remote_world = world_;
                     spec.remote_rank = rank_;
                     spec.remote_col = hr.home;
+                    spec.remote_oshift = hr.owner_shift;
                     FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
                 }
                 // A chunk's outputs bound the keys it can add to the local
@@ -701,7 +733,8 @@ public:
                             spec.wbits = SlotRef{idx->rows->cols[hr.arity].get(), 1};
                             spec.ovf_bits = sink->ovf_bits.get();
                             spec.new_tuples = sink->counter.get() + 2;
-                            spec.tile_set = 0;
+                            spec.new_widx = sink->widx.get();
+                            spec.tile_set = word_combine_;
                         }
                     } else {
                         spec.bs = BlockSetArgs();
@@ -948,7 +981,7 @@ public:
             spec.key_mode = 1;
             spec.n_out = r.arity;
             for (u32 j = 0; j < r.arity; ++j) spec.col[j] = SlotRef{v.cols[j].get(), 0};
-            push(spec, owner_filter(SlotRef{v.cols[kc].get(), 0}));
+            push(spec, owner_filter(SlotRef{v.cols[kc].get(), 0}, kc == r.home ? r.owner_shift : 0));
             for (u32 w = 0; w < W; ++w) spec.keys[w] = pool.words[w].get();
             spec.d_count = c_->d_scalars + 20;
             FV_CUDA(cudaMemsetAsync(spec.d_count, 0, 8, c_->stream));
@@ -1006,6 +1039,10 @@ public:
         if (!s.counter.get()) {
             s.counter = DBuf<u64>(c_, 3);
             FV_CUDA(cudaMemsetAsync(s.counter.get(), 0, 24, c_->stream));
+            // fresh counters are zero and the block count is the last one read
+            s.pre = true;
+            s.pre_vals[0] = s.pre_vals[1] = s.pre_vals[2] = 0;
+            s.pre_vals[3] = r.blocks.blocks;
         }
         if (r.block_mode) {
             block_reserve(r, s, extra);
@@ -1082,13 +1119,18 @@ public:
     // Sink counters (new, overflow) and the block count in one sync; also
     // updates the relation's new-blocks-per-candidate estimate.
     void read_block_counters(RelState& r, HeadSink& s, u64* nw, u64* ov) {
-        FV_CUDA(cudaMemcpyAsync(c_->pinned, s.counter.get(), 24, cudaMemcpyDeviceToHost, c_->stream));
-        FV_CUDA(cudaMemcpyAsync(c_->pinned + 3, r.blocks.count.get(), 8, cudaMemcpyDeviceToHost, c_->stream));
-        c_->sync();
-        *nw = c_->pinned[0];
-        *ov = c_->pinned[1];
-        s.tuples = c_->pinned[2];
-        r.blocks.blocks = c_->pinned[3];
+        const u64* v = s.pre_vals;
+        if (!s.pre) {
+            FV_CUDA(cudaMemcpyAsync(c_->pinned, s.counter.get(), 24, cudaMemcpyDeviceToHost, c_->stream));
+            FV_CUDA(cudaMemcpyAsync(c_->pinned + 3, r.blocks.count.get(), 8, cudaMemcpyDeviceToHost, c_->stream));
+            c_->sync();
+            v = c_->pinned;
+        }
+        s.pre = false;
+        *nw = v[0];
+        *ov = v[1];
+        s.tuples = v[2];
+        r.blocks.blocks = v[3];
         s.bound = std::max(s.bound, *nw);
         if (s.chunk_cands) {
             const double got = double(r.blocks.blocks - std::min(r.blocks.blocks, s.chunk_blocks0)) /
@@ -1118,6 +1160,7 @@ public:
         BlockSet ns;
         engine_blockset_alloc(c_, ns, cap, b.blocks, r.word_mode);
         ns.ratio = b.ratio;
+        ns.generation = b.generation + 1;
         if (b.capacity()) engine_blockset_grow(c_, b, ns);
         if (trace_)
             std::fprintf(stderr, "[fvlog]   %s block set -> %llu slots (%llu blocks)\n", r.name.c_str(),
@@ -1134,9 +1177,13 @@ public:
             FV_CUDA(cudaMemcpyAsync(tmp.get(), s.ovf.get(), 8 * n, cudaMemcpyDeviceToDevice, c_->stream));
             FV_CUDA(cudaMemsetAsync(s.counter.get() + 1, 0, 8, c_->stream));
             // At least double the directory (n keys may share far fewer
-            // blocks; another round follows if they do not fit).
-            const u64 need = std::max(r.blocks.blocks + std::max<u64>(4096, std::min(n, r.blocks.blocks)),
-                                      r.blocks.capacity() / 2 + 1);
+            // blocks; another round follows if they do not fit). A long list
+            // (a seed, a first large iteration) is sized exactly by counting
+            // its distinct blocks, so it drains in one round.
+            u64 need = std::max(r.blocks.blocks + std::max<u64>(4096, std::min(n, r.blocks.blocks)),
+                                r.blocks.capacity() / 2 + 1);
+            if (n >= (u64(1) << 16))
+                need = std::max(need, r.blocks.blocks + engine_count_blocks(c_, tmp.get(), n, st_.key_shift, r.arity));
             if (!block_grow(r, need, r.keys.count + s.bound + n)) {
                 // too sparse for blocks: the key set takes over, overflow keys included
                 convert_to_keyset(r, &s, tmp.get(), n);
@@ -1145,8 +1192,9 @@ public:
             if (r.word_mode) {
                 DBuf<u32> tb(c_, n);
                 FV_CUDA(cudaMemcpyAsync(tb.get(), s.ovf_bits.get(), 4 * n, cudaMemcpyDeviceToDevice, c_->stream));
-                engine_blockset_word_insert(c_, tmp.get(), tb.get(), n, block_args(r), s.keys.get(), s.counter.get(),
-                                            s.counter.get() + 2, s.ovf.get(), s.ovf_bits.get(), s.counter.get() + 1);
+                engine_blockset_word_insert(c_, tmp.get(), tb.get(), n, block_args(r), s.keys.get(), s.widx.get(),
+                                            s.counter.get(), s.counter.get() + 2, s.ovf.get(), s.ovf_bits.get(),
+                                            s.counter.get() + 1);
             } else {
                 engine_blockset_insert(c_, tmp.get(), n, block_args(r), s.keys.get(), s.counter.get(), s.ovf.get(),
                                        s.counter.get() + 1);
@@ -1157,16 +1205,23 @@ public:
     }
 
     void block_reserve(RelState& r, HeadSink& s, u64 extra) {
+        u64 nw = 0, ov = 0;
+        if (r.blocks.capacity()) read_block_counters(r, s, &nw, &ov);
+        else s.pre = false;
         if (s.bound + extra > s.cap) {
-            const u64 have = sink_count(s);
+            const u64 have = r.blocks.capacity() ? nw : sink_count(s);
             const u64 nc = std::max<u64>(have + extra, 2 * s.cap);
             DBuf<u64> nk(c_, nc);
             if (have) FV_CUDA(cudaMemcpyAsync(nk.get(), s.keys.get(), 8 * have, cudaMemcpyDeviceToDevice, c_->stream));
             s.keys = std::move(nk);
+            if (r.word_mode) {
+                DBuf<u32> nw_idx(c_, nc);
+                if (have)
+                    FV_CUDA(cudaMemcpyAsync(nw_idx.get(), s.widx.get(), 4 * have, cudaMemcpyDeviceToDevice, c_->stream));
+                s.widx = std::move(nw_idx);
+            }
             s.cap = nc;
         }
-        u64 nw = 0, ov = 0;
-        if (r.blocks.capacity()) read_block_counters(r, s, &nw, &ov);
         if (ov) {
             drain_overflow(r, s, ov);
             if (!r.block_mode) return;
@@ -1185,6 +1240,7 @@ public:
         }
         s.chunk_blocks0 = r.blocks.blocks;
         s.chunk_cands = extra;
+        if (nw == 0) s.gen0 = r.blocks.generation;  // no entry recorded yet
     }
 
     // Replace a relation's block set by a key set holding FULL's rows plus
@@ -1255,8 +1311,8 @@ public:
         if (pool.n) {
             hash_reserve(r, s, pool.n);
             engine_blockset_word_insert(c_, pool.words[0].get(), nullptr, pool.n, block_args(r), s.keys.get(),
-                                        s.counter.get(), s.counter.get() + 2, s.ovf.get(), s.ovf_bits.get(),
-                                        s.counter.get() + 1);
+                                        s.widx.get(), s.counter.get(), s.counter.get() + 2, s.ovf.get(),
+                                        s.ovf_bits.get(), s.counter.get() + 1);
             s.candidates += pool.n;
         }
         u64 nw = 0, ov = 0;
@@ -1284,7 +1340,8 @@ public:
         // One entry per word first written this iteration; its merged mask
         // is read (and cleared) from the DELTA bitmap.
         s.bits = DBuf<u32>(c_, nw);
-        engine_blockset_collect(c_, s.keys.get(), nw, block_args(r), s.bits.get());
+        const bool idx_ok = s.gen0 == r.blocks.generation && r.blocks.capacity() <= (u64(1) << 27);
+        engine_blockset_collect(c_, s.keys.get(), idx_ok ? s.widx.get() : nullptr, nw, block_args(r), s.bits.get());
         auto delta_index = std::make_unique<JoinIndex>();
         const bool grouped = engine_group_keys(c_, s.keys, nw, st_.key_shift, delta_index.get(), Dv.cols[0].get(),
                                                Dv.cols[1].get(), s.bits.get(), Dv.cols[2].get());
@@ -1479,6 +1536,11 @@ private:
     const double block_sparse_bytes_ = [] {
         const char* e = std::getenv("FVLOG_BLOCK_SPARSE_BYTES");
         return e ? std::atof(e) : kBlockSparseMinBytes;
+    }();
+    // FVLOG_WORD_COMBINE=0: no tile-local OR-combine of word-form outputs.
+    const u32 word_combine_ = [] {
+        const char* e = std::getenv("FVLOG_WORD_COMBINE");
+        return e ? static_cast<u32>(std::atoi(e) != 0) : 1u;
     }();
     // FVLOG_BLOCK_TILE_SET=0: no tile-local dedup before the block-set probe.
     const u32 block_tile_set_ = [] {
@@ -1758,8 +1820,13 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     // A(x, y), DELTA(y, z) -> head(x, z), joined on DELTA's column 0 with
     // nothing else to check (right-linear TC) — and whose other derivations
     // are single-atom copies (pooled). FVLOG_WORDS=0 disables.
+    // Partitioned runs additionally need every derivation of the head to stay
+    // where it is produced — the composition variants local (homed on the
+    // column they carry, z) and the copies replicated (owner-filtered) — and
+    // no partition copies; the home column's owner is then taken over 32-value
+    // windows (owner_shift 5) so a word never straddles two ranks.
     const char* words_env = std::getenv("FVLOG_WORDS");
-    if (!eng.dist() && !(words_env && std::string(words_env) == "0")) {
+    if (!(words_env && std::string(words_env) == "0")) {
         auto composition = [](const Plan& p, long d) {
             return p.sources.size() == 2 && d == 1 && p.joins.size() == 1 && p.joins[0].right_source == 1 &&
                    p.joins[0].right_col == 0 && p.joins[0].residual_eq.empty() && !p.sources[1].constrained() &&
@@ -1768,18 +1835,23 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         };
         for (auto& [name, r] : st->relations) {
             if (!(r->block_mode && r->levels_mode && r->arity == 2)) continue;
-            bool ok = true, any = false;
+            bool ok = !eng.dist() || (r->home == 1 && r->keyset == std::set<u32>{1});
+            bool any = false;
             for (auto& v : variants) {
                 const Plan& p = *v.plan;
+                const DistPlan& dp = dplans[v.plan_index];
                 const bool reads_delta = v.delta_source >= 0 && p.sources[v.delta_source].relation == name;
                 if (p.head == name && !p.joins.empty()) {
-                    if (reads_delta && composition(p, v.delta_source)) any = true;
+                    if (reads_delta && composition(p, v.delta_source) && (!eng.dist() || dp.local_out)) any = true;
                     else ok = false;
+                } else if (p.head == name) {
+                    if (eng.dist() && !dp.replicated_out) ok = false;
                 } else if (reads_delta) {
                     ok = false;
                 }
             }
             r->word_mode = ok && any;
+            if (r->word_mode && eng.dist()) r->owner_shift = 5;
         }
     }
 
@@ -1824,7 +1896,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         std::vector<u64> counts;  // per head: |Δ|, |FULL| (local, then global)
         for (auto& [name, pool] : pooled) {
             RelState& r = *st->relations.at(name);
-            if (eng.dist()) eng.route_pool(pool, r.home);
+            if (eng.dist()) eng.route_pool(pool, r.home, r.owner_shift);
             const u64 nd = r.hash_mode ? eng.hash_finalize(r, sinks[name], pool) : eng.dedup_merge_home(r, pool);
             if (eng.dist()) eng.forward_delta(r);
             counts.push_back(nd);
@@ -1926,6 +1998,18 @@ const DevVersion& sorted_rows(const EvalState& s, const RelState& r, DevVersion&
     if (!r.levels_mode) return r.full;
     Ctx* c = s.ctx;
     const u64 n = r.rows();
+    if (r.block_mode && r.blocks.capacity() && !std::getenv("FVLOG_DUMP_SORT")) {
+        // The block set holds FULL exactly: decode its bitmaps in row order
+        // (FVLOG_DUMP_SORT=1: concatenate the levels and radix-sort instead).
+        tmp.n = n;
+        tmp.cols.clear();
+        for (u32 j = 0; j < r.arity; ++j) tmp.cols.emplace_back(c, n);
+        const u64 got = engine_blockset_dump(c, r.blocks, r.arity, n ? tmp.cols[0].get() : nullptr,
+                                             r.arity == 2 && n ? tmp.cols[1].get() : nullptr);
+        if (got != n) fail(FV_ERR_INVALID, "block set holds " + std::to_string(got) + " rows, expected " +
+                                               std::to_string(n));
+        return tmp;
+    }
     // Levels are grouped by column 0 per iteration; one sort of their
     // concatenation gives the lexicographic dump (like dump_relation's std::sort).
     tmp.n = n;

@@ -124,6 +124,7 @@ struct BlockSet {
     DBuf<u64> dir;
     DBuf<u32> bits;
     DBuf<u32> dbits;  // word form: this iteration's new bits, same layout as `bits`
+    u64 generation = 0;  // directory growths so far (recorded word indices die with one)
     DBuf<u64> count;  // device: blocks claimed
     u64 mask = 0;
     u64 blocks = 0;   // host copy of `count` (last read)
@@ -184,6 +185,10 @@ struct RelState {
     // word form. Left when the block set turns out sparse (word_sparse).
     bool word_mode = false;
     bool word_sparse = false;
+    // Partitioned runs: the home column's owner is owner(v >> owner_shift).
+    // A word-form relation owns whole 32-value windows (shift 5), so every
+    // word of its DELTA lives on one rank.
+    u32 owner_shift = 0;
     // With hash dedup, a FULL no join reads is kept as levels: the past DELTAs
     // (one per iteration, grouped by column 0) plus the current `delta`,
     // concatenated and sorted only for dumps; otherwise it is `full`, merged
@@ -298,7 +303,8 @@ struct Filter {
     SlotRef a, b;
     u32 op = kFilterEq;
     u32 value = 0;  // kFilterConst: the constant; kFilterOwner: this rank
-    u32 world = 1;  // kFilterOwner: owner(a) = floor(hash32(a) * world / 2^32) must equal value
+    u32 world = 1;  // kFilterOwner: owner(a) = floor(hash32(a >> oshift) * world / 2^32) must equal value
+    u32 oshift = 0;  // kFilterOwner: RelState::owner_shift of the owning relation
 };
 
 struct OutSpec {
@@ -329,6 +335,7 @@ struct OutSpec {
     // instead of probing the local key set. remote_world = 0: all local.
     u32 remote_world = 0, remote_rank = 0;
     u32 remote_col = 0;  // head column whose owner decides (the home column)
+    u32 remote_oshift = 0;  // ... of its value >> remote_oshift
     // Key mode, one word, no key set: drop tile-local repeats and append the
     // tile's distinct keys at keys[0][*d_count ...].
     u32 tile_dedup = 0;
@@ -346,6 +353,7 @@ struct OutSpec {
     // *new_tuples.
     SlotRef wbits;
     u32* ovf_bits = nullptr;
+    u32* new_widx = nullptr;  // bitmap word index of each appended new word
     u64* new_tuples = nullptr;
 };
 
@@ -392,11 +400,20 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
 // are OR-ed into FULL and into the DELTA bitmap (s.dbits); a word's first
 // DELTA writer appends its key to new_keys[*d_new ...] and *d_tuples counts
 // the new bits; entries without a directory slot go to ovf/ovf_bits[*d_ovf ...].
+// new_widx (parallel to new_keys) records the entry's bitmap word index.
 void engine_blockset_word_insert(Ctx* c, const u64* keys, const u32* bits, u64 n, const BlockSetArgs& s,
-                                 u64* new_keys, u64* d_new, u64* d_tuples, u64* ovf, u32* ovf_bits, u64* d_ovf);
+                                 u64* new_keys, u32* new_widx, u64* d_new, u64* d_tuples, u64* ovf, u32* ovf_bits,
+                                 u64* d_ovf);
 // The merged DELTA masks of n word keys (each inserted this iteration), read
-// from s.dbits into out_bits and cleared there.
-void engine_blockset_collect(Ctx* c, const u64* keys, u64 n, const BlockSetArgs& s, u32* out_bits);
+// from s.dbits into out_bits and cleared there; widx (recorded word indices,
+// valid while the directory has not grown) or null (look the blocks up).
+void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, const BlockSetArgs& s, u32* out_bits);
+// Distinct block ids among n packed keys (directory sizing).
+u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity);
+// FULL of a block-set relation as lexicographically sorted SoA rows (c0, and
+// c1 for binary relations; null c0: count only), decoded from the bitmaps in
+// order — no sort of the tuples. Returns the row count.
+u64 engine_blockset_dump(Ctx* c, const BlockSet& s, u32 arity, u32* c0, u32* c1);
 // Tuples (x, z) of n word entries (x, z base, mask), entry order kept (so
 // entries grouped by x give tuples grouped by x); returns the tuple count.
 // out_x null: count only.
@@ -446,6 +463,7 @@ struct RouteKey {
     u32 shift = 0;
     u32 hi = 0;
     u64 mask = ~u64(0);
+    u32 oshift = 0;  // owner of v >> oshift (RelState::owner_shift)
 };
 // Group n rows by destination rank: u32 columns `c32` and u64 columns `c64`
 // are scattered into the matching *_out buffers (capacity n) so that rows for

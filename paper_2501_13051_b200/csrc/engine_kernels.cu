@@ -41,7 +41,8 @@ __device__ __forceinline__ bool pass_filters(const Filter* f, u32 n, u64 i, u64 
         if (f[k].op == kFilterConst) {
             if (a != f[k].value) return false;
         } else if (f[k].op == kFilterOwner) {
-            if (static_cast<u32>((static_cast<u64>(hash32(a)) * f[k].world) >> 32) != f[k].value) return false;
+            if (static_cast<u32>((static_cast<u64>(hash32(a >> f[k].oshift)) * f[k].world) >> 32) != f[k].value)
+                return false;
         } else {
             const u32 b = slot(f[k].b, i, p);
             if ((a == b) != (f[k].op == kFilterEq)) return false;
@@ -275,7 +276,8 @@ __device__ __forceinline__ u64 word_key_of(u64 key, u32 shift, u32* bit) {
 // directory slot are flagged in *ovf_mask.
 template <int N>
 __device__ __forceinline__ void blockset_word_items(const BlockSetArgs& s, u32 live, const u64 (&key)[N],
-                                                    const u32 (&bits)[N], u32* first, u32* ones, u32* ovf_mask) {
+                                                    const u32 (&bits)[N], u32* first, u32* ones, u32* ovf_mask,
+                                                    u32 (&widx)[N]) {
     u64 slot[N];
     u32 wi[N];
 #pragma unroll
@@ -316,6 +318,7 @@ __device__ __forceinline__ void blockset_word_items(const BlockSetArgs& s, u32 l
     u32 fm = 0, n1 = 0;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
+        widx[k] = static_cast<u32>(slot[k]);  // bitmap word index (valid until the directory grows)
         if (!nb[k]) continue;
         n1 += __popc(nb[k]);
         if (atomicOr(s.dbits + slot[k], nb[k]) == 0) fm |= 1u << k;
@@ -469,7 +472,7 @@ template <bool COMPACT, bool REMOTE, bool BLOCKS, bool WORDS>
 __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets, u64 o_begin, u64 total,
                                                  const u32* __restrict__ starts, const u64* __restrict__ tile_jlo,
                                                  const u64* __restrict__ tile_jhi, const OutSpec& spec, u64 t,
-                                                 MatShared& sh) {
+                                                 MatShared& sh, u32* __restrict__ s_acc) {
     u32* s_owner = sh.owner;
     unsigned long long* s_set = sh.set;
     u32* s_warp = sh.warp;
@@ -550,13 +553,42 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
             u32 wb[kMatItems], first, ones, ovf_mask;
 #pragma unroll
             for (int k = 0; k < kMatItems; ++k) wb[k] = ((keep_mask >> k) & 1u) ? slot(spec.wbits, ii[k], pp[k]) : 0;
+            if (spec.tile_set) {
+                // Tile-local combine: outputs of one tile that hit the same
+                // FULL word (one probe row's x with the same z word from
+                // several DELTA rows) OR their masks in shared memory; only
+                // the first of them goes to the global bitmap.
+                __syncthreads();  // s_set / s_acc initialised (the sparse path has no barrier before this)
+                u32 own = 0, joined = 0, hslot[kMatItems];
+#pragma unroll
+                for (int k = 0; k < kMatItems; ++k) {
+                    hslot[k] = 0;
+                    if (!((keep_mask >> k) & 1u)) continue;
+                    u32 h = static_cast<u32>(hs[k] >> 40) & (kMatSetSlots - 1);
+                    for (int probe = 0; probe < kMatSetProbes; ++probe) {
+                        const unsigned long long prev = atomicCAS(s_set + h, ~0ull, static_cast<unsigned long long>(key[k]));
+                        if (prev == ~0ull || prev == key[k]) {
+                            (prev == ~0ull ? own : joined) |= 1u << k;
+                            hslot[k] = h;
+                            atomicOr(s_acc + h, wb[k]);
+                            break;
+                        }
+                        h = (h + 1) & (kMatSetSlots - 1);
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < kMatItems; ++k)
+                    if ((own >> k) & 1u) wb[k] = s_acc[hslot[k]];
+                keep_mask &= ~joined;
+            }
             if (spec.probe_count) {
                 const u32 m = __reduce_add_sync(0xffffffffu, __popc(keep_mask));
                 if (lane == 0 && m) atomicAdd(reinterpret_cast<unsigned long long*>(spec.probe_count), static_cast<unsigned long long>(m));
             }
-            blockset_word_items(spec.bs, keep_mask, key, wb, &first, &ones, &ovf_mask);
-            append_words(spec.new_keys, static_cast<u32*>(nullptr), spec.new_count, spec.new_tuples, ones, first, key,
-                         wb);
+            u32 widx[kMatItems];
+            blockset_word_items(spec.bs, keep_mask, key, wb, &first, &ones, &ovf_mask, widx);
+            append_words(spec.new_keys, spec.new_widx, spec.new_count, spec.new_tuples, ones, first, key, widx);
             append_words(spec.ovf_keys, spec.ovf_bits, spec.ovf_count, static_cast<u64*>(nullptr), 0u, ovf_mask, key,
                          wb);
             return;
@@ -591,7 +623,8 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
                     const u32 hv = static_cast<u32>(spec.n_out < 2 ? key[k]
                                                     : spec.remote_col ? key[k] & ((u64(1) << spec.shift) - 1)
                                                                       : key[k] >> spec.shift);
-                    if (static_cast<u32>((static_cast<u64>(hash32(hv)) * spec.remote_world) >> 32) != spec.remote_rank)
+                    if (static_cast<u32>((static_cast<u64>(hash32(hv >> spec.remote_oshift)) * spec.remote_world) >> 32) !=
+                        spec.remote_rank)
                         remote_mask |= 1u << k;
                 }
             }
@@ -726,6 +759,7 @@ __global__ void __launch_bounds__(kMatBlock, BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_
                                                                  const u64* __restrict__ tile_jhi, u64 tiles,
                                                                  u32 group, OutSpec spec) {
     __shared__ MatShared sh;
+    extern __shared__ u32 s_acc[];  // word form only: combined masks of the tile set (kMatSetSlots, dynamic)
     const bool dedup = (BLOCKS ? spec.bs.dir != nullptr : spec.ht_slots != nullptr) || spec.tile_dedup;
     const u64 t0 = u64(blockIdx.x) * group;
     const u64 t1 = min(t0 + group, tiles);
@@ -734,11 +768,15 @@ __global__ void __launch_bounds__(kMatBlock, BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_
         const bool reset = dedup && (t == t0 || sh.set_fill > kMatSetSlots / 4);
         __syncthreads();  // every thread has read set_fill before it is cleared
         if (reset) {
-            for (u32 i = threadIdx.x; i < kMatSetSlots; i += kMatBlock) sh.set[i] = ~0ull;
+            for (u32 i = threadIdx.x; i < kMatSetSlots; i += kMatBlock) {
+                sh.set[i] = ~0ull;
+                if (WORDS) s_acc[i] = 0;
+            }
             if (threadIdx.x == 0) sh.set_fill = 0;
             __syncthreads();
         }
-        materialize_tile<COMPACT, REMOTE, BLOCKS, WORDS>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh);
+        materialize_tile<COMPACT, REMOTE, BLOCKS, WORDS>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh,
+                                                         s_acc);
     }
 }
 
@@ -1162,9 +1200,9 @@ __global__ void blockset_insert_kernel(const u64* __restrict__ keys, u64 n, Bloc
 // new_keys (new bits counted in *new_tuples), entries without a directory
 // slot go to the overflow list with their full mask.
 __global__ void blockset_word_insert_kernel(const u64* __restrict__ keys, const u32* __restrict__ bits_in, u64 n,
-                                            BlockSetArgs s, u64* __restrict__ new_keys, u64* new_count,
-                                            u64* new_tuples, u64* __restrict__ ovf, u32* __restrict__ ovf_bits,
-                                            u64* ovf_count) {
+                                            BlockSetArgs s, u64* __restrict__ new_keys, u32* __restrict__ new_widx,
+                                            u64* new_count, u64* new_tuples, u64* __restrict__ ovf,
+                                            u32* __restrict__ ovf_bits, u64* ovf_count) {
     constexpr int ITEMS = 4;
     const u64 base = u64(blockIdx.x) * blockDim.x * ITEMS + threadIdx.x;
     u64 key[ITEMS];
@@ -1185,21 +1223,29 @@ __global__ void blockset_word_insert_kernel(const u64* __restrict__ keys, const 
             live |= 1u << k;
         }
     }
-    u32 om, first, ones;
-    blockset_word_items(s, live, key, b, &first, &ones, &om);
-    append_words(new_keys, static_cast<u32*>(nullptr), new_count, new_tuples, ones, first, key, b);
+    u32 om, first, ones, widx[ITEMS];
+    blockset_word_items(s, live, key, b, &first, &ones, &om, widx);
+    append_words(new_keys, new_widx, new_count, new_tuples, ones, first, key, widx);
     append_words(ovf, ovf_bits, ovf_count, static_cast<u64*>(nullptr), 0u, om, key, b);
 }
 
 // DELTA's merged masks: entry i (a word first written this iteration) reads
-// its block's DELTA bitmap word and clears it for the next iteration.
-__global__ void blockset_collect_kernel(const u64* __restrict__ keys, u64 n, BlockSetArgs s, u32* __restrict__ out) {
+// its block's DELTA bitmap word and clears it for the next iteration. With
+// widx (no directory growth since the entries were appended) the word index
+// recorded at append time is used; otherwise the block is looked up.
+__global__ void blockset_collect_kernel(const u64* __restrict__ keys, const u32* __restrict__ widx, u64 n,
+                                        BlockSetArgs s, u32* __restrict__ out) {
     GRID_STRIDE(i, n) {
-        u32 bp;
-        const u64 bid = block_of(keys[i], s.shift, 2, &bp);
-        u64 h = block_home(bid, s.mask);
-        while (__ldcg(s.dir + h) != bid) h = (h + 1) & s.mask;  // present: inserted this iteration
-        const u64 w = h * 32 + (bp >> 5);
+        u64 w;
+        if (widx) {
+            w = widx[i];
+        } else {
+            u32 bp;
+            const u64 bid = block_of(keys[i], s.shift, 2, &bp);
+            u64 h = block_home(bid, s.mask);
+            while (__ldcg(s.dir + h) != bid) h = (h + 1) & s.mask;  // present: inserted this iteration
+            w = h * 32 + (bp >> 5);
+        }
         out[i] = s.dbits[w];
         s.dbits[w] = 0;
     }
@@ -1227,6 +1273,115 @@ struct ExpandWordsOp {
         }
     }
 };
+
+// Block ids of packed keys (the distinct count sizes a directory).
+__global__ void block_ids_kernel(const u64* __restrict__ keys, u64 n, u32 shift, u32 arity, u64* __restrict__ out) {
+    GRID_STRIDE(i, n) {
+        u32 bp;
+        out[i] = block_of(keys[i], shift, arity, &bp);
+    }
+}
+
+struct DistinctOp {
+    const u64* v;
+    __device__ u64 value(u64 i) const { return (i == 0 || v[i] != v[i - 1]) ? 1 : 0; }
+    __device__ void emit(u64, u64, u64) const {}
+};
+
+// ---- sorted rows straight from a block set (dumps of block-set relations) -----------
+//
+// The bitmaps hold FULL exactly, so the lexicographic dump needs no sort of
+// the tuples: the used directory slots are compacted and their block ids
+// radix-sorted (10^6 blocks for C2's 6.5·10^8 tuples), then every (block,
+// row) bitmap word is placed in row-major output order — for block row A
+// with blocks j0..j1 (ascending b), word r of block j is item
+// 32·j0 + r·(j1 - j0) + (j - j0) — its popcount prefix-summed and its bits
+// written as rows.
+
+struct BlockCompactOp {
+    const u64* dir;
+    u64* bids;
+    u32* slots;
+    __device__ u64 value(u64 i) const { return dir[i] != kEmptySlot ? 1 : 0; }
+    __device__ void emit(u64 i, u64 p, u64 v) const {
+        if (!v) return;
+        bids[p] = dir[i];
+        slots[p] = static_cast<u32>(i);
+    }
+};
+
+// First block of every block row (binary: bid >> 27) among the sorted ids.
+struct RowStartOp {
+    const u64* bids;
+    u32* starts;
+    __device__ u64 value(u64 j) const { return (j == 0 || (bids[j] >> 27) != (bids[j - 1] >> 27)) ? 1 : 0; }
+    __device__ void emit(u64 j, u64 p, u64 v) const {
+        if (v) starts[p] = static_cast<u32>(j);
+    }
+};
+
+__device__ __forceinline__ void block_item(const u32* __restrict__ starts, u64 rows, u64 m, u64 j, u32 r, u32 arity,
+                                           u64* g) {
+    if (arity != 2) {
+        *g = j * 32 + r;
+        return;
+    }
+    // block row of j: last start <= j
+    u64 lo = 0, hi = rows;
+    while (hi - lo > 1) {
+        const u64 mid = (lo + hi) >> 1;
+        if (starts[mid] <= j) lo = mid;
+        else hi = mid;
+    }
+    const u64 j0 = starts[lo], j1 = lo + 1 < rows ? starts[lo + 1] : m;
+    *g = 32 * j0 + u64(r) * (j1 - j0) + (j - j0);
+}
+
+__global__ void block_count_kernel(const u64* __restrict__ bids, const u32* __restrict__ slots,
+                                   const u32* __restrict__ bits, const u32* __restrict__ starts, u64 rows, u64 m,
+                                   u32 arity, u32* __restrict__ cnt) {
+    GRID_STRIDE(t, m * 32) {
+        const u64 j = t >> 5;
+        const u32 r = static_cast<u32>(t & 31);
+        u64 g;
+        block_item(starts, rows, m, j, r, arity, &g);
+        cnt[g] = __popc(bits[u64(slots[j]) * 32 + r]);
+    }
+}
+
+__global__ void block_expand_kernel(const u64* __restrict__ bids, const u32* __restrict__ slots,
+                                    const u32* __restrict__ bits, const u32* __restrict__ starts, u64 rows, u64 m,
+                                    u32 arity, const u64* __restrict__ off, u32* __restrict__ c0,
+                                    u32* __restrict__ c1) {
+    GRID_STRIDE(t, m * 32) {
+        const u64 j = t >> 5;
+        const u32 r = static_cast<u32>(t & 31);
+        u32 w = bits[u64(slots[j]) * 32 + r];
+        if (!w) continue;
+        u64 g;
+        block_item(starts, rows, m, j, r, arity, &g);
+        u64 pos = off[g];
+        const u64 bid = bids[j];
+        if (arity == 2) {
+            const u32 a = static_cast<u32>((bid >> 27) * 32 + r);
+            const u32 b0 = static_cast<u32>((bid & ((u64(1) << 27) - 1)) * 32);
+            while (w) {
+                const u32 b = __ffs(w) - 1;
+                w &= w - 1;
+                c0[pos] = a;
+                c1[pos] = b0 + b;
+                ++pos;
+            }
+        } else {
+            const u32 v0 = static_cast<u32>(bid * 1024 + r * 32);
+            while (w) {
+                const u32 b = __ffs(w) - 1;
+                w &= w - 1;
+                c0[pos++] = v0 + b;
+            }
+        }
+    }
+}
 
 // Directory growth: every used old slot re-homed in the new directory, its
 // 128-byte bitmap moved with 16-byte vector loads/stores. Block ids are
@@ -1536,7 +1691,7 @@ __device__ __forceinline__ u32 route_dest(const RouteKey& k, u64 i, u32 world) {
     u32 v;
     if (k.col) v = k.col[i];
     else v = static_cast<u32>(k.hi ? (k.word[i] >> k.shift) : (k.word[i] & k.mask));
-    return static_cast<u32>((static_cast<u64>(hash32(v)) * world) >> 32);
+    return static_cast<u32>((static_cast<u64>(hash32(v >> k.oshift)) * world) >> 32);
 }
 
 __global__ void route_count_kernel(RouteKey key, u64 n, u32 world, unsigned long long* counts) {
@@ -1641,33 +1796,102 @@ void engine_blockset_insert(Ctx* c, const u64* keys, u64 n, const BlockSetArgs& 
 }
 
 void engine_blockset_word_insert(Ctx* c, const u64* keys, const u32* bits, u64 n, const BlockSetArgs& s,
-                                 u64* new_keys, u64* d_new, u64* d_tuples, u64* ovf, u32* ovf_bits, u64* d_ovf) {
+                                 u64* new_keys, u32* new_widx, u64* d_new, u64* d_tuples, u64* ovf, u32* ovf_bits,
+                                 u64* d_ovf) {
     if (!n) return;
     ProfScope prof(c, "blockset_insert", (bits ? 12.0 : 8.0) * double(n));
     const unsigned grid = static_cast<unsigned>(ceil_div(n, u64(256) * 4));
-    blockset_word_insert_kernel<<<grid, 256, 0, c->stream>>>(keys, bits, n, s, new_keys, d_new, d_tuples, ovf,
-                                                             ovf_bits, d_ovf);
+    blockset_word_insert_kernel<<<grid, 256, 0, c->stream>>>(keys, bits, n, s, new_keys, new_widx, d_new, d_tuples,
+                                                             ovf, ovf_bits, d_ovf);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }
 
-void engine_blockset_collect(Ctx* c, const u64* keys, u64 n, const BlockSetArgs& s, u32* out_bits) {
+void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, const BlockSetArgs& s, u32* out_bits) {
     if (!n) return;
-    ProfScope prof(c, "blockset_collect", 20.0 * double(n));
-    blockset_collect_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, n, s, out_bits);
+    ProfScope prof(c, "blockset_collect", (widx ? 16.0 : 20.0) * double(n));
+    blockset_collect_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, widx, n, s, out_bits);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }
 
 u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u64 n, u32* out_x, u32* out_z) {
     if (!n) return 0;
-    u64* d = c->d_scalars + 36;
+    u64* d = c->d_scalars + 40;
     {
         ProfScope prof(c, "expand_words", 12.0 * double(n));
         tile_scan(c, ExpandWordsOp{x, zb, bits, out_x, out_z}, n, d);
     }
     u64 total = 0;
     c->read_scalars(d, &total, 1);
+    return total;
+}
+
+u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity) {
+    if (!n) return 0;
+    DBuf<u64> ids(c, n), alt(c, n);
+    {
+        ProfScope prof(c, "count_blocks", 16.0 * double(n));
+        block_ids_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, n, shift, arity, ids.get());
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+    }
+    if (radix_sort_keys_u64(c, ids.get(), alt.get(), n, 0, 54)) ids.swap(alt);
+    u64* d = c->d_scalars + 42;
+    tile_scan(c, DistinctOp{ids.get()}, n, d);
+    u64 m = 0;
+    c->read_scalars(d, &m, 1);
+    return m;
+}
+
+u64 engine_blockset_dump(Ctx* c, const BlockSet& s, u32 arity, u32* c0, u32* c1) {
+    const u64 cap = s.capacity();
+    if (!cap) return 0;
+    u64* d = c->d_scalars + 41;
+    DBuf<u64> bids(c, cap), bids_alt(c, cap);
+    DBuf<u32> slots(c, cap), slots_alt(c, cap);
+    u64 m = 0;
+    {
+        ProfScope prof(c, "blockset_dump", 8.0 * double(cap));
+        tile_scan(c, BlockCompactOp{s.dir.get(), bids.get(), slots.get()}, cap, d);
+    }
+    c->read_scalars(d, &m, 1);
+    if (!m) return 0;
+    // binary ids are (a >> 5) << 27 | (b >> 5): bits [0, 27) and [27, 54)
+    if (radix_sort_pairs_u64(c, bids.get(), bids_alt.get(), slots.get(), slots_alt.get(), m, 0, 54)) {
+        bids.swap(bids_alt);
+        slots.swap(slots_alt);
+    }
+    DBuf<u32> starts(c, arity == 2 ? m : 1);
+    u64 rows = 0;
+    if (arity == 2) {
+        tile_scan(c, RowStartOp{bids.get(), starts.get()}, m, d);
+        c->read_scalars(d, &rows, 1);
+    }
+    DBuf<u32> cnt(c, m * 32);
+    DBuf<u64> off(c, m * 32 + 1);
+    u64 total = 0;
+    {
+        ProfScope prof(c, "blockset_dump", 136.0 * double(m));
+        block_count_kernel<<<grid_for(m * 32), 256, 0, c->stream>>>(bids.get(), slots.get(), s.bits.get(),
+                                                                     starts.get(), rows, m, arity, cnt.get());
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+    }
+    exclusive_scan_counts(c, cnt.get(), off.get(), m * 32);
+    {
+        FV_CUDA(cudaMemcpyAsync(c->pinned, off.get() + m * 32, 8, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        total = c->pinned[0];
+    }
+    if (c0) {
+        ProfScope prof(c, "blockset_dump", 4.0 * double(arity) * double(total));
+        block_expand_kernel<<<grid_for(m * 32), 256, 0, c->stream>>>(bids.get(), slots.get(), s.bits.get(),
+                                                                      starts.get(), rows, m, arity, off.get(),
+                                                                      c0, c1);
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+    }
     return total;
 }
 
@@ -1894,9 +2118,21 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
     // Instantiations: filtered (COMPACT), partitioned routing (REMOTE) and
     // block-set dedup (BLOCKS) each keep their own register budget.
 #define FV_MAT_LAUNCH(C_, R_, B_) FV_MAT_LAUNCH_W(C_, R_, B_, false)
-#define FV_MAT_LAUNCH_W(C_, R_, B_, W_)                                                                    \
-    materialize_kernel<C_, R_, B_, W_><<<grid, kMatBlock, 0, c->stream>>>(offsets, m, o_begin, o_end, starts, \
-                                                                           jlo, jhi, tiles, group, spec)
+#define FV_MAT_LAUNCH_W(C_, R_, B_, W_)                                                                         \
+    do {                                                                                                        \
+        const size_t dyn = W_ ? sizeof(u32) * kMatSetSlots : 0;                                                 \
+        if (W_) {                                                                                               \
+            static const bool attr_set = [] {                                                                   \
+                return cudaFuncSetAttribute(materialize_kernel<C_, R_, B_, W_>,                                 \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,                        \
+                                            static_cast<int>(sizeof(u32) * kMatSetSlots)) == cudaSuccess;      \
+            }();                                                                                                \
+            if (!attr_set) fail(FV_ERR_CUDA, "materialize: dynamic shared memory attribute");                   \
+        }                                                                                                       \
+        materialize_kernel<C_, R_, B_, W_><<<grid, kMatBlock, dyn, c->stream>>>(offsets, m, o_begin, o_end,     \
+                                                                                 starts, jlo, jhi, tiles, group, \
+                                                                                 spec);                          \
+    } while (0)
     const bool blocks = spec.bs.dir != nullptr;
     const bool cmp = spec.n_filters != 0;
     const bool words = spec.wbits.ptr != nullptr;

@@ -93,6 +93,7 @@ struct Ctx {
     cudaMemPool_t pool = nullptr;
     std::string last_error;
     u64 launches = 0;
+    u64 syncs = 0;  // host synchronisations (sync / read_scalars): the per-iteration host round trips
     LookbackPool lb;
     u64* pinned = nullptr; // small pinned host buffer for scalar readbacks
     u64* d_scalars = nullptr; // device scalar slots

@@ -58,6 +58,7 @@ void Ctx::release(void* p) {
 }
 
 void Ctx::sync() {
+    ++syncs;
     FV_CUDA(cudaStreamSynchronize(stream));
     if (!prof_pending.empty()) prof_flush();
 }
@@ -130,6 +131,7 @@ u32 Ctx::lookback_epoch(u64 words, u32** tile_counter) {
 }
 
 void Ctx::read_scalars(const u64* d, u64* h, int n) {
+    ++syncs;
     FV_CUDA(cudaMemcpyAsync(pinned, d, sizeof(u64) * n, cudaMemcpyDeviceToHost, stream));
     FV_CUDA(cudaStreamSynchronize(stream));
     std::memcpy(h, pinned, sizeof(u64) * n);

@@ -196,6 +196,10 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
         }
         b = __shfl_sync(0xffffffffu, b, leader);
         rank[k] = b + __popc(peers & lanemask_lt());
+        // The next item's leader for this digit may be another lane: order
+        // this lane's counter update before its read (compute-sanitizer
+        // racecheck flagged the pair without it).
+        __syncwarp();
     }
     __syncthreads();
 

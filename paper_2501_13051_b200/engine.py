@@ -420,7 +420,19 @@ def owner(v: int, world: int) -> int:
     return int(_lib.lib().fv_owner(v, world))
 
 
+def _map_process_nccl() -> None:
+    """libfvlog binds the NCCL already mapped into the process (RTLD_NOLOAD)
+    and only loads libnccl.so.2 itself when there is none. Under PyTorch that
+    must be torch's bundled NCCL: once another libnccl.so.2 owns the soname,
+    torch's CUDA library cannot load. Importing torch first maps it."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _map_process_nccl()
     _bind()
     buf = C.create_string_buffer(128)
     check(_lib.lib().fv_nccl_unique_id(buf))
@@ -429,6 +441,7 @@ def nccl_unique_id() -> bytes:
 
 def set_nccl(ctx: Context, rank: int, world: int, uid: bytes) -> None:
     """Make later evaluations on ctx hash-partitioned over NCCL."""
+    _map_process_nccl()
     _bind()
     b = C.create_string_buffer(uid, 128)
     check(ctx._lib.fv_ctx_set_nccl(ctx.h, rank, world, b), ctx.h)
