@@ -1307,7 +1307,17 @@ public:
     // Word form: the iteration's new words become DELTA (columns x, z base,
     // mask, grouped by x; the counting sort also yields its column-0 join
     // index); returns |DELTA| in tuples.
+    // A first large insert into a block set with no growth history (a seed):
+    // measure its distinct blocks so the directory is sized before the
+    // insert instead of by overflow rounds.
+    void estimate_blocks(RelState& r, const CandPool& pool) {
+        if (!r.block_mode || r.blocks.ratio > 0 || pool.n < (u64(1) << 16) || block_ratio_ >= 0) return;
+        const u64 nb = engine_count_blocks(c_, pool.words[0].get(), pool.n, st_.key_shift, r.arity);
+        r.blocks.ratio = double(nb) / double(pool.n);
+    }
+
     u64 word_finalize(RelState& r, HeadSink& s, CandPool& pool) {
+        estimate_blocks(r, pool);
         if (pool.n) {
             hash_reserve(r, s, pool.n);
             engine_blockset_word_insert(c_, pool.words[0].get(), nullptr, pool.n, block_args(r), s.keys.get(),
@@ -1400,6 +1410,7 @@ public:
     // Sort the iteration's new keys into Δ and fold them into FULL.
     u64 hash_finalize(RelState& r, HeadSink& s, CandPool& pool) {
         if (r.word_mode) return word_finalize(r, s, pool);
+        estimate_blocks(r, pool);
         if (pool.n) {
             hash_reserve(r, s, pool.n);
             if (r.block_mode)
@@ -1856,11 +1867,15 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     }
 
     const bool trace = std::getenv("FVLOG_TRACE") != nullptr;
+    u64 syncs_seen = c->syncs;
     auto tr = [&](const char* what, Clock::time_point t, u64 it) {
         if (trace) {
+            // host syncs of the phase (the trace's own sync not counted)
+            const u64 phase_syncs = c->syncs - syncs_seen;
             c->sync();
-            std::fprintf(stderr, "[fvlog] it=%llu %-10s %.3f ms\n", static_cast<unsigned long long>(it), what,
-                         ms_since(t));
+            syncs_seen = c->syncs;
+            std::fprintf(stderr, "[fvlog] it=%llu %-10s %.3f ms  host syncs %llu\n", static_cast<unsigned long long>(it),
+                         what, ms_since(t), static_cast<unsigned long long>(phase_syncs));
         }
     };
     if (trace) tr("setup", t0, 0);
@@ -2090,6 +2105,8 @@ u64 fingerprint(const EvalState& s, const std::string& rel) {
     if (it == s.relations.end()) fail(FV_ERR_RANGE, "unknown relation '" + rel + "'");
     const RelState& r = *it->second;
     if (!r.levels_mode) return engine_fingerprint(s.ctx, r.full.ptrs(), r.full.n, r.arity);
+    if (r.block_mode && r.blocks.capacity() && !std::getenv("FVLOG_DUMP_SORT"))
+        return engine_blockset_fingerprint(s.ctx, r.blocks, r.arity);  // the bitmaps hold FULL exactly
     u64 h = 0;  // the fingerprint is a sum over rows: additive over levels
     for (const DevVersion* lv : levels_of(r)) {
         if (lv->cols.size() == r.arity + 1 && lv->n) {  // word form: fingerprint of its tuples

@@ -93,6 +93,9 @@ struct JoinIndex {
     u64 n_unique = 0;
     DBuf<u32> ukeys, ustart, ucount;
     HashIndex ht;
+    // domain > 0: direct-address index (from a counting-sort grouping):
+    // ustart/ucount have `domain` entries indexed by value, no ukeys/ht.
+    u64 domain = 0;
 };
 
 using IndexMap = std::map<std::pair<int, u32>, std::unique_ptr<JoinIndex>>;
@@ -408,6 +411,8 @@ void engine_blockset_word_insert(Ctx* c, const u64* keys, const u32* bits, u64 n
 // from s.dbits into out_bits and cleared there; widx (recorded word indices,
 // valid while the directory has not grown) or null (look the blocks up).
 void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, const BlockSetArgs& s, u32* out_bits);
+// fingerprint() of a block set's rows, from its bitmaps.
+u64 engine_blockset_fingerprint(Ctx* c, const BlockSet& s, u32 arity);
 // Distinct block ids among n packed keys (directory sizing).
 u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity);
 // FULL of a block-set relation as lexicographically sorted SoA rows (c0, and

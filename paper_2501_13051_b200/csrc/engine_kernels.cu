@@ -66,12 +66,20 @@ __device__ __forceinline__ bool ht_lookup(const u64* __restrict__ slots, u32 mas
 
 __global__ void probe_count_kernel(const u32* __restrict__ probe, u64 n, const u64* __restrict__ slots,
                                    u32 mask, const u32* __restrict__ ustart, const u32* __restrict__ ucount,
-                                   RowFilter pred, u32* __restrict__ starts, u32* __restrict__ counts) {
+                                   u64 domain, RowFilter pred, u32* __restrict__ starts, u32* __restrict__ counts) {
     GRID_STRIDE(i, n) {
         u32 s = 0, c = 0, r;
-        if (pass_filters(pred.f, pred.n, i, 0) && ht_lookup(slots, mask, probe[i], &r)) {
-            s = ustart[r];
-            c = ucount[r];
+        if (pass_filters(pred.f, pred.n, i, 0)) {
+            const u32 v = probe[i];
+            if (domain) {  // direct-address index: run of value v at ustart[v], ucount[v]
+                if (v < domain) {
+                    s = ustart[v];
+                    c = ucount[v];
+                }
+            } else if (ht_lookup(slots, mask, v, &r)) {
+                s = ustart[r];
+                c = ucount[r];
+            }
         }
         starts[i] = s;
         counts[i] = c;
@@ -464,6 +472,7 @@ struct MatShared {
     u64 base;
     u32 warp[kMatBlock / 32 + 1];
     u32 set_fill;                           // keys inserted into `set` since its last reset
+    unsigned long long tuples;              // word form: new tuples of this CTA (one global atomic at the end)
 };
 
 // One output tile of the output-partitioned join expansion (see lbs_kernel in
@@ -588,7 +597,12 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
             }
             u32 widx[kMatItems];
             blockset_word_items(spec.bs, keep_mask, key, wb, &first, &ones, &ovf_mask, widx);
-            append_words(spec.new_keys, spec.new_widx, spec.new_count, spec.new_tuples, ones, first, key, widx);
+            append_words(spec.new_keys, spec.new_widx, spec.new_count, static_cast<u64*>(nullptr), 0u, first, key,
+                         widx);
+            {
+                const u32 t = __reduce_add_sync(0xffffffffu, ones);
+                if (lane == 0 && t) atomicAdd(&sh.tuples, static_cast<unsigned long long>(t));
+            }
             append_words(spec.ovf_keys, spec.ovf_bits, spec.ovf_count, static_cast<u64*>(nullptr), 0u, ovf_mask, key,
                          wb);
             return;
@@ -751,8 +765,11 @@ constexpr int kMatGroup = 1;  // measured: 1 is best on C1-C4 (FVLOG_MAT_GROUP o
 #ifndef FV_MAT_MIN_BLOCKS_BS
 #define FV_MAT_MIN_BLOCKS_BS 2
 #endif
+#ifndef FV_MAT_MIN_BLOCKS_W
+#define FV_MAT_MIN_BLOCKS_W 2
+#endif
 template <bool COMPACT, bool REMOTE, bool BLOCKS, bool WORDS>
-__global__ void __launch_bounds__(kMatBlock, BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_MAT_MIN_BLOCKS) materialize_kernel(const u64* __restrict__ offsets, u64 m,
+__global__ void __launch_bounds__(kMatBlock, WORDS ? FV_MAT_MIN_BLOCKS_W : (BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_MAT_MIN_BLOCKS)) materialize_kernel(const u64* __restrict__ offsets, u64 m,
                                                                  u64 o_begin, u64 total,
                                                                  const u32* __restrict__ starts,
                                                                  const u64* __restrict__ tile_jlo,
@@ -763,6 +780,7 @@ __global__ void __launch_bounds__(kMatBlock, BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_
     const bool dedup = (BLOCKS ? spec.bs.dir != nullptr : spec.ht_slots != nullptr) || spec.tile_dedup;
     const u64 t0 = u64(blockIdx.x) * group;
     const u64 t1 = min(t0 + group, tiles);
+    if (WORDS && threadIdx.x == 0) sh.tuples = 0;  // ordered by the loop's first barrier
     for (u64 t = t0; t < t1; ++t) {
         __syncthreads();  // previous tile's shared reads/updates are done
         const bool reset = dedup && (t == t0 || sh.set_fill > kMatSetSlots / 4);
@@ -777,6 +795,10 @@ __global__ void __launch_bounds__(kMatBlock, BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_
         }
         materialize_tile<COMPACT, REMOTE, BLOCKS, WORDS>(offsets, o_begin, total, starts, tile_jlo, tile_jhi, spec, t, sh,
                                                          s_acc);
+    }
+    if (WORDS) {
+        __syncthreads();
+        if (threadIdx.x == 0 && sh.tuples) atomicAdd(reinterpret_cast<unsigned long long*>(spec.new_tuples), sh.tuples);
     }
 }
 
@@ -1114,7 +1136,52 @@ __global__ void fingerprint_kernel(Cols8 c, u32 arity, u64 n, unsigned long long
     if (lane_id() == 0) atomicAdd(out, acc);
 }
 
+// Fingerprint of a block set's rows straight from its bitmaps (the same sum
+// over rows as fingerprint_kernel): one thread per bitmap word.
+__global__ void blockset_fingerprint_kernel(const u64* __restrict__ dir, const u32* __restrict__ bits, u64 cap,
+                                            u32 arity, unsigned long long* out) {
+    unsigned long long acc = 0;
+    GRID_STRIDE(t, cap * 32) {
+        const u64 slot = t >> 5;
+        const u32 r = static_cast<u32>(t & 31);
+        const u64 bid = dir[slot];
+        if (bid == kEmptySlot) continue;
+        u32 w = bits[t];
+        while (w) {
+            const u32 b = __ffs(w) - 1;
+            w &= w - 1;
+            u64 h = 0x2545F4914F6CDD1Dull;
+            if (arity == 2) {
+                h = mix64(h ^ static_cast<u32>((bid >> 27) * 32 + r));
+                h = mix64(h ^ static_cast<u32>((bid & ((u64(1) << 27) - 1)) * 32 + b));
+            } else {
+                h = mix64(h ^ static_cast<u32>(bid * 1024 + r * 32 + b));
+            }
+            acc += h;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane_id() == 0) atomicAdd(out, acc);
+}
+
 }  // namespace
+
+u64 engine_blockset_fingerprint(Ctx* c, const BlockSet& s, u32 arity) {
+    const u64 cap = s.capacity();
+    if (!cap) return 0;
+    u64* d = c->d_scalars + 43;
+    FV_CUDA(cudaMemsetAsync(d, 0, 8, c->stream));
+    {
+        ProfScope prof(c, "fingerprint", 136.0 * double(cap));
+        blockset_fingerprint_kernel<<<grid_for(cap * 32), 256, 0, c->stream>>>(
+            s.dir.get(), s.bits.get(), cap, arity, reinterpret_cast<unsigned long long*>(d));
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+    }
+    u64 h = 0;
+    c->read_scalars(d, &h, 1);
+    return h;
+}
 
 namespace {
 
@@ -1233,21 +1300,34 @@ __global__ void blockset_word_insert_kernel(const u64* __restrict__ keys, const 
 // its block's DELTA bitmap word and clears it for the next iteration. With
 // widx (no directory growth since the entries were appended) the word index
 // recorded at append time is used; otherwise the block is looked up.
+constexpr int kCollectItems = 4;  // independent gathers in flight per thread
 __global__ void blockset_collect_kernel(const u64* __restrict__ keys, const u32* __restrict__ widx, u64 n,
                                         BlockSetArgs s, u32* __restrict__ out) {
-    GRID_STRIDE(i, n) {
-        u64 w;
+    const u64 base = u64(blockIdx.x) * blockDim.x * kCollectItems + threadIdx.x;
+    u64 w[kCollectItems];
+#pragma unroll
+    for (int k = 0; k < kCollectItems; ++k) {
+        const u64 i = base + u64(k) * blockDim.x;
+        w[k] = ~u64(0);
+        if (i >= n) continue;
         if (widx) {
-            w = widx[i];
+            w[k] = widx[i];
         } else {
             u32 bp;
             const u64 bid = block_of(keys[i], s.shift, 2, &bp);
             u64 h = block_home(bid, s.mask);
             while (__ldcg(s.dir + h) != bid) h = (h + 1) & s.mask;  // present: inserted this iteration
-            w = h * 32 + (bp >> 5);
+            w[k] = h * 32 + (bp >> 5);
         }
-        out[i] = s.dbits[w];
-        s.dbits[w] = 0;
+    }
+    u32 v[kCollectItems];
+#pragma unroll
+    for (int k = 0; k < kCollectItems; ++k) v[k] = w[k] != ~u64(0) ? __ldcg(s.dbits + w[k]) : 0;
+#pragma unroll
+    for (int k = 0; k < kCollectItems; ++k) {
+        if (w[k] == ~u64(0)) continue;
+        out[base + u64(k) * blockDim.x] = v[k];
+        s.dbits[w[k]] = 0;
     }
 }
 
@@ -1627,8 +1707,12 @@ struct GroupRunsOp {
 struct GroupBaseOp {
     const u32* cnt;
     u64* base;
+    u32* base32;  // optional: the run starts as u32 (direct-address join index)
     __device__ u64 value(u64 i) const { return cnt[i]; }
-    __device__ void emit(u64 i, u64 p, u64) const { base[i] = p; }
+    __device__ void emit(u64 i, u64 p, u64) const {
+        base[i] = p;
+        if (base32) base32[i] = static_cast<u32>(p);
+    }
 };
 
 __global__ void unpack_keys_kernel(const u64* __restrict__ keys, u64 n, u32 arity, u32 shift, u32* c0, u32* c1) {
@@ -1810,7 +1894,8 @@ void engine_blockset_word_insert(Ctx* c, const u64* keys, const u32* bits, u64 n
 void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, const BlockSetArgs& s, u32* out_bits) {
     if (!n) return;
     ProfScope prof(c, "blockset_collect", (widx ? 16.0 : 20.0) * double(n));
-    blockset_collect_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, widx, n, s, out_bits);
+    blockset_collect_kernel<<<static_cast<unsigned>(ceil_div(n, u64(256) * kCollectItems)), 256, 0, c->stream>>>(
+        keys, widx, n, s, out_bits);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }
@@ -1946,7 +2031,7 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
     if (shift > kGroupMaxBits || n > (u64(kGroupMaxPerValue) << shift)) return false;
     if (n <= 1) return false;  // already grouped; the caller indexes it the usual way
     const u64 domain = u64(1) << shift;
-    DBuf<u32> cnt(c, domain), cursor(c, domain);
+    DBuf<u32> cnt(c, domain), cursor(c, domain), base32(c, runs ? domain : 0);
     DBuf<u64> base(c, domain), out(c, col0 ? 0 : n);
     FV_CUDA(cudaMemsetAsync(cnt.get(), 0, 4 * domain, c->stream));
     FV_CUDA(cudaMemsetAsync(cursor.get(), 0, 4 * domain, c->stream));
@@ -1954,7 +2039,7 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
         ProfScope prof(c, "group_keys", double(n) * 8.0 * 3.0);
         group_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys.get(), n, shift, cnt.get());
         FV_CUDA(cudaGetLastError());
-        tile_scan(c, GroupBaseOp{cnt.get(), base.get()}, domain, nullptr);
+        tile_scan(c, GroupBaseOp{cnt.get(), base.get(), runs ? base32.get() : nullptr}, domain, nullptr);
         group_scatter_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys.get(), n, shift, base.get(), cursor.get(),
                                                                   out.get(), col0, col1, pay_in, pay_out);
         FV_CUDA(cudaGetLastError());
@@ -1962,14 +2047,15 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
     }
     if (!col0) keys.swap(out);
     if (runs) {
-        DBuf<u32> uk(c, std::min<u64>(n, domain)), us(c, std::min<u64>(n, domain)), uc(c, std::min<u64>(n, domain));
-        u64* d = c->d_scalars + 34;
-        tile_scan(c, GroupRunsOp{cnt.get(), base.get(), uk.get(), us.get(), uc.get()}, domain, d);
-        c->read_scalars(d, &runs->n_unique, 1);
-        runs->ukeys = std::move(uk);
-        runs->ustart = std::move(us);
-        runs->ucount = std::move(uc);
-        build_run_hash(c, *runs);
+        // Direct-address run index over the value domain: the run of value v
+        // is (base32[v], cnt[v]) — no compaction, no hash table, no host
+        // readback of the run count.
+        runs->domain = domain;
+        runs->n_unique = n;  // not counted; non-zero marks a non-empty index
+        runs->ustart = std::move(base32);
+        runs->ucount = std::move(cnt);
+        runs->ukeys = DBuf<u32>();
+        runs->ht = HashIndex();
     }
     return true;
 }
@@ -2071,7 +2157,7 @@ void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, c
     }
     ProfScope prof(c, "join_probe_count", double(n) * 20.0);
     probe_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(probe, n, idx.ht.slots.get(), idx.ht.mask,
-                                                            idx.ustart.get(), idx.ucount.get(), pred,
+                                                            idx.ustart.get(), idx.ucount.get(), idx.domain, pred,
                                                             starts, counts);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
