@@ -527,6 +527,59 @@ public:
 
     // ---- execute_plan (P/src/engine.cpp:72-146) for one variant ------------------
 
+    // Join step k of plan p is a word composition: the right atom is binary,
+    // unconstrained, joined on its column 0 with nothing else to check, and
+    // the head is (left-side column, right atom's column 1) with no guard.
+    static bool word_step_ok(const Plan& p, size_t k) {
+        const PlanJoin& j = p.joins[k];
+        const u32 R = j.right_source;
+        return k + 1 == p.joins.size() && p.sources[R].arity == 2 && !p.sources[R].constrained() &&
+               j.right_col == 0 && j.residual_eq.empty() && p.guard_neq.empty() && p.head_arity == 2 &&
+               p.output_cols.size() == 2 && p.output_cols[1] == ColRef{R, 1} && p.output_cols[0].source != R;
+    }
+
+    // Word form of a binary version of r (home copy) with its column-0 join
+    // index, cached until the version changes. Built from the lexicographic
+    // order when the version has it, else from a sorted copy.
+    WordBuild& word_build(RelState& r, Which which) {
+        if (which == kOld && r.old_is_full) which = kFull;
+        auto it = r.word_builds.find(static_cast<int>(which));
+        if (it != r.word_builds.end()) return *it->second;
+        const DevVersion& v = version(r, r.home, which);
+        auto wb = std::make_unique<WordBuild>();
+        const u64 n = v.n;
+        DevVersion sorted;
+        const DevVersion* src = &v;
+        if (!v.lex_sorted && n > 1) {
+            std::vector<DBuf<u64>> words;
+            words.emplace_back(c_, n);
+            u64* wp = words[0].get();
+            engine_pack_keys(c_, v.ptrs(), n, st_.key_shift, &wp);
+            engine_sort_keys(c_, words, n, 2, st_.key_shift);
+            sorted.n = n;
+            sorted.cols.emplace_back(c_, n);
+            sorted.cols.emplace_back(c_, n);
+            std::vector<u32*> dc{sorted.cols[0].get(), sorted.cols[1].get()};
+            engine_unpack_keys(c_, words[0].get(), n, 2, st_.key_shift, dc);
+            src = &sorted;
+        }
+        for (int j = 0; j < 3; ++j) wb->words.cols.emplace_back(c_, std::max<u64>(n, 1));
+        wb->words.n = n ? engine_tuples_to_words(c_, src->cols[0].get(), src->cols[1].get(), n,
+                                                 wb->words.cols[0].get(), wb->words.cols[1].get(),
+                                                 wb->words.cols[2].get())
+                        : 0;
+        wb->words.lex_sorted = true;
+        wb->idx.rows = &wb->words;
+        engine_build_runs(c_, wb->words.cols[0].get(), wb->words.n, wb->idx);
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   word build of %s (%s): %llu rows -> %llu words\n", r.name.c_str(),
+                         which == kDelta ? "delta" : (which == kOld ? "old" : "full"),
+                         static_cast<unsigned long long>(n), static_cast<unsigned long long>(wb->words.n));
+        WordBuild& ref = *wb;
+        r.word_builds.emplace(static_cast<int>(which), std::move(wb));
+        return ref;
+    }
+
     // One variant's execution state (execute_plan, P/src/engine.cpp:72-146).
     struct VarRun {
         const Plan& plan;
@@ -625,10 +678,15 @@ public:
         if (D && dp.shuffle[k]) cur = shuffle(cur, jn.left);
         std::unique_ptr<JoinIndex> tmp;
         JoinIndex* idx;
+        const bool word_step = k + 1 == nj && !D && word_step_ok(plan, k);
         if (plan.sources[R].constrained()) {
             tmp = std::make_unique<JoinIndex>();
             build_index_on(*v.ver[R], jn.right_col, *tmp, &plan.sources[R]);
             idx = tmp.get();
+        } else if (word_step && v.ver[R]->cols.size() == 2 && rel(plan.head).word_sink) {
+            // Composition into a word sink: probe the word form of the build
+            // version (x, z base, mask), one output per word.
+            idx = &word_build(rr, v.which[R]).idx;
         } else {
             idx = &index(rr, rpart ? dp.src_copy[R] : 0, v.which[R], jn.right_col);
         }
@@ -725,12 +783,14 @@ public:
                         spec.ovf_count = sink->counter.get() + 1;
                         spec.tile_set = block_tile_set_;
                         spec.wbits = SlotRef();
-                        if (hr.word_mode) {
-                            // Word-form composition: the build side is DELTA's
-                            // words (x, z base, mask); one output per word.
-                            if (idx->rows->cols.size() != hr.arity + 1)
-                                fail(FV_ERR_INVALID, "word-form head joined without a word-form DELTA");
-                            spec.wbits = SlotRef{idx->rows->cols[hr.arity].get(), 1};
+                        spec.word_sink = 0;
+                        if (hr.word_sink) {
+                            // Word sink: a composition step whose build side
+                            // is in word form (x, z base, mask) emits one
+                            // output per word; other joins emit their tuples
+                            // as one-bit words.
+                            if (idx->rows->cols.size() == 3) spec.wbits = SlotRef{idx->rows->cols[2].get(), 1};
+                            spec.word_sink = 1;
                             spec.ovf_bits = sink->ovf_bits.get();
                             spec.new_tuples = sink->counter.get() + 2;
                             spec.new_widx = sink->widx.get();
@@ -904,6 +964,7 @@ public:
             delta.n = 0;
             delta.cols.resize(arity);
             indexes.clear();
+            if (home) home->word_builds.clear();
             if (home) set_old(*home, nullptr);
             return 0;
         }
@@ -927,6 +988,8 @@ public:
         c_->prof_add_bytes("merge_dedup", 8.0 * double(nd) * arity);
         C.n = full.n + nd;
         Dv.n = nd;
+        C.lex_sorted = Dv.lex_sorted = true;  // merge-path output of sorted inputs
+        if (home) home->word_builds.clear();
         if (home && nd) {
             set_old(*home, &full);
         } else if (home) {
@@ -936,6 +999,12 @@ public:
         delta = std::move(Dv);
         indexes.clear();
         return nd;
+    }
+
+    // A relation's versions changed: its join indexes and word builds go.
+    static void invalidate(RelState& r) {
+        r.indexes.clear();
+        r.word_builds.clear();
     }
 
     // The FULL a merge is about to replace becomes FULL - DELTA (moved, no
@@ -1154,11 +1223,11 @@ public:
         if (force_blocks_ < 0 && bytes > block_sparse_bytes_ && bytes > kBlockSparseFactor * keyset_bytes) {
             // A word-form relation cannot switch mid-iteration (its DELTA is
             // words): it grows and leaves the word form at the next finalize.
-            if (!r.word_mode) return false;
+            if (!r.word_sink) return false;
             r.word_sparse = true;
         }
         BlockSet ns;
-        engine_blockset_alloc(c_, ns, cap, b.blocks, r.word_mode);
+        engine_blockset_alloc(c_, ns, cap, b.blocks, r.word_sink);
         ns.ratio = b.ratio;
         ns.generation = b.generation + 1;
         if (b.capacity()) engine_blockset_grow(c_, b, ns);
@@ -1189,7 +1258,7 @@ public:
                 convert_to_keyset(r, &s, tmp.get(), n);
                 return;
             }
-            if (r.word_mode) {
+            if (r.word_sink) {
                 DBuf<u32> tb(c_, n);
                 FV_CUDA(cudaMemcpyAsync(tb.get(), s.ovf_bits.get(), 4 * n, cudaMemcpyDeviceToDevice, c_->stream));
                 engine_blockset_word_insert(c_, tmp.get(), tb.get(), n, block_args(r), s.keys.get(), s.widx.get(),
@@ -1214,7 +1283,7 @@ public:
             DBuf<u64> nk(c_, nc);
             if (have) FV_CUDA(cudaMemcpyAsync(nk.get(), s.keys.get(), 8 * have, cudaMemcpyDeviceToDevice, c_->stream));
             s.keys = std::move(nk);
-            if (r.word_mode) {
+            if (r.word_sink) {
                 DBuf<u32> nw_idx(c_, nc);
                 if (have)
                     FV_CUDA(cudaMemcpyAsync(nw_idx.get(), s.widx.get(), 4 * have, cudaMemcpyDeviceToDevice, c_->stream));
@@ -1228,7 +1297,7 @@ public:
         }
         if (s.ovf_cap < extra) {
             s.ovf = DBuf<u64>(c_, extra);
-            if (r.word_mode) s.ovf_bits = DBuf<u32>(c_, extra);
+            if (r.word_sink) s.ovf_bits = DBuf<u32>(c_, extra);
             s.ovf_cap = extra;
         }
         s.bound = nw + extra;
@@ -1334,7 +1403,24 @@ public:
             }
         }
         const u64 tuples = s.counter.get() ? s.tuples : 0;
-        r.indexes.clear();
+        if (!r.word_mode) {
+            // Word sink with a tuple DELTA: the merged words of the
+            // iteration expand to packed tuple keys, then the usual path.
+            DBuf<u64> tk(c_, std::max<u64>(tuples, 1));
+            if (nw) {
+                s.bits = DBuf<u32>(c_, nw);
+                const bool idx_ok = s.gen0 == r.blocks.generation && r.blocks.capacity() <= (u64(1) << 27);
+                engine_blockset_collect(c_, s.keys.get(), idx_ok ? s.widx.get() : nullptr, nw, block_args(r),
+                                        s.bits.get());
+                engine_expand_word_keys(c_, s.keys.get(), s.bits.get(), nw, tk.get());
+            }
+            s.keys = DBuf<u64>();
+            s.cap = 0;
+            const u64 nd = finish_delta(r, std::move(tk), tuples);
+            if (r.word_sparse) leave_word_mode(r);
+            return nd;
+        }
+        invalidate(r);
         if (r.delta.n) r.levels.push_back(std::move(r.delta));
         DevVersion Dv;
         Dv.n = nw;
@@ -1400,8 +1486,9 @@ public:
     void leave_word_mode(RelState& r) {
         to_tuples(r.delta, r.arity);
         for (auto& lv : r.levels) to_tuples(lv, r.arity);
-        r.indexes.clear();
+        invalidate(r);
         r.word_mode = false;
+        r.word_sink = false;
         r.word_sparse = false;
         if (trace_) std::fprintf(stderr, "[fvlog]   %s leaves the word form\n", r.name.c_str());
         convert_to_keyset(r, nullptr, nullptr, 0);
@@ -1409,7 +1496,7 @@ public:
 
     // Sort the iteration's new keys into Δ and fold them into FULL.
     u64 hash_finalize(RelState& r, HeadSink& s, CandPool& pool) {
-        if (r.word_mode) return word_finalize(r, s, pool);
+        if (r.word_sink) return word_finalize(r, s, pool);
         estimate_blocks(r, pool);
         if (pool.n) {
             hash_reserve(r, s, pool.n);
@@ -1433,7 +1520,15 @@ public:
                              double(s.candidates) / double(std::max<u64>(nd, 1)));
             if (want != r.keys.group_bits) relayout_keys(r, want);
         }
-        r.indexes.clear();
+        DBuf<u64> keys = std::move(s.keys);
+        s.cap = 0;
+        return finish_delta(r, std::move(keys), nd);
+    }
+
+    // The iteration's nd new packed tuple keys become DELTA (grouped by
+    // column 0 in levels mode, sorted and merged into FULL otherwise).
+    u64 finish_delta(RelState& r, DBuf<u64>&& new_keys, u64 nd) {
+        invalidate(r);
         DevVersion Dv;
         Dv.n = nd;
         for (u32 j = 0; j < r.arity; ++j) Dv.cols.emplace_back(c_, nd);
@@ -1447,8 +1542,7 @@ public:
         }
         r.keys.count += nd;
         std::vector<DBuf<u64>> words;
-        words.push_back(std::move(s.keys));
-        s.cap = 0;
+        words.push_back(std::move(new_keys));
         // Levels-mode FULL is never merged, so Δ only has to be grouped by
         // column 0 (its join index): unary keys are distinct (already
         // grouped), binary keys take a counting sort on column 0 when its
@@ -1489,6 +1583,8 @@ public:
             u64* d_new = c_->d_scalars + 23;
             engine_merge(c_, r.full.ptrs(), r.full.n, bw.data(), nd, r.arity, st_.key_shift, cc, uc, d_new);
             C.n = r.full.n + nd;
+            C.lex_sorted = true;
+            Dv.lex_sorted = true;  // unpacked from the sorted keys
             set_old(r, &r.full);
             r.full = std::move(C);
         }
@@ -1826,42 +1922,61 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         r->levels_mode = r->hash_mode && !full_read.count(name);
         r->block_mode = r->hash_mode && eng.blocks_enabled();
     }
-    // Word form (RelState::word_mode): a binary block-set relation whose
-    // DELTA is only ever read by composition variants of itself — two atoms
-    // A(x, y), DELTA(y, z) -> head(x, z), joined on DELTA's column 0 with
-    // nothing else to check (right-linear TC) — and whose other derivations
-    // are single-atom copies (pooled). FVLOG_WORDS=0 disables.
-    // Partitioned runs additionally need every derivation of the head to stay
-    // where it is produced — the composition variants local (homed on the
-    // column they carry, z) and the copies replicated (owner-filtered) — and
-    // no partition copies; the home column's owner is then taken over 32-value
-    // windows (owner_shift 5) so a word never straddles two ranks.
+    // Word sinks (RelState::word_sink, single GPU): binary block-set
+    // relations that head at least one word composition step (a last join
+    // step whose right atom is joined on its column 0 and gives the head's
+    // column 1, Engine::word_step_ok) take every insert as words.
+    // Word DELTA (RelState::word_mode): a levels-mode word sink whose DELTA is
+    // only ever read as the right atom of such a step into a word sink — e.g.
+    // right-linear TC, reach(x, z) :- edge(x, y), reach(y, z) — keeps DELTA
+    // and the levels as words. FVLOG_WORDS=0 disables both.
+    // Partitioned runs: only the word DELTA of a relation whose every
+    // derivation stays where it is produced — the composition variants local
+    // (homed on the column they carry, z) and the copies replicated
+    // (owner-filtered) — with no partition copies; the home column's owner is
+    // then taken over 32-value windows (owner_shift 5) so a word never
+    // straddles two ranks.
     const char* words_env = std::getenv("FVLOG_WORDS");
     if (!(words_env && std::string(words_env) == "0")) {
-        auto composition = [](const Plan& p, long d) {
-            return p.sources.size() == 2 && d == 1 && p.joins.size() == 1 && p.joins[0].right_source == 1 &&
-                   p.joins[0].right_col == 0 && p.joins[0].residual_eq.empty() && !p.sources[1].constrained() &&
-                   p.guard_neq.empty() && p.head_arity == 2 && p.output_cols.size() == 2 &&
-                   p.output_cols[1] == ColRef{1, 1} && p.output_cols[0].source == 0;
-        };
+        auto last_step = [](const Plan& p) { return p.joins.size() - 1; };
+        if (!eng.dist()) {
+            for (auto& v : variants) {
+                const Plan& p = *v.plan;
+                RelState& h = *st->relations.at(p.head);
+                if (h.block_mode && h.arity == 2 && !p.joins.empty() && Engine::word_step_ok(p, last_step(p)))
+                    h.word_sink = true;
+            }
+        }
         for (auto& [name, r] : st->relations) {
             if (!(r->block_mode && r->levels_mode && r->arity == 2)) continue;
+            if (!eng.dist() && !r->word_sink) continue;
             bool ok = !eng.dist() || (r->home == 1 && r->keyset == std::set<u32>{1});
             bool any = false;
             for (auto& v : variants) {
                 const Plan& p = *v.plan;
                 const DistPlan& dp = dplans[v.plan_index];
                 const bool reads_delta = v.delta_source >= 0 && p.sources[v.delta_source].relation == name;
-                if (p.head == name && !p.joins.empty()) {
-                    if (reads_delta && composition(p, v.delta_source) && (!eng.dist() || dp.local_out)) any = true;
-                    else ok = false;
-                } else if (p.head == name) {
-                    if (eng.dist() && !dp.replicated_out) ok = false;
-                } else if (reads_delta) {
-                    ok = false;
+                const bool composes = reads_delta && !p.joins.empty() &&
+                                      static_cast<u32>(v.delta_source) == p.joins[last_step(p)].right_source &&
+                                      Engine::word_step_ok(p, last_step(p));
+                if (eng.dist()) {
+                    // only the exchange-free TC shape: head == r, composition local, copies replicated
+                    if (p.head == name && !p.joins.empty()) {
+                        if (composes && p.sources.size() == 2 && dp.local_out) any = true;
+                        else ok = false;
+                    } else if (p.head == name) {
+                        if (!dp.replicated_out) ok = false;
+                    } else if (reads_delta) {
+                        ok = false;
+                    }
+                    continue;
                 }
+                if (!reads_delta) continue;
+                if (composes && st->relations.at(p.head)->word_sink) any = true;
+                else ok = false;
             }
             r->word_mode = ok && any;
+            if (r->word_mode) r->word_sink = true;
             if (r->word_mode && eng.dist()) r->owner_shift = 5;
         }
     }

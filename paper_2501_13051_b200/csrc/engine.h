@@ -79,6 +79,9 @@ struct FactsBlock {
 struct DevVersion {
     u64 n = 0;
     std::vector<DBuf<u32>> cols;
+    // Rows in lexicographic (col 0, col 1, ...) order (sorted FULL / DELTA,
+    // seeded EDB): a word build of it needs no sort.
+    bool lex_sorted = false;
     std::vector<const u32*> ptrs() const {
         std::vector<const u32*> p;
         for (auto& c : cols) p.push_back(c.get());
@@ -99,6 +102,14 @@ struct JoinIndex {
 };
 
 using IndexMap = std::map<std::pair<int, u32>, std::unique_ptr<JoinIndex>>;
+
+// A binary version in word form for the build side of a composition join
+// (RelState::word_builds): columns (x, z & ~31, mask) grouped by x, with its
+// join index on column 0.
+struct WordBuild {
+    DevVersion words;
+    JoinIndex idx;
+};
 
 // Open-addressing set of packed row keys (empty slot = all ones, which no
 // key can equal when 2 * shift < 64), load factor <= 1/2 (3/4 when memory
@@ -188,6 +199,15 @@ struct RelState {
     // word form. Left when the block set turns out sparse (word_sparse).
     bool word_mode = false;
     bool word_sparse = false;
+    // Word sink (block mode, binary, single GPU): every insert into the
+    // relation goes through the word protocol (FULL bitmap OR + per-block
+    // DELTA bitmap, first writer appends), so composition joins can emit
+    // whole words into it; with word_mode off its DELTA is expanded back to
+    // tuples at finalize. word_mode implies word_sink.
+    bool word_sink = false;
+    // Word forms of this relation's versions built for composition joins
+    // (key: Which), invalidated with `indexes`.
+    std::map<int, std::unique_ptr<WordBuild>> word_builds;
     // Partitioned runs: the home column's owner is owner(v >> owner_shift).
     // A word-form relation owns whole 32-value windows (shift 5), so every
     // word of its DELTA lives on one rank.
@@ -355,6 +375,7 @@ struct OutSpec {
     // carry their masks in ovf_bits, and the new tuples (bits) are counted in
     // *new_tuples.
     SlotRef wbits;
+    u32 word_sink = 0;  // the head is a word sink (WORDS kernel; wbits null: one-bit words)
     u32* ovf_bits = nullptr;
     u32* new_widx = nullptr;  // bitmap word index of each appended new word
     u64* new_tuples = nullptr;
@@ -415,6 +436,12 @@ void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, co
 u64 engine_blockset_fingerprint(Ctx* c, const BlockSet& s, u32 arity);
 // Distinct block ids among n packed keys (directory sizing).
 u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity);
+// Packed tuple keys of n word entries (word key, mask) into out, sized by
+// the caller to the sum of the masks' popcounts (no host readback).
+void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out);
+// Word form (x, z base, mask) of a lexicographically sorted binary version
+// of n rows; outputs sized n; returns the word count.
+u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits);
 // FULL of a block-set relation as lexicographically sorted SoA rows (c0, and
 // c1 for binary relations; null c0: count only), decoded from the bitmaps in
 // order — no sort of the tuples. Returns the row count.

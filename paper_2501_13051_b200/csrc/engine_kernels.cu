@@ -560,8 +560,20 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
             // Word form: each output is a whole DELTA word; OR it into FULL's
             // bitmap and append the bits that were new.
             u32 wb[kMatItems], first, ones, ovf_mask;
+            if (spec.wbits.ptr) {
 #pragma unroll
-            for (int k = 0; k < kMatItems; ++k) wb[k] = ((keep_mask >> k) & 1u) ? slot(spec.wbits, ii[k], pp[k]) : 0;
+                for (int k = 0; k < kMatItems; ++k) wb[k] = ((keep_mask >> k) & 1u) ? slot(spec.wbits, ii[k], pp[k]) : 0;
+            } else {
+                // tuple candidates into a word sink: one-bit words
+#pragma unroll
+                for (int k = 0; k < kMatItems; ++k) {
+                    wb[k] = 0;
+                    if ((keep_mask >> k) & 1u) {
+                        key[k] = word_key_of(key[k], spec.shift, &wb[k]);
+                        hs[k] = keyset_line_hash(key[k], spec.ht_group_bits);
+                    }
+                }
+            }
             if (spec.tile_set) {
                 // Tile-local combine: outputs of one tile that hit the same
                 // FULL word (one probe row's x with the same z word from
@@ -1331,6 +1343,47 @@ __global__ void blockset_collect_kernel(const u64* __restrict__ keys, const u32*
     }
 }
 
+// Packed tuple keys of n word entries (word key, mask), in entry order.
+struct ExpandWordKeysOp {
+    const u64* keys;
+    const u32* bits;
+    u64* out;
+    __device__ u64 value(u64 i) const { return __popc(bits[i]); }
+    __device__ void emit(u64 i, u64 p, u64 v) const {
+        if (!v) return;
+        const u64 k = keys[i];  // (x << shift) | zb, zb a multiple of 32
+        u32 m = bits[i];
+        while (m) {
+            const u32 b = __ffs(m) - 1;
+            m &= m - 1;
+            out[p++] = k + b;
+        }
+    }
+};
+
+// Words of a lexicographically sorted binary version: one entry per run of
+// rows with the same (x, z >> 5) (runs are at most 32 rows: rows are distinct).
+struct TuplesToWordsOp {
+    const u32* c0;
+    const u32* c1;
+    u64 n;
+    u32* x;
+    u32* zb;
+    u32* bits;
+    __device__ u64 value(u64 i) const {
+        return (i == 0 || c0[i] != c0[i - 1] || (c1[i] >> 5) != (c1[i - 1] >> 5)) ? 1 : 0;
+    }
+    __device__ void emit(u64 i, u64 p, u64 v) const {
+        if (!v) return;
+        const u32 a = c0[i], w = c1[i] >> 5;
+        u32 m = 0;
+        for (u64 j = i; j < n && c0[j] == a && (c1[j] >> 5) == w; ++j) m |= 1u << (c1[j] & 31);
+        x[p] = a;
+        zb[p] = w << 5;
+        bits[p] = m;
+    }
+};
+
 // Tuples of word entries (x, z base, mask), in entry order: entry i's set
 // bits become rows (x, base + bit) at its prefix of the popcounts.
 struct ExpandWordsOp {
@@ -1900,6 +1953,24 @@ void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, co
     c->count_launch();
 }
 
+void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out) {
+    if (!n) return;
+    ProfScope prof(c, "expand_words", 12.0 * double(n));
+    tile_scan(c, ExpandWordKeysOp{keys, bits, out}, n, nullptr);
+}
+
+u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits) {
+    if (!n) return 0;
+    u64* d = c->d_scalars + 45;
+    {
+        ProfScope prof(c, "tuples_to_words", 8.0 * double(n));
+        tile_scan(c, TuplesToWordsOp{c0, c1, n, x, zb, bits}, n, d);
+    }
+    u64 total = 0;
+    c->read_scalars(d, &total, 1);
+    return total;
+}
+
 u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u64 n, u32* out_x, u32* out_z) {
     if (!n) return 0;
     u64* d = c->d_scalars + 40;
@@ -2221,7 +2292,7 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
     } while (0)
     const bool blocks = spec.bs.dir != nullptr;
     const bool cmp = spec.n_filters != 0;
-    const bool words = spec.wbits.ptr != nullptr;
+    const bool words = spec.word_sink != 0;
     if (words && (!blocks || spec.remote_world)) fail(FV_ERR_INVALID, "word-form join needs a local block set");
     if (spec.remote_world) {
         if (blocks) {
