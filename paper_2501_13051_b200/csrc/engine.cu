@@ -1385,15 +1385,54 @@ public:
         r.blocks.ratio = double(nb) / double(pool.n);
     }
 
-    u64 word_finalize(RelState& r, HeadSink& s, CandPool& pool) {
+    // Insert a head's pooled candidates (copies, unfused joins) into its set;
+    // the new keys join the ones the fused joins appended.
+    void insert_pool(RelState& r, HeadSink& s, CandPool& pool) {
+        if (!r.hash_mode) return;
         estimate_blocks(r, pool);
-        if (pool.n) {
-            hash_reserve(r, s, pool.n);
+        if (!pool.n) return;
+        hash_reserve(r, s, pool.n);
+        if (r.word_sink)
             engine_blockset_word_insert(c_, pool.words[0].get(), nullptr, pool.n, block_args(r), s.keys.get(),
                                         s.widx.get(), s.counter.get(), s.counter.get() + 2, s.ovf.get(),
                                         s.ovf_bits.get(), s.counter.get() + 1);
-            s.candidates += pool.n;
+        else if (r.block_mode)
+            engine_blockset_insert(c_, pool.words[0].get(), pool.n, block_args(r), s.keys.get(), s.counter.get(),
+                                   s.ovf.get(), s.counter.get() + 1);
+        else
+            engine_hash_insert(c_, pool.words[0].get(), pool.n, r.keys, s.keys.get(), s.counter.get());
+        s.candidates += pool.n;
+        pool.n = 0;
+    }
+
+    // The set counters of several heads in one host round trip (the next
+    // read_block_counters of each uses them).
+    void prefetch_counters(const std::vector<std::pair<RelState*, HeadSink*>>& heads) {
+        std::vector<std::pair<RelState*, HeadSink*>> live;
+        for (auto& [r, s] : heads)
+            if (r->block_mode && r->blocks.capacity() && s->counter.get()) live.emplace_back(r, s);
+        if (live.empty()) return;
+        if (batch_pinned_cap_ < 4 * live.size()) {
+            if (batch_pinned_) cudaFreeHost(batch_pinned_);
+            batch_pinned_cap_ = std::max<size_t>(256, 8 * live.size());
+            FV_CUDA(cudaMallocHost(&batch_pinned_, sizeof(u64) * batch_pinned_cap_));
         }
+        for (size_t q = 0; q < live.size(); ++q) {
+            FV_CUDA(cudaMemcpyAsync(batch_pinned_ + 4 * q, live[q].second->counter.get(), 24, cudaMemcpyDeviceToHost,
+                                    c_->stream));
+            FV_CUDA(cudaMemcpyAsync(batch_pinned_ + 4 * q + 3, live[q].first->blocks.count.get(), 8,
+                                    cudaMemcpyDeviceToHost, c_->stream));
+        }
+        c_->sync();
+        for (size_t q = 0; q < live.size(); ++q) {
+            HeadSink& s = *live[q].second;
+            s.pre = true;
+            for (int k = 0; k < 4; ++k) s.pre_vals[k] = batch_pinned_[4 * q + k];
+        }
+    }
+
+    u64 word_finalize(RelState& r, HeadSink& s, CandPool& pool) {
+        insert_pool(r, s, pool);
         u64 nw = 0, ov = 0;
         if (s.counter.get()) {
             read_block_counters(r, s, &nw, &ov);
@@ -1497,22 +1536,18 @@ public:
     // Sort the iteration's new keys into Δ and fold them into FULL.
     u64 hash_finalize(RelState& r, HeadSink& s, CandPool& pool) {
         if (r.word_sink) return word_finalize(r, s, pool);
-        estimate_blocks(r, pool);
-        if (pool.n) {
-            hash_reserve(r, s, pool.n);
-            if (r.block_mode)
-                engine_blockset_insert(c_, pool.words[0].get(), pool.n, block_args(r), s.keys.get(), s.counter.get(),
-                                       s.ovf.get(), s.counter.get() + 1);
-            else
-                engine_hash_insert(c_, pool.words[0].get(), pool.n, r.keys, s.keys.get(), s.counter.get());
-            s.candidates += pool.n;
-        }
+        insert_pool(r, s, pool);
+        u64 nd = 0;
         if (r.block_mode && s.counter.get()) {
-            u64 nw, ov;
-            read_block_counters(r, s, &nw, &ov);
-            if (ov) drain_overflow(r, s, ov);
+            u64 ov;
+            read_block_counters(r, s, &nd, &ov);
+            if (ov) {
+                drain_overflow(r, s, ov);
+                nd = sink_count(s);  // the drain may also have converted the set
+            }
+        } else {
+            nd = sink_count(s);
         }
-        const u64 nd = sink_count(s);
         if (!r.block_mode && forced_group_ < 0 && r.keys.capacity() && s.candidates) {
             const u32 want = double(s.candidates) <= group_ratio_ * double(std::max<u64>(nd, 1)) ? 1u : 0u;
             if (trace_)
@@ -1602,9 +1637,16 @@ public:
     u32 world() const { return world_; }
     u32 rank() const { return rank_; }
 
+public:
+    ~Engine() {
+        if (batch_pinned_) cudaFreeHost(batch_pinned_);
+    }
+
 private:
     Ctx* c_;
     EvalState& st_;
+    u64* batch_pinned_ = nullptr;  // prefetch_counters staging
+    size_t batch_pinned_cap_ = 0;
     bool force_partitioned_ = false;
     std::map<InterKey, InterPolicy> inter_policy_;
     const bool trace_ = std::getenv("FVLOG_TRACE") != nullptr;
@@ -2024,9 +2066,19 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         tr("variants", ti, iteration);
         const auto tf = Clock::now();
         std::vector<u64> counts;  // per head: |Δ|, |FULL| (local, then global)
+        // Set heads: pooled candidates inserted first, all heads' counters
+        // then read in one round trip (not one per head).
+        std::vector<std::pair<RelState*, HeadSink*>> set_heads;
         for (auto& [name, pool] : pooled) {
             RelState& r = *st->relations.at(name);
             if (eng.dist()) eng.route_pool(pool, r.home, r.owner_shift);
+            if (r.hash_mode) set_heads.emplace_back(&r, &sinks[name]);
+        }
+        eng.prefetch_counters(set_heads);
+        for (auto& [r, s] : set_heads) eng.insert_pool(*r, *s, pooled.at(r->name));
+        eng.prefetch_counters(set_heads);
+        for (auto& [name, pool] : pooled) {
+            RelState& r = *st->relations.at(name);
             const u64 nd = r.hash_mode ? eng.hash_finalize(r, sinks[name], pool) : eng.dedup_merge_home(r, pool);
             if (eng.dist()) eng.forward_delta(r);
             counts.push_back(nd);

@@ -1407,6 +1407,8 @@ struct ExpandWordsOp {
     }
 };
 
+__global__ void set_u64_kernel(u64* p, u64 v) { *p = v; }
+
 // Block ids of packed keys (the distinct count sizes a directory).
 __global__ void block_ids_kernel(const u64* __restrict__ keys, u64 n, u32 shift, u32 arity, u64* __restrict__ out) {
     GRID_STRIDE(i, n) {
@@ -1901,8 +1903,8 @@ void engine_blockset_alloc(Ctx* c, BlockSet& s, u64 cap, u64 blocks, bool delta_
     s.blocks = blocks;
     FV_CUDA(cudaMemsetAsync(s.dir.get(), 0xff, 8 * cap, c->stream));
     FV_CUDA(cudaMemsetAsync(s.bits.get(), 0, 128 * cap, c->stream));
-    FV_CUDA(cudaMemcpyAsync(s.count.get(), &blocks, 8, cudaMemcpyHostToDevice, c->stream));
-    c->sync();  // `blocks` is a host stack value
+    set_u64_kernel<<<1, 1, 0, c->stream>>>(s.count.get(), blocks);  // stream-ordered, no host sync
+    FV_CUDA(cudaGetLastError());
 }
 
 void engine_blockset_grow(Ctx* c, const BlockSet& from, BlockSet& to) {
