@@ -533,8 +533,12 @@ public:
     static bool word_step_ok(const Plan& p, size_t k) {
         const PlanJoin& j = p.joins[k];
         const u32 R = j.right_source;
+        // the only guard allowed is x != z between the two head columns (a
+        // word drops x's own bit)
+        const bool guard_ok = p.guard_neq.empty() ||
+                              (p.guard_neq.size() == 1 && p.guard_neq[0].first + p.guard_neq[0].second == 1);
         return k + 1 == p.joins.size() && p.sources[R].arity == 2 && !p.sources[R].constrained() &&
-               j.right_col == 0 && j.residual_eq.empty() && p.guard_neq.empty() && p.head_arity == 2 &&
+               j.right_col == 0 && j.residual_eq.empty() && guard_ok && p.head_arity == 2 &&
                p.output_cols.size() == 2 && p.output_cols[1] == ColRef{R, 1} && p.output_cols[0].source != R;
     }
 
@@ -679,11 +683,15 @@ public:
         std::unique_ptr<JoinIndex> tmp;
         JoinIndex* idx;
         const bool word_step = k + 1 == nj && !D && word_step_ok(plan, k);
+        // A deduplicated binary intermediate (x, z) of a composition step is
+        // produced through a temporary word sink instead of rows + sort-unique.
+        ColRef inter_refs[2];
+        const bool inter_word = !D && words_ && k + 1 < nj && inter_word_ok(v, k, inter_refs);
         if (plan.sources[R].constrained()) {
             tmp = std::make_unique<JoinIndex>();
             build_index_on(*v.ver[R], jn.right_col, *tmp, &plan.sources[R]);
             idx = tmp.get();
-        } else if (word_step && v.ver[R]->cols.size() == 2 && rel(plan.head).word_sink) {
+        } else if ((word_step && rel(plan.head).word_sink && v.ver[R]->cols.size() == 2) || inter_word) {
             // Composition into a word sink: probe the word form of the build
             // version (x, z base, mask), one output per word.
             idx = &word_build(rr, v.which[R]).idx;
@@ -734,8 +742,13 @@ public:
         for (auto& [lref, rcol] : jn.residual_eq)
             push(spec, Filter{slot_of(lref), SlotRef{idx->rows->cols[rcol].get(), 1}, kFilterEq, 0});
         if (last) {
+            // Word build side: the x != z guard is applied to the words (the
+            // word of x's own window drops x's bit), not as a row filter.
+            const bool word_guard = idx->rows->cols.size() == 3 && !plan.guard_neq.empty();
+            spec.word_neq = word_guard ? 1 : 0;
             for (auto& [ga, gb] : plan.guard_neq)
-                push(spec, Filter{slot_of(plan.output_cols[ga]), slot_of(plan.output_cols[gb]), kFilterNeq, 0});
+                if (!word_guard)
+                    push(spec, Filter{slot_of(plan.output_cols[ga]), slot_of(plan.output_cols[gb]), kFilterNeq, 0});
             if (D && dp.replicated_out) {
                 const RelState& h = rel(plan.head);
                 push(spec, owner_filter(slot_of(plan.output_cols[h.home]), h.owner_shift));
@@ -848,6 +861,13 @@ public:
             }
             return;
         }
+        if (inter_word) {
+            Inter next = word_intermediate(*idx, offsets.get(), n, T, starts.get(), slot_of(inter_refs[0]),
+                                           inter_refs);
+            if (!D && next.n == 0) return;
+            join_step(v, k + 1, std::move(next));
+            return;
+        }
         // Intermediate: the columns later steps and the head still need.
         std::vector<ColRef> refs;
         for (const ColRef& r : v.needed[k]) {
@@ -886,6 +906,85 @@ public:
         }
     }
 
+    // Step k (not the last) can produce its intermediate as words: the right
+    // atom is binary, unconstrained, joined on its column 0 with nothing else
+    // to check, the later steps and the head need exactly one left-side
+    // column and the right atom's column 1, and the step's intermediates have
+    // been measured to repeat (maybe_dedup_inter's policy is on). refs[0]:
+    // the left-side column, refs[1] = {R, 1}.
+    bool inter_word_ok(VarRun& v, size_t k, ColRef (&refs)[2]) {
+        const Plan& p = v.plan;
+        const PlanJoin& j = p.joins[k];
+        const u32 R = j.right_source;
+        if (p.sources[R].arity != 2 || p.sources[R].constrained() || j.right_col != 0 || !j.residual_eq.empty())
+            return false;
+        if (v.ver[R]->cols.size() != 2) return false;
+        std::vector<ColRef> need;
+        for (const ColRef& r : v.needed[k])
+            if (r.source <= R) need.push_back(r);
+        if (need.size() != 2) return false;
+        const ColRef right{R, 1};
+        if (need[0] == right) std::swap(need[0], need[1]);
+        if (!(need[1] == right) || need[0].source >= R) return false;
+        auto it = inter_policy_.find(std::make_tuple(&p, k, v.delta_source));
+        if (it == inter_policy_.end() || !it->second.on) return false;
+        refs[0] = need[0];
+        refs[1] = need[1];
+        return true;
+    }
+
+    // The distinct (x, z) rows of a composition step, through a temporary
+    // word sink: the join emits one word per (probe row, build word), the
+    // block set dedups, the merged words expand to the rows (grouped by x).
+    Inter word_intermediate(JoinIndex& idx, const u64* offsets, u64 n, u64 T, const u32* starts, const SlotRef& left,
+                            const ColRef (&refs)[2]) {
+        RelState tmp;
+        tmp.name = "(intermediate)";
+        tmp.arity = 2;
+        tmp.hash_mode = tmp.block_mode = tmp.levels_mode = tmp.word_sink = true;
+        tmp.delta.cols.resize(2);
+        HeadSink sk;
+        OutSpec spec;
+        spec.shift = st_.key_shift;
+        spec.key_mode = 1;
+        spec.n_out = 2;
+        spec.col[0] = left;
+        spec.col[1] = SlotRef{idx.rows->cols[1].get(), 1};
+        spec.wbits = SlotRef{idx.rows->cols[2].get(), 1};
+        spec.word_sink = 1;
+        spec.tile_set = word_combine_;
+        for (u64 t0 = 0; t0 < T; t0 += kFusedChunk) {
+            const u64 t1 = std::min(T, t0 + kFusedChunk);
+            hash_reserve(tmp, sk, t1 - t0);
+            spec.bs = block_args(tmp);
+            spec.ovf_keys = sk.ovf.get();
+            spec.ovf_count = sk.counter.get() + 1;
+            spec.ovf_bits = sk.ovf_bits.get();
+            spec.new_keys = sk.keys.get();
+            spec.new_count = sk.counter.get();
+            spec.new_tuples = sk.counter.get() + 2;
+            spec.new_widx = sk.widx.get();
+            engine_materialize(c_, offsets, n, T, starts, spec, t0, t1);
+        }
+        CandPool none;
+        none.arity = 2;
+        const u64 nd = T ? hash_finalize(tmp, sk, none) : 0;
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   word intermediate: %llu word outputs -> %llu rows\n",
+                         static_cast<unsigned long long>(T), static_cast<unsigned long long>(nd));
+        Inter next;
+        next.n = nd;
+        if (nd) {
+            next.owned = std::move(tmp.delta.cols);
+        } else {
+            next.owned.emplace_back(c_, 0);
+            next.owned.emplace_back(c_, 0);
+        }
+        next.cols[refs[0]] = next.owned[0].get();
+        next.cols[refs[1]] = next.owned[1].get();
+        return next;
+    }
+
     // Distinct rows of a join intermediate that dropped columns. The join
     // multiplies duplicates: in CSPA's valueAlias(x,y) :- valueFlow(z,x),
     // memoryAlias(z,w), valueFlow(w,y) the (x,w) pairs repeat once per z and
@@ -907,7 +1006,7 @@ public:
         const u32 a = static_cast<u32>(x.owned.size());
         if (a == 0 || a > FV_MAX_ARITY || x.n < 2 || x.owned.size() != x.cols.size()) return;
         InterPolicy& policy = inter_policy_[key];
-        const bool measure = !policy.on && x.n >= kInterProbeRows &&
+        const bool measure = !policy.on && x.n >= inter_probe_rows_ &&
                              (policy.measured == 0 || x.n >= 4 * policy.measured);
         if (!policy.on && !measure) return;
         std::vector<const u32*> cols;
@@ -1656,6 +1755,8 @@ private:
     }
     const u64 pool_chunk_ = env_rows("FVLOG_POOL_CHUNK", kPoolChunk);
     const u64 inter_chunk_ = env_rows("FVLOG_INTER_CHUNK", kInterChunk);
+    // FVLOG_INTER_PROBE_ROWS (tests): the intermediate size at which repeats are first measured.
+    const u64 inter_probe_rows_ = env_rows("FVLOG_INTER_PROBE_ROWS", kInterProbeRows);
     const u64 pool_budget_ = env_rows("FVLOG_POOL_BUDGET", kPoolBudget);
     const double group_ratio_ = [] {
         const char* e = std::getenv("FVLOG_GROUP_RATIO");
@@ -1685,6 +1786,11 @@ private:
     const double block_sparse_bytes_ = [] {
         const char* e = std::getenv("FVLOG_BLOCK_SPARSE_BYTES");
         return e ? std::atof(e) : kBlockSparseMinBytes;
+    }();
+    // FVLOG_WORDS=0: no word sinks, word builds or word intermediates.
+    const bool words_ = [] {
+        const char* e = std::getenv("FVLOG_WORDS");
+        return !(e && std::string(e) == "0");
     }();
     // FVLOG_WORD_COMBINE=0: no tile-local OR-combine of word-form outputs.
     const u32 word_combine_ = [] {
@@ -2074,8 +2180,12 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
             if (eng.dist()) eng.route_pool(pool, r.home, r.owner_shift);
             if (r.hash_mode) set_heads.emplace_back(&r, &sinks[name]);
         }
-        eng.prefetch_counters(set_heads);
-        for (auto& [r, s] : set_heads) eng.insert_pool(*r, *s, pooled.at(r->name));
+        bool any_pool = false;
+        for (auto& [r, s] : set_heads) any_pool = any_pool || pooled.at(r->name).n > 0;
+        if (any_pool) {
+            eng.prefetch_counters(set_heads);
+            for (auto& [r, s] : set_heads) eng.insert_pool(*r, *s, pooled.at(r->name));
+        }
         eng.prefetch_counters(set_heads);
         for (auto& [name, pool] : pooled) {
             RelState& r = *st->relations.at(name);

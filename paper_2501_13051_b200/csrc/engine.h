@@ -376,6 +376,11 @@ struct OutSpec {
     // *new_tuples.
     SlotRef wbits;
     u32 word_sink = 0;  // the head is a word sink (WORDS kernel; wbits null: one-bit words)
+    u32 word_neq = 0;   // word outputs drop the bit of their own x (guard x != z)
+    // Profiling only: the tuple candidates the word outputs stand for
+    // (sum of their masks' popcounts), for the implementation-independent
+    // algorithmic bytes of SURVEY.md §8(d).
+    u64* cand_count = nullptr;
     u32* ovf_bits = nullptr;
     u32* new_widx = nullptr;  // bitmap word index of each appended new word
     u64* new_tuples = nullptr;

@@ -12,6 +12,7 @@
 //   merge         dedup_rows + deduplicate + difference + merge_delta
 //                 (relation.cpp:71-108, kernels.cpp:210-268) as ONE
 //                 merge-path pass over sorted FULL and sorted candidates.
+#include <optional>
 #include <cstdlib>
 
 #include "engine.h"
@@ -563,6 +564,14 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
             if (spec.wbits.ptr) {
 #pragma unroll
                 for (int k = 0; k < kMatItems; ++k) wb[k] = ((keep_mask >> k) & 1u) ? slot(spec.wbits, ii[k], pp[k]) : 0;
+                if (spec.word_neq) {
+#pragma unroll
+                    for (int k = 0; k < kMatItems; ++k) {
+                        const u64 x = key[k] >> spec.shift, zb = key[k] & ((u64(1) << spec.shift) - 1);
+                        if ((x & ~u64(31)) == zb) wb[k] &= ~(1u << static_cast<u32>(x & 31));
+                        if (!wb[k]) keep_mask &= ~(1u << k);
+                    }
+                }
             } else {
                 // tuple candidates into a word sink: one-bit words
 #pragma unroll
@@ -573,6 +582,14 @@ __device__ __forceinline__ void materialize_tile(const u64* __restrict__ offsets
                         hs[k] = keyset_line_hash(key[k], spec.ht_group_bits);
                     }
                 }
+            }
+            if (spec.cand_count) {
+                u32 tc = 0;
+#pragma unroll
+                for (int k = 0; k < kMatItems; ++k)
+                    if ((keep_mask >> k) & 1u) tc += __popc(wb[k]);
+                tc = __reduce_add_sync(0xffffffffu, tc);
+                if (lane == 0 && tc) atomicAdd(reinterpret_cast<unsigned long long*>(spec.cand_count), static_cast<unsigned long long>(tc));
             }
             if (spec.tile_set) {
                 // Tile-local combine: outputs of one tile that hit the same
@@ -2263,9 +2280,20 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
     tile_rows_kernel<<<grid_for(tiles), 256, 0, c->stream>>>(offsets, m, o_begin, o_end, tiles, rows.get(),
                                                              rows.get() + tiles);
     FV_CUDA(cudaGetLastError());
-    // The fused join + key-set dedup is profiled as "join_dedup".
-    ProfScope prof(c, fused_set(spec) ? "join_dedup" : "join_materialize",
-                   frac * double(m) * (12.0 + side0) + double(outs) * (side1 + out_bytes));
+    // The fused join + key-set dedup is profiled as "join_dedup". Word
+    // outputs are charged per tuple candidate they stand for (SURVEY.md
+    // §8(d)'s B_alg is implementation-independent): each costs its build-side
+    // value (4 B) and its write + read by dedup (2 * 8 B), counted by the
+    // kernel when profiling.
+    const bool word_prof = c->prof && spec.word_sink && spec.wbits.ptr;
+    OutSpec pspec = spec;
+    if (word_prof) {
+        pspec.cand_count = c->d_scalars + 46;
+        FV_CUDA(cudaMemsetAsync(pspec.cand_count, 0, 8, c->stream));
+    }
+    std::optional<ProfScope> prof;
+    prof.emplace(c, fused_set(spec) ? "join_dedup" : "join_materialize",
+                 frac * double(m) * (12.0 + side0) + (word_prof ? 0.0 : double(outs) * (side1 + out_bytes)));
     static const u32 env_group = [] {
         const char* e = std::getenv("FVLOG_MAT_GROUP");
         return e ? static_cast<u32>(std::atoi(e)) : 0u;
@@ -2290,7 +2318,7 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
         }                                                                                                       \
         materialize_kernel<C_, R_, B_, W_><<<grid, kMatBlock, dyn, c->stream>>>(offsets, m, o_begin, o_end,     \
                                                                                  starts, jlo, jhi, tiles, group, \
-                                                                                 spec);                          \
+                                                                                 pspec);                         \
     } while (0)
     const bool blocks = spec.bs.dir != nullptr;
     const bool cmp = spec.n_filters != 0;
@@ -2318,6 +2346,12 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
 #undef FV_MAT_LAUNCH_W
     FV_CUDA(cudaGetLastError());
     c->count_launch(2);
+    prof.reset();  // the launch's event closes before the candidate count is read
+    if (word_prof) {
+        u64 tc = 0;
+        c->read_scalars(pspec.cand_count, &tc, 1);
+        c->prof_add_bytes("join_dedup", double(tc) * (4.0 + 16.0));
+    }
 }
 
 void engine_project(Ctx* c, u64 n, const OutSpec& spec) {

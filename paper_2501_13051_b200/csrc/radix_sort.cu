@@ -133,6 +133,49 @@ __global__ void radix_bins_kernel(const unsigned long long* __restrict__ hist, u
     if (threadIdx.x == 0) trivial[p] = is_trivial ? 1 : 0;
 }
 
+// ---- bulk tile loads (TMA 1D bulk copy, cp.async.bulk) -------------------------
+//
+// A full tile's keys (and values) are copied global -> shared by the TMA
+// engine in one bulk transfer per array, completing on an mbarrier; the
+// threads then read their warp-striped items from shared memory. The copy is
+// one 32 KB request instead of 16 dependent 8-byte loads per thread, so the
+// SM issues no load instructions for the tile (SASS: UBLKCP).
+
+__device__ __forceinline__ u32 smem_u32(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, u32 bytes, u64* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
+    asm volatile(
+        "{\n"
+        " .reg .pred done;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        " @!done bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+#ifndef FV_SORT_BULK
+#define FV_SORT_BULK 1
+#endif
+
 // ---- onesweep pass ------------------------------------------------------------
 
 template <typename K, bool HAS_VAL>
@@ -152,9 +195,13 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
     __shared__ u64 s_global[kRadix];
     __shared__ u32 s_tile;
     __shared__ u32 s_warp_sums[kSortWarps];
+    __shared__ alignas(8) u64 s_bar;
 
     const u32 tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    if (tid == 0) {
+        s_tile = atomicAdd(tile_counter, 1u);
+        if (FV_SORT_BULK) mbar_init(&s_bar, 1);
+    }
     for (u32 i = tid; i < kSortWarps * kRadix; i += kSortBlock) (&s_whist[0][0])[i] = 0;
     __syncthreads();
     const u32 tile = s_tile;
@@ -165,13 +212,35 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
     u32 val[ITEMS];
     u32 rank[ITEMS];
     u32 dig[ITEMS];
+    // Full tiles of 16-byte aligned arrays arrive by one TMA bulk copy per
+    // array; the partial last tile (and unaligned inputs) load directly.
+    const bool bulk = FV_SORT_BULK && tile_base + TILE <= n &&
+                      !(reinterpret_cast<uintptr_t>(keys_in) & 15) &&
+                      (!HAS_VAL || !(reinterpret_cast<uintptr_t>(vals_in) & 15));
+    if (bulk) {
+        if (tid == 0) {
+            constexpr u32 kb = sizeof(K) * TILE, vb = HAS_VAL ? sizeof(u32) * TILE : 0;
+            mbar_expect_tx(&s_bar, kb + vb);
+            bulk_load(s_keys, keys_in + tile_base, kb, &s_bar);
+            if (HAS_VAL) bulk_load(s_vals, vals_in + tile_base, vb, &s_bar);
+        }
+        mbar_wait(&s_bar, 0);
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-        const u64 i = warp_base + u64(k) * 32 + lane;
-        const bool valid = i < n;
-        key[k] = valid ? keys_in[i] : K(0);
-        if (HAS_VAL) val[k] = valid ? vals_in[i] : 0u;
-        dig[k] = valid ? digit_of(key[k], shift, mask) : 0xffffu;
+        for (int k = 0; k < ITEMS; ++k) {
+            const u32 li = warp * WARP_TILE + k * 32 + lane;
+            key[k] = s_keys[li];
+            if (HAS_VAL) val[k] = s_vals[li];
+            dig[k] = digit_of(key[k], shift, mask);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const u64 i = warp_base + u64(k) * 32 + lane;
+            const bool valid = i < n;
+            key[k] = valid ? keys_in[i] : K(0);
+            if (HAS_VAL) val[k] = valid ? vals_in[i] : 0u;
+            dig[k] = valid ? digit_of(key[k], shift, mask) : 0xffffu;
+        }
     }
     // Warp-level stable ranking, item-major (k outer, lane inner) = input order.
 #pragma unroll

@@ -327,8 +327,10 @@ def test_keyset_growth_paths_match_reference(ctx, grow, monkeypatch):
     {"FVLOG_BLOCK_SPARSE_BYTES": "0", "FVLOG_WORDS": "1"},    # word form left mid-run (sparse -> key set)
     {"FVLOG_WORD_COMBINE": "0"},                              # no tile-local OR-combine of word outputs
     {"FVLOG_DUMP_SORT": "1"},                                 # dumps by sorting the levels, not from the bitmaps
+    {"FVLOG_INTER_PROBE_ROWS": "2"},                          # intermediates deduplicated early (word intermediates)
+    {"FVLOG_INTER_PROBE_ROWS": "2", "FVLOG_WORDS": "0"},      # ... by sort-unique
 ], ids=["keyset", "blocks", "blocks-overflow", "blocks-convert", "blocks-no-tile-set", "no-words",
-        "words-overflow", "words-leave", "words-no-combine", "dump-sort"])
+        "words-overflow", "words-leave", "words-no-combine", "dump-sort", "inter-words", "inter-sort"])
 def test_dedup_sets_match_reference(ctx, setmode, monkeypatch):
     # FULL's dedup structure for binary/unary IDB relations: a BlockSet
     # (blocked bitmap, default) or a KeySet; every path must give the
