@@ -699,6 +699,9 @@ public:
             idx = &index(rr, rpart ? dp.src_copy[R] : 0, v.which[R], jn.right_col);
         }
         if (!D && idx->rows->n == 0) return;
+        // The build side is in word form (x, z base, mask): a binary atom whose
+        // version has three columns (a ternary atom's version also has three).
+        const bool word_build_side = plan.sources[R].arity == 2 && idx->rows->cols.size() == 3;
         const u64 n = cur.n;
         DBuf<u32> starts(c_, n), counts(c_, n);
         RowFilter pred;
@@ -744,7 +747,7 @@ public:
         if (last) {
             // Word build side: the x != z guard is applied to the words (the
             // word of x's own window drops x's bit), not as a row filter.
-            const bool word_guard = idx->rows->cols.size() == 3 && !plan.guard_neq.empty();
+            const bool word_guard = word_build_side && !plan.guard_neq.empty();
             spec.word_neq = word_guard ? 1 : 0;
             for (auto& [ga, gb] : plan.guard_neq)
                 if (!word_guard)
@@ -802,7 +805,7 @@ public:
                             // is in word form (x, z base, mask) emits one
                             // output per word; other joins emit their tuples
                             // as one-bit words.
-                            if (idx->rows->cols.size() == 3) spec.wbits = SlotRef{idx->rows->cols[2].get(), 1};
+                            if (word_build_side) spec.wbits = SlotRef{idx->rows->cols[2].get(), 1};
                             spec.word_sink = 1;
                             spec.ovf_bits = sink->ovf_bits.get();
                             spec.new_tuples = sink->counter.get() + 2;

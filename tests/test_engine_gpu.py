@@ -65,6 +65,25 @@ def test_engine_vs_oracle_and_naive_random_programs(ctx, oracle):
     assert compared > 15
 
 
+@pytest.mark.parametrize("words", ["1", "0"])
+def test_guard_with_a_ternary_build_side(ctx, words, monkeypatch):
+    # Regression (found by the reference's own engine suite through the
+    # drop-in shim, P/tests/engine_test.cpp:262-276, random program round 7):
+    # a three-column build version was taken for a word-form one and the
+    # guard v2 != v3 was dropped.
+    monkeypatch.setenv("FVLOG_WORDS", words)
+    text = ("i1(v3, v1) :- e0(v2, v4), i1(v1, v4), e1(v4, v4, v3), v2 != v3.\n"
+            "i1(v3, v1) :- e1(v3, v1, v2), v3 != v2.\n")
+    facts = {"e0": np.array([[7, 2], [5, 1], [3, 4], [5, 1], [1, 1]], np.uint32),
+             "e1": np.array([[0, 5, 4], [5, 1, 0], [1, 3, 3], [3, 1, 2], [5, 4, 3], [5, 5, 7], [3, 4, 6], [0, 1, 0],
+                             [4, 4, 3], [0, 2, 1], [5, 2, 4], [3, 6, 0], [1, 1, 1], [2, 1, 4], [3, 6, 2], [7, 3, 1],
+                             [4, 7, 7], [1, 7, 3], [0, 4, 1], [4, 0, 6], [6, 5, 0], [4, 6, 3], [5, 2, 5], [2, 0, 6],
+                             [0, 1, 7], [7, 1, 5], [1, 5, 4]], np.uint32)}
+    st = E.evaluate_program(text, facts, ctx=ctx)
+    exp = naive.naive_evaluate(text, {k: [tuple(int(x) for x in r) for r in v] for k, v in facts.items()})
+    assert _rows_set(st.dump("i1")) == exp["i1"]
+
+
 def test_residual_equalities_follow_the_naive_semantics(ctx):
     # Multi-variable joins: the reference's filter_pairs_eq (P/src/kernels.cpp:155)
     # indexes the left values by pair position; the engine implements the
