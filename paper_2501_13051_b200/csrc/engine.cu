@@ -702,6 +702,15 @@ public:
         // The build side is in word form (x, z base, mask): a binary atom whose
         // version has three columns (a ternary atom's version also has three).
         const bool word_build_side = plan.sources[R].arity == 2 && idx->rows->cols.size() == 3;
+        // Reversed composition: the probe side (source 0) is a word-form
+        // DELTA (y, z base, mask) joined on y with the build atom's column 1;
+        // the head is (build column 0, the word).
+        const bool word_probe_side = k == 0 && nj == 1 && plan.sources[0].arity == 2 && v.ver[0]->cols.size() == 3 &&
+                                     jn.left == ColRef{0, 0} && jn.residual_eq.empty() && plan.head_arity == 2 &&
+                                     plan.output_cols.size() == 2 && plan.output_cols[0] == ColRef{R, 0} &&
+                                     plan.output_cols[1] == ColRef{0, 1} && !plan.sources[R].constrained() &&
+                                     (plan.guard_neq.empty() || (plan.guard_neq.size() == 1 &&
+                                                                  plan.guard_neq[0].first + plan.guard_neq[0].second == 1));
         const u64 n = cur.n;
         DBuf<u32> starts(c_, n), counts(c_, n);
         RowFilter pred;
@@ -747,7 +756,8 @@ public:
         if (last) {
             // Word build side: the x != z guard is applied to the words (the
             // word of x's own window drops x's bit), not as a row filter.
-            const bool word_guard = word_build_side && !plan.guard_neq.empty();
+            const bool word_guard = (word_build_side || word_probe_side) && !plan.guard_neq.empty() &&
+                                    rel(plan.head).word_sink;
             spec.word_neq = word_guard ? 1 : 0;
             for (auto& [ga, gb] : plan.guard_neq)
                 if (!word_guard)
@@ -806,6 +816,7 @@ public:
                             // output per word; other joins emit their tuples
                             // as one-bit words.
                             if (word_build_side) spec.wbits = SlotRef{idx->rows->cols[2].get(), 1};
+                            else if (word_probe_side) spec.wbits = SlotRef{v.ver[0]->cols[2].get(), 0};
                             spec.word_sink = 1;
                             spec.ovf_bits = sink->ovf_bits.get();
                             spec.new_tuples = sink->counter.get() + 2;
@@ -1976,6 +1987,13 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         long delta_source;
         size_t plan_index;     // index into dplans
         std::vector<u8> old_src;  // per executed source: read FULL - DELTA
+        // Reversed orientation of a two-atom word composition (DELTA first,
+        // probing its words against the other atom indexed on the join
+        // column): chosen when DELTA's words are few next to the other atom,
+        // and always in partitioned runs (the other atom is replicated, DELTA
+        // is this rank's share).
+        const Plan* alt = nullptr;
+        size_t alt_index = 0;
     };
     std::vector<DistPlan> dplans;
     std::deque<Plan> reordered;  // delta-first plans (stable addresses)
@@ -2034,6 +2052,19 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         const std::map<std::string, u32> home = eng.dist() ? choose_home_cols(pv, idb_arity) : std::map<std::string, u32>();
         for (auto& [name, col] : home) st->relations.at(name)->home = col;
         for (auto& v : variants) dplans.push_back(dist_plan(*v.plan, idb, home));
+        for (auto& v : variants) {
+            const Plan& p = *v.plan;
+            if (v.delta_source != 1 || p.sources.size() != 2 || idb.count(p.sources[0].relation) ||
+                !Engine::word_step_ok(p, 0))
+                continue;
+            Plan rp;
+            std::vector<u32> order;
+            if (!delta_first_plan(p, 1, rp, &order)) continue;
+            reordered.push_back(std::move(rp));
+            v.alt = &reordered.back();
+            dplans.push_back(dist_plan(*v.alt, idb, home));
+            v.alt_index = dplans.size() - 1;
+        }
     }
     for (auto& v : variants)
         for (size_t s = 0; s < v.plan->sources.size(); ++s) {
@@ -2133,6 +2164,11 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     }
 
     const bool trace = std::getenv("FVLOG_TRACE") != nullptr;
+    // FVLOG_REVERSE=0: two-atom word compositions always probe in rule
+    // order; =1: always reversed (when eligible); unset: by size.
+    const char* rev_env = std::getenv("FVLOG_REVERSE");
+    const bool reverse_env = !(rev_env && std::string(rev_env) == "0");
+    const bool reverse_always = rev_env && std::string(rev_env) == "1";
     u64 syncs_seen = c->syncs;
     auto tr = [&](const char* what, Clock::time_point t, u64 it) {
         if (trace) {
@@ -2170,6 +2206,14 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
             if (v.delta_source < 0 && iteration != 0) continue;
             RelState& hr = *st->relations.at(v.plan->head);
             HeadSink* sink = hr.hash_mode ? &sinks[v.plan->head] : nullptr;
+            if (v.alt && hr.word_sink && reverse_env) {
+                const RelState& dr = *st->relations.at(v.plan->sources[1].relation);
+                const RelState& pr = *st->relations.at(v.plan->sources[0].relation);
+                if (dr.word_mode && (reverse_always || eng.dist() || 2 * dr.delta.n < pr.full.n)) {
+                    eng.exec_variant(*v.alt, dplans[v.alt_index], 0, {}, pooled[v.plan->head], sink);
+                    continue;
+                }
+            }
             eng.exec_variant(*v.plan, dplans[v.plan_index], v.delta_source, v.old_src, pooled[v.plan->head], sink);
         }
         tr("variants", ti, iteration);
