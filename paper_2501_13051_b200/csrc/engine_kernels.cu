@@ -1360,23 +1360,57 @@ __global__ void blockset_collect_kernel(const u64* __restrict__ keys, const u32*
     }
 }
 
-// Packed tuple keys of n word entries (word key, mask), in entry order.
-struct ExpandWordKeysOp {
-    const u64* keys;
+
+// Exclusive prefix of the masks' popcounts (the tuples' output offsets).
+struct PopcOffsetsOp {
     const u32* bits;
-    u64* out;
+    u64* off;
     __device__ u64 value(u64 i) const { return __popc(bits[i]); }
-    __device__ void emit(u64 i, u64 p, u64 v) const {
-        if (!v) return;
-        const u64 k = keys[i];  // (x << shift) | zb, zb a multiple of 32
-        u32 m = bits[i];
-        while (m) {
-            const u32 b = __ffs(m) - 1;
-            m &= m - 1;
-            out[p++] = k + b;
+    __device__ void emit(u64 i, u64 p, u64) const { off[i] = p; }
+};
+
+// Warp-cooperative expansion of word entries into packed tuple keys: a warp
+// takes 32 consecutive words and writes their tuples 32 at a time, each
+// lane finding its word by a shuffle search over the warp's offsets and its
+// bit with __fns, so the writes are coalesced (a thread-per-word loop writes
+// up to 32 scattered rows per thread).
+__global__ void expand_word_keys_kernel(const u64* __restrict__ keys, const u32* __restrict__ bits,
+                                        const u64* __restrict__ off, u64 n, u64* __restrict__ out) {
+    const u32 lane = lane_id();
+    const u64 warps = (n + 31) / 32;
+    for (u64 w = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / 32; w < warps;
+         w += (u64(gridDim.x) * blockDim.x) / 32) {
+        const u64 i = w * 32 + lane;
+        const bool valid = i < n;
+        const u64 k = valid ? keys[i] : 0;
+        const u32 m = valid ? bits[i] : 0;
+        const u64 o = valid ? off[i] : 0;
+        const u64 base = __shfl_sync(0xffffffffu, o, 0);
+        const u32 rel = static_cast<u32>(o - base);  // this word's first output within the warp
+        const u32 cnt = __popc(m);
+        u32 tot = valid ? rel + cnt : 0;  // the warp's output count: the largest end offset
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) tot = max(tot, __shfl_xor_sync(0xffffffffu, tot, d));
+        for (u32 j = 0; j < tot; j += 32) {
+            const u32 t = j + lane;  // output index within the warp's range
+            // last word whose first output <= t (words with no bits are skipped)
+            u32 lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const u32 cand = lo + step;
+                const u32 r = __shfl_sync(0xffffffffu, valid ? rel : 0xffffffffu, cand);
+                if (r <= t) lo = cand;
+            }
+            const u32 wr = __shfl_sync(0xffffffffu, rel, lo);
+            const u32 wm = __shfl_sync(0xffffffffu, m, lo);
+            const u64 wk = __shfl_sync(0xffffffffu, k, lo);
+            if (t < tot) {
+                const u32 b = __fns(wm, 0, t - wr + 1);
+                out[base + t] = wk + b;
+            }
         }
     }
-};
+}
 
 // Words of a lexicographically sorted binary version: one entry per run of
 // rows with the same (x, z >> 5) (runs are at most 32 rows: rows are distinct).
@@ -1761,20 +1795,6 @@ __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 sh
 // Runs of the grouped keys straight from the counters: one row per non-empty
 // value (value, base, count) — the column-0 join index of the grouped DELTA
 // without a pass over its rows.
-struct GroupRunsOp {
-    const u32* cnt;
-    const u64* base;
-    u32* ukeys;
-    u32* ustart;
-    u32* ucount;
-    __device__ u64 value(u64 i) const { return cnt[i] ? 1 : 0; }
-    __device__ void emit(u64 i, u64 p, u64 v) const {
-        if (!v) return;
-        ukeys[p] = static_cast<u32>(i);
-        ustart[p] = static_cast<u32>(base[i]);
-        ucount[p] = cnt[i];
-    }
-};
 
 struct GroupBaseOp {
     const u32* cnt;
@@ -1974,8 +1994,12 @@ void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, co
 
 void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out) {
     if (!n) return;
+    DBuf<u64> off(c, n);
     ProfScope prof(c, "expand_words", 12.0 * double(n));
-    tile_scan(c, ExpandWordKeysOp{keys, bits, out}, n, nullptr);
+    tile_scan(c, PopcOffsetsOp{bits, off.get()}, n, nullptr);
+    expand_word_keys_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, bits, off.get(), n, out);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
 }
 
 u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits) {
