@@ -545,13 +545,32 @@ public:
     // Word form of a binary version of r (home copy) with its column-0 join
     // index, cached until the version changes. Built from the lexicographic
     // order when the version has it, else from a sorted copy.
-    WordBuild& word_build(RelState& r, Which which) {
+    // from_bitmap: FULL's words are read from the block set's bitmaps
+    // (row-major, no tuple pass) — only valid before the iteration inserts
+    // into the relation (prepare_full_words), since the bitmaps then already
+    // hold this iteration's new rows.
+    WordBuild& word_build(RelState& r, Which which, bool from_bitmap = false) {
         if (which == kOld && r.old_is_full) which = kFull;
         auto it = r.word_builds.find(static_cast<int>(which));
         if (it != r.word_builds.end()) return *it->second;
         const DevVersion& v = version(r, r.home, which);
         auto wb = std::make_unique<WordBuild>();
         const u64 n = v.n;
+        if (from_bitmap && which == kFull && r.block_mode && r.blocks.capacity() && r.arity == 2 && !dist()) {
+            for (int j = 0; j < 3; ++j) wb->words.cols.emplace_back(c_, std::max<u64>(n, 1));
+            wb->words.n = engine_blockset_words(c_, r.blocks, wb->words.cols[0].get(), wb->words.cols[1].get(),
+                                                wb->words.cols[2].get(), std::max<u64>(n, 1));
+            wb->words.lex_sorted = true;
+            wb->idx.rows = &wb->words;
+            engine_build_runs(c_, wb->words.cols[0].get(), wb->words.n, wb->idx);
+            if (trace_)
+                std::fprintf(stderr, "[fvlog]   word build of %s (full, from the bitmaps): %llu rows -> %llu words\n",
+                             r.name.c_str(), static_cast<unsigned long long>(n),
+                             static_cast<unsigned long long>(wb->words.n));
+            WordBuild& ref = *wb;
+            r.word_builds.emplace(static_cast<int>(kFull), std::move(wb));
+            return ref;
+        }
         DevVersion sorted;
         const DevVersion* src = &v;
         if (!v.lex_sorted && n > 1) {
@@ -582,6 +601,21 @@ public:
         WordBuild& ref = *wb;
         r.word_builds.emplace(static_cast<int>(which), std::move(wb));
         return ref;
+    }
+
+    // Word builds of FULL for the iteration's composition steps, taken from
+    // the block sets before any insert of the iteration.
+    void prepare_full_words(const std::vector<std::pair<const Plan*, long>>& active) {
+        if (dist() || !words_) return;
+        for (auto& [p, d] : active) {
+            if (p->joins.empty()) continue;
+            const size_t k = p->joins.size() - 1;
+            if (!word_step_ok(*p, k) || !rel(p->head).word_sink) continue;
+            const u32 R = p->joins[k].right_source;
+            if (static_cast<long>(R) == d) continue;  // DELTA build
+            RelState& r = rel(p->sources[R].relation);
+            if (r.block_mode && !r.levels_mode) word_build(r, kFull, true);
+        }
     }
 
     // One variant's execution state (execute_plan, P/src/engine.cpp:72-146).
@@ -1676,6 +1710,11 @@ public:
     // The iteration's nd new packed tuple keys become DELTA (grouped by
     // column 0 in levels mode, sorted and merged into FULL otherwise).
     u64 finish_delta(RelState& r, DBuf<u64>&& new_keys, u64 nd) {
+        // FULL's word build becomes the build of FULL - DELTA when the merge
+        // keeps the replaced FULL (exactly-once variants read it).
+        std::unique_ptr<WordBuild> full_words;
+        if (auto it = r.word_builds.find(static_cast<int>(kFull)); it != r.word_builds.end())
+            full_words = std::move(it->second);
         invalidate(r);
         DevVersion Dv;
         Dv.n = nd;
@@ -1735,6 +1774,7 @@ public:
             Dv.lex_sorted = true;  // unpacked from the sorted keys
             set_old(r, &r.full);
             r.full = std::move(C);
+            if (!r.old_is_full && full_words) r.word_builds.emplace(static_cast<int>(kOld), std::move(full_words));
         }
         r.delta = std::move(Dv);
         if (have_index) {
@@ -2202,6 +2242,12 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         std::map<std::string, CandPool> pooled;
         std::map<std::string, HeadSink> sinks;
         for (auto& v : variants) pooled[v.plan->head].arity = v.plan->head_arity;
+        {
+            std::vector<std::pair<const Plan*, long>> active;
+            for (auto& v : variants)
+                if (v.delta_source >= 0 || iteration == 0) active.emplace_back(v.plan, v.delta_source);
+            eng.prepare_full_words(active);
+        }
         for (auto& v : variants) {
             if (v.delta_source < 0 && iteration != 0) continue;
             RelState& hr = *st->relations.at(v.plan->head);

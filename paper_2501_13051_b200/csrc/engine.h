@@ -447,6 +447,9 @@ void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u6
 // Word form (x, z base, mask) of a lexicographically sorted binary version
 // of n rows; outputs sized n; returns the word count.
 u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits);
+// The non-empty words of a binary block set in row-major (x, z) order —
+// FULL's word form straight from its bitmaps; outputs hold cap_out entries.
+u64 engine_blockset_words(Ctx* c, const BlockSet& s, u32* x, u32* zb, u32* bits, u64 cap_out);
 // FULL of a block-set relation as lexicographically sorted SoA rows (c0, and
 // c1 for binary relations; null c0: count only), decoded from the bitmaps in
 // order — no sort of the tuples. Returns the row count.

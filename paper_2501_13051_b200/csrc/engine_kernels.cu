@@ -1523,15 +1523,37 @@ __device__ __forceinline__ void block_item(const u32* __restrict__ starts, u64 r
     *g = 32 * j0 + u64(r) * (j1 - j0) + (j - j0);
 }
 
+// words = 0: the item's tuple count (popcount); 1: whether it is a non-empty word.
 __global__ void block_count_kernel(const u64* __restrict__ bids, const u32* __restrict__ slots,
                                    const u32* __restrict__ bits, const u32* __restrict__ starts, u64 rows, u64 m,
-                                   u32 arity, u32* __restrict__ cnt) {
+                                   u32 arity, u32 words, u32* __restrict__ cnt) {
     GRID_STRIDE(t, m * 32) {
         const u64 j = t >> 5;
         const u32 r = static_cast<u32>(t & 31);
         u64 g;
         block_item(starts, rows, m, j, r, arity, &g);
-        cnt[g] = __popc(bits[u64(slots[j]) * 32 + r]);
+        const u32 w = bits[u64(slots[j]) * 32 + r];
+        cnt[g] = words ? (w != 0) : __popc(w);
+    }
+}
+
+// The non-empty bitmap words in row-major order: (x, z base, mask).
+__global__ void block_words_kernel(const u64* __restrict__ bids, const u32* __restrict__ slots,
+                                   const u32* __restrict__ bits, const u32* __restrict__ starts, u64 rows, u64 m,
+                                   const u64* __restrict__ off, u32* __restrict__ x, u32* __restrict__ zb,
+                                   u32* __restrict__ wbits) {
+    GRID_STRIDE(t, m * 32) {
+        const u64 j = t >> 5;
+        const u32 r = static_cast<u32>(t & 31);
+        const u32 w = bits[u64(slots[j]) * 32 + r];
+        if (!w) continue;
+        u64 g;
+        block_item(starts, rows, m, j, r, 2, &g);
+        const u64 pos = off[g];
+        const u64 bid = bids[j];
+        x[pos] = static_cast<u32>((bid >> 27) * 32 + r);
+        zb[pos] = static_cast<u32>((bid & ((u64(1) << 27) - 1)) * 32);
+        wbits[pos] = w;
     }
 }
 
@@ -2043,37 +2065,81 @@ u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity) {
     return m;
 }
 
+namespace {
+// Sorted block ids (with their slots) and block-row starts of a block set.
+struct SortedBlocks {
+    DBuf<u64> bids;
+    DBuf<u32> slots, starts;
+    u64 m = 0, rows = 0;
+};
+
+SortedBlocks sorted_blocks(Ctx* c, const BlockSet& s, u32 arity) {
+    SortedBlocks b;
+    const u64 cap = s.capacity();
+    u64* d = c->d_scalars + 41;
+    b.bids = DBuf<u64>(c, cap);
+    b.slots = DBuf<u32>(c, cap);
+    DBuf<u64> bids_alt(c, cap);
+    DBuf<u32> slots_alt(c, cap);
+    {
+        ProfScope prof(c, "blockset_dump", 8.0 * double(cap));
+        tile_scan(c, BlockCompactOp{s.dir.get(), b.bids.get(), b.slots.get()}, cap, d);
+    }
+    c->read_scalars(d, &b.m, 1);
+    if (!b.m) return b;
+    // binary ids are (a >> 5) << 27 | (b >> 5): bits [0, 27) and [27, 54)
+    if (radix_sort_pairs_u64(c, b.bids.get(), bids_alt.get(), b.slots.get(), slots_alt.get(), b.m, 0, 54)) {
+        b.bids.swap(bids_alt);
+        b.slots.swap(slots_alt);
+    }
+    b.starts = DBuf<u32>(c, arity == 2 ? b.m : 1);
+    if (arity == 2) {
+        tile_scan(c, RowStartOp{b.bids.get(), b.starts.get()}, b.m, d);
+        c->read_scalars(d, &b.rows, 1);
+    }
+    return b;
+}
+}  // namespace
+
+u64 engine_blockset_words(Ctx* c, const BlockSet& s, u32* x, u32* zb, u32* bits, u64 cap_out) {
+    if (!s.capacity()) return 0;
+    SortedBlocks b = sorted_blocks(c, s, 2);
+    if (!b.m) return 0;
+    const u64 items = b.m * 32;
+    DBuf<u32> cnt(c, items);
+    DBuf<u64> off(c, items + 1);
+    ProfScope prof(c, "blockset_words", 136.0 * double(b.m));
+    block_count_kernel<<<grid_for(items), 256, 0, c->stream>>>(b.bids.get(), b.slots.get(), s.bits.get(),
+                                                                b.starts.get(), b.rows, b.m, 2, 1, cnt.get());
+    FV_CUDA(cudaGetLastError());
+    exclusive_scan_counts(c, cnt.get(), off.get(), items);
+    FV_CUDA(cudaMemcpyAsync(c->pinned, off.get() + items, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    const u64 total = c->pinned[0];
+    if (total > cap_out) fail(FV_ERR_INVALID, "blockset_words: more words than the output holds");
+    block_words_kernel<<<grid_for(items), 256, 0, c->stream>>>(b.bids.get(), b.slots.get(), s.bits.get(),
+                                                                b.starts.get(), b.rows, b.m, off.get(), x, zb, bits);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch(2);
+    return total;
+}
+
 u64 engine_blockset_dump(Ctx* c, const BlockSet& s, u32 arity, u32* c0, u32* c1) {
     const u64 cap = s.capacity();
     if (!cap) return 0;
-    u64* d = c->d_scalars + 41;
-    DBuf<u64> bids(c, cap), bids_alt(c, cap);
-    DBuf<u32> slots(c, cap), slots_alt(c, cap);
-    u64 m = 0;
-    {
-        ProfScope prof(c, "blockset_dump", 8.0 * double(cap));
-        tile_scan(c, BlockCompactOp{s.dir.get(), bids.get(), slots.get()}, cap, d);
-    }
-    c->read_scalars(d, &m, 1);
+    SortedBlocks b = sorted_blocks(c, s, arity);
+    const u64 m = b.m, rows = b.rows;
     if (!m) return 0;
-    // binary ids are (a >> 5) << 27 | (b >> 5): bits [0, 27) and [27, 54)
-    if (radix_sort_pairs_u64(c, bids.get(), bids_alt.get(), slots.get(), slots_alt.get(), m, 0, 54)) {
-        bids.swap(bids_alt);
-        slots.swap(slots_alt);
-    }
-    DBuf<u32> starts(c, arity == 2 ? m : 1);
-    u64 rows = 0;
-    if (arity == 2) {
-        tile_scan(c, RowStartOp{bids.get(), starts.get()}, m, d);
-        c->read_scalars(d, &rows, 1);
-    }
+    DBuf<u64>& bids = b.bids;
+    DBuf<u32>& slots = b.slots;
+    DBuf<u32>& starts = b.starts;
     DBuf<u32> cnt(c, m * 32);
     DBuf<u64> off(c, m * 32 + 1);
     u64 total = 0;
     {
         ProfScope prof(c, "blockset_dump", 136.0 * double(m));
         block_count_kernel<<<grid_for(m * 32), 256, 0, c->stream>>>(bids.get(), slots.get(), s.bits.get(),
-                                                                     starts.get(), rows, m, arity, cnt.get());
+                                                                     starts.get(), rows, m, arity, 0, cnt.get());
         FV_CUDA(cudaGetLastError());
         c->count_launch();
     }
