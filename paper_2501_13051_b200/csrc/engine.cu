@@ -542,6 +542,23 @@ public:
                p.output_cols.size() == 2 && p.output_cols[1] == ColRef{R, 1} && p.output_cols[0].source != R;
     }
 
+    // Source 0 can be carried as words: binary and unconstrained, its column
+    // 1 is the head's column 1 and nothing else (never a join key or a
+    // residual; no guard but x != z between the two head columns).
+    static bool carry_ok(const Plan& p) {
+        const ColRef y{0, 1};
+        if (p.sources[0].arity != 2 || p.sources[0].constrained() || p.head_arity != 2 || p.output_cols.size() != 2 ||
+            !(p.output_cols[1] == y) || p.output_cols[0] == y)
+            return false;
+        for (const PlanJoin& j : p.joins) {
+            if (j.left == y) return false;
+            for (auto& [l, rc] : j.residual_eq)
+                if (l == y) return false;
+        }
+        return p.guard_neq.empty() ||
+               (p.guard_neq.size() == 1 && p.guard_neq[0].first + p.guard_neq[0].second == 1);
+    }
+
     // Word form of a binary version of r (home copy) with its column-0 join
     // index, cached until the version changes. Built from the lexicographic
     // order when the version has it, else from a sorted copy.
@@ -631,6 +648,10 @@ public:
         bool D = false;
         CandPool& out;
         HeadSink* sink;
+        // Source 0 is carried as words (x, z base, mask) through the chain:
+        // its column 1 is only the head's column 1, so the mask rides along
+        // as ColRef {0, 2} and the last step emits one word per row.
+        bool carry = false;
     };
 
     // `old_src[s]`: source s reads FULL - DELTA instead of FULL (exactly-once
@@ -648,9 +669,20 @@ public:
             v.ver[s] = &version(r, kc, v.which[s]);
             if (!v.D && v.ver[s]->n == 0) return;  // engine.cpp:76-78
         }
+        // (partitioned runs: only a DELTA that is already words — the word
+        // builds are single-GPU)
+        v.carry = words_ && !plan.joins.empty() && rel(plan.head).word_sink && carry_ok(plan) &&
+                  (!v.D || v.ver[0]->cols.size() == 3);
+        if (v.carry && v.ver[0]->cols.size() == 2) {
+            // the probe side as words (cached word build of that version)
+            WordBuild& wb = word_build(rel(plan.sources[0].relation), v.which[0]);
+            v.ver[0] = &wb.words;
+            if (v.ver[0]->n == 0) return;
+        }
         Inter cur;
         cur.n = v.ver[0]->n;
         for (u32 j = 0; j < plan.sources[0].arity; ++j) cur.cols[ColRef{0, j}] = v.ver[0]->cols[j].get();
+        if (v.carry) cur.cols[ColRef{0, 2}] = v.ver[0]->cols[2].get();
         const size_t nj = plan.joins.size();
         v.needed.resize(nj);
         for (size_t k = 0; k < nj; ++k) {
@@ -660,6 +692,7 @@ public:
                 for (auto& r : plan.joins[q].residual_eq) s.insert(r.first);
             }
             for (auto& r : plan.output_cols) s.insert(r);
+            if (v.carry) s.insert(ColRef{0, 2});
         }
         if (nj) {
             join_step(v, 0, std::move(cur));
@@ -736,15 +769,8 @@ public:
         // The build side is in word form (x, z base, mask): a binary atom whose
         // version has three columns (a ternary atom's version also has three).
         const bool word_build_side = plan.sources[R].arity == 2 && idx->rows->cols.size() == 3;
-        // Reversed composition: the probe side (source 0) is a word-form
-        // DELTA (y, z base, mask) joined on y with the build atom's column 1;
-        // the head is (build column 0, the word).
-        const bool word_probe_side = k == 0 && nj == 1 && plan.sources[0].arity == 2 && v.ver[0]->cols.size() == 3 &&
-                                     jn.left == ColRef{0, 0} && jn.residual_eq.empty() && plan.head_arity == 2 &&
-                                     plan.output_cols.size() == 2 && plan.output_cols[0] == ColRef{R, 0} &&
-                                     plan.output_cols[1] == ColRef{0, 1} && !plan.sources[R].constrained() &&
-                                     (plan.guard_neq.empty() || (plan.guard_neq.size() == 1 &&
-                                                                  plan.guard_neq[0].first + plan.guard_neq[0].second == 1));
+        // Carried words: the last step's head column 1 is source 0's word.
+        const bool word_probe_side = v.carry && k + 1 == nj;
         const u64 n = cur.n;
         DBuf<u32> starts(c_, n), counts(c_, n);
         RowFilter pred;
@@ -849,8 +875,8 @@ public:
                             // is in word form (x, z base, mask) emits one
                             // output per word; other joins emit their tuples
                             // as one-bit words.
-                            if (word_build_side) spec.wbits = SlotRef{idx->rows->cols[2].get(), 1};
-                            else if (word_probe_side) spec.wbits = SlotRef{v.ver[0]->cols[2].get(), 0};
+                            if (word_probe_side) spec.wbits = slot_of(ColRef{0, 2});
+                            else if (word_build_side) spec.wbits = SlotRef{idx->rows->cols[2].get(), 1};
                             spec.word_sink = 1;
                             spec.ovf_bits = sink->ovf_bits.get();
                             spec.new_tuples = sink->counter.get() + 2;
@@ -947,7 +973,9 @@ public:
             u64 produced = t1 - t0;
             if (compacts) c_->read_scalars(spec.d_count, &produced, 1);
             next.n = produced;
-            if (spec.n_out < bound_cols) maybe_dedup_inter(next, std::make_tuple(&plan, k, delta_source));
+            // (carried word masks are 32-bit payloads, not domain values:
+            // the packed-key dedup does not apply)
+            if (spec.n_out < bound_cols && !v.carry) maybe_dedup_inter(next, std::make_tuple(&plan, k, delta_source));
             if (!D && next.n == 0) continue;
             join_step(v, k + 1, std::move(next));
             if (T == 0) break;
