@@ -942,6 +942,27 @@ public:
             join_step(v, k + 1, std::move(next));
             return;
         }
+        // A carried word with one other needed column: the intermediate is
+        // merged into words (same (x, z window) rows OR their masks) through
+        // a temporary word sink instead of being materialized row by row.
+        if (v.carry && !D && words_) {
+            std::vector<ColRef> need;
+            for (const ColRef& r : v.needed[k])
+                if (r.source <= R) need.push_back(r);
+            const ColRef yb{0, 1}, ym{0, 2};
+            std::vector<ColRef> other;
+            for (const ColRef& r : need)
+                if (!(r == yb) && !(r == ym)) other.push_back(r);
+            if (other.size() == 1 && need.size() == 3 && spec.n_filters == 0) {
+                const ColRef refs3[3] = {other[0], yb, ym};
+                const SlotRef zb = slot_of(yb), wm = slot_of(ym);
+                Inter next = word_intermediate(*idx, offsets.get(), n, T, starts.get(), slot_of(other[0]), refs3, &zb,
+                                               &wm);
+                if (next.n == 0) return;
+                join_step(v, k + 1, std::move(next));
+                return;
+            }
+        }
         // Intermediate: the columns later steps and the head still need.
         std::vector<ColRef> refs;
         for (const ColRef& r : v.needed[k]) {
@@ -1012,21 +1033,28 @@ public:
     // The distinct (x, z) rows of a composition step, through a temporary
     // word sink: the join emits one word per (probe row, build word), the
     // block set dedups, the merged words expand to the rows (grouped by x).
+    // carried: the word is source 0's carried word (z base {0,1}, mask {0,2},
+    // given as zb / wbits); the intermediate stays in word form — one row per
+    // (x, z window) with the masks of all its derivations OR-ed — and keeps
+    // carrying it (refs[1] = {0,1}, refs[2] = {0,2}).
     Inter word_intermediate(JoinIndex& idx, const u64* offsets, u64 n, u64 T, const u32* starts, const SlotRef& left,
-                            const ColRef (&refs)[2]) {
+                            const ColRef* refs, const SlotRef* zb = nullptr, const SlotRef* wbits = nullptr) {
+        const bool carried = zb != nullptr;
         RelState tmp;
         tmp.name = "(intermediate)";
         tmp.arity = 2;
         tmp.hash_mode = tmp.block_mode = tmp.levels_mode = tmp.word_sink = true;
-        tmp.delta.cols.resize(2);
+        tmp.word_mode = carried;
+        tmp.temp = true;
+        tmp.delta.cols.resize(carried ? 3 : 2);
         HeadSink sk;
         OutSpec spec;
         spec.shift = st_.key_shift;
         spec.key_mode = 1;
         spec.n_out = 2;
         spec.col[0] = left;
-        spec.col[1] = SlotRef{idx.rows->cols[1].get(), 1};
-        spec.wbits = SlotRef{idx.rows->cols[2].get(), 1};
+        spec.col[1] = carried ? *zb : SlotRef{idx.rows->cols[1].get(), 1};
+        spec.wbits = carried ? *wbits : SlotRef{idx.rows->cols[2].get(), 1};
         spec.word_sink = 1;
         spec.tile_set = word_combine_;
         for (u64 t0 = 0; t0 < T; t0 += kFusedChunk) {
@@ -1049,15 +1077,15 @@ public:
             std::fprintf(stderr, "[fvlog]   word intermediate: %llu word outputs -> %llu rows\n",
                          static_cast<unsigned long long>(T), static_cast<unsigned long long>(nd));
         Inter next;
-        next.n = nd;
-        if (nd) {
+        const size_t nc = carried ? 3 : 2;
+        next.n = carried ? tmp.delta.n : nd;  // word form: one row per word
+        if (next.n) {
             next.owned = std::move(tmp.delta.cols);
         } else {
-            next.owned.emplace_back(c_, 0);
-            next.owned.emplace_back(c_, 0);
+            next.owned.clear();
+            for (size_t j = 0; j < nc; ++j) next.owned.emplace_back(c_, 0);
         }
-        next.cols[refs[0]] = next.owned[0].get();
-        next.cols[refs[1]] = next.owned[1].get();
+        for (size_t j = 0; j < nc; ++j) next.cols[refs[j]] = next.owned[j].get();
         return next;
     }
 
@@ -1631,7 +1659,7 @@ public:
             s.keys = DBuf<u64>();
             s.cap = 0;
             const u64 nd = finish_delta(r, std::move(tk), tuples);
-            if (r.word_sparse) leave_word_mode(r);
+            if (r.word_sparse && !r.temp) leave_word_mode(r);
             return nd;
         }
         invalidate(r);
@@ -1642,7 +1670,7 @@ public:
         if (nw == 0) {
             r.delta = std::move(Dv);
             set_old(r, nullptr);
-            if (r.word_sparse) leave_word_mode(r);
+            if (r.word_sparse && !r.temp) leave_word_mode(r);
             return 0;
         }
         r.keys.count += tuples;
@@ -1678,7 +1706,7 @@ public:
             delta_index->rows = &r.delta;
             r.indexes.emplace(std::make_pair(static_cast<int>(kDelta), 0u), std::move(delta_index));
         }
-        if (r.word_sparse) leave_word_mode(r);
+        if (r.word_sparse && !r.temp) leave_word_mode(r);
         return tuples;
     }
 

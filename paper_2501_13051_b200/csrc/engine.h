@@ -208,6 +208,9 @@ struct RelState {
     // Word forms of this relation's versions built for composition joins
     // (key: Which), invalidated with `indexes`.
     std::map<int, std::unique_ptr<WordBuild>> word_builds;
+    // A join's temporary word sink (word intermediates): never leaves the
+    // word form (its result is consumed right away).
+    bool temp = false;
     // Partitioned runs: the home column's owner is owner(v >> owner_shift).
     // A word-form relation owns whole 32-value windows (shift 5), so every
     // word of its DELTA lives on one rank.
