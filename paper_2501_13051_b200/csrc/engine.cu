@@ -2090,6 +2090,7 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         // is this rank's share).
         const Plan* alt = nullptr;
         size_t alt_index = 0;
+        std::vector<u8> alt_old;  // old_src of the alternative order
     };
     std::vector<DistPlan> dplans;
     std::deque<Plan> reordered;  // delta-first plans (stable addresses)
@@ -2150,14 +2151,17 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         for (auto& v : variants) dplans.push_back(dist_plan(*v.plan, idb, home));
         for (auto& v : variants) {
             const Plan& p = *v.plan;
-            if (v.delta_source != 1 || p.sources.size() != 2 || idb.count(p.sources[0].relation) ||
-                !Engine::word_step_ok(p, 0))
-                continue;
+            if (v.delta_source != 1 || p.sources.size() != 2 || !Engine::word_step_ok(p, 0)) continue;
             Plan rp;
             std::vector<u32> order;
             if (!delta_first_plan(p, 1, rp, &order)) continue;
+            // The other atom becomes the build side, probed on its join
+            // column: only when that index is cheap — column 0 (a run index
+            // of the sorted version) or a static EDB relation.
+            if (rp.joins[0].right_col != 0 && idb.count(rp.sources[1].relation)) continue;
             reordered.push_back(std::move(rp));
             v.alt = &reordered.back();
+            v.alt_old = {0, v.old_src.empty() ? u8(0) : v.old_src[0]};
             dplans.push_back(dist_plan(*v.alt, idb, home));
             v.alt_index = dplans.size() - 1;
         }
@@ -2309,10 +2313,13 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
             RelState& hr = *st->relations.at(v.plan->head);
             HeadSink* sink = hr.hash_mode ? &sinks[v.plan->head] : nullptr;
             if (v.alt && hr.word_sink && reverse_env) {
+                // DELTA's rows (words when it is word form) against the other
+                // atom's rows: probe the smaller side.
                 const RelState& dr = *st->relations.at(v.plan->sources[1].relation);
                 const RelState& pr = *st->relations.at(v.plan->sources[0].relation);
-                if (dr.word_mode && (reverse_always || eng.dist() || 2 * dr.delta.n < pr.full.n)) {
-                    eng.exec_variant(*v.alt, dplans[v.alt_index], 0, {}, pooled[v.plan->head], sink);
+                const u64 other = v.old_src.empty() || !v.old_src[0] || pr.old_is_full ? pr.rows() : pr.full_old.n;
+                if (reverse_always || (eng.dist() && dr.word_mode) || (!eng.dist() && 2 * dr.delta.n < other)) {
+                    eng.exec_variant(*v.alt, dplans[v.alt_index], 0, v.alt_old, pooled[v.plan->head], sink);
                     continue;
                 }
             }
