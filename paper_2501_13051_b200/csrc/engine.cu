@@ -366,6 +366,16 @@ public:
 
     JoinIndex& index(RelState& r, u32 kc, Which which, u32 col) {
         if (which == kOld && r.old_is_full) which = kFull;
+        if (col == 1 && r.arity == 2 && !dist() && !r.levels_mode && r.hash_mode && by1_) {
+            if (which == kFull) {
+                if (!r.by1) {
+                    r.by1 = std::make_unique<JoinIndex>();
+                    build_index_on(r.full, 1, *r.by1, nullptr);
+                }
+                return *r.by1;
+            }
+            if (which == kOld && r.old_by1) return *r.old_by1;
+        }
         IndexMap& m = vindexes(r, kc);
         auto key = std::make_pair(static_cast<int>(which), col);
         auto it = m.find(key);
@@ -1763,6 +1773,40 @@ public:
         return finish_delta(r, std::move(keys), nd);
     }
 
+    // Merge DELTA (just built, sorted by column 0) into the (col 1, col 0)
+    // ordered copy of FULL: sort DELTA's (col 1, col 0) keys, one merge-path
+    // pass, the column-1 run index rebuilt.
+    void advance_by1(RelState& r, const DevVersion& d) {
+        JoinIndex& o = *r.by1;
+        const u64 nd = d.n, nf = o.rows->n;
+        std::vector<DBuf<u64>> words;
+        words.emplace_back(c_, nd);
+        u64* wp = words[0].get();
+        engine_pack_keys(c_, std::vector<const u32*>{d.cols[1].get(), d.cols[0].get()}, nd, st_.key_shift, &wp);
+        engine_sort_keys(c_, words, nd, 2, st_.key_shift);
+        DevVersion C, unused;
+        for (int j = 0; j < 2; ++j) {
+            C.cols.emplace_back(c_, nf + nd);
+            unused.cols.emplace_back(c_, nd);
+        }
+        std::vector<u64*> bw{words[0].get()};
+        // merge order (col 1, col 0); C keeps column semantics (cols[1] = col 1)
+        engine_merge(c_, std::vector<const u32*>{o.rows->cols[1].get(), o.rows->cols[0].get()}, nf, bw.data(), nd, 2,
+                     st_.key_shift, std::vector<u32*>{C.cols[1].get(), C.cols[0].get()},
+                     std::vector<u32*>{unused.cols[1].get(), unused.cols[0].get()}, c_->d_scalars + 47);
+        C.n = nf + nd;
+        auto ni = std::make_unique<JoinIndex>();
+        ni->owned = std::move(C);
+        ni->rows = &ni->owned;
+        engine_build_runs(c_, ni->owned.cols[1].get(), ni->owned.n, *ni);
+        // the replaced copy is FULL - DELTA's (exactly-once variants probe it)
+        r.old_by1 = r.keep_old && !r.old_is_full ? std::move(r.by1) : nullptr;
+        r.by1 = std::move(ni);
+        if (trace_)
+            std::fprintf(stderr, "[fvlog]   %s (col 1, col 0) copy: +%llu rows by merge\n", r.name.c_str(),
+                         static_cast<unsigned long long>(nd));
+    }
+
     // The iteration's nd new packed tuple keys become DELTA (grouped by
     // column 0 in levels mode, sorted and merged into FULL otherwise).
     u64 finish_delta(RelState& r, DBuf<u64>&& new_keys, u64 nd) {
@@ -1830,6 +1874,7 @@ public:
             Dv.lex_sorted = true;  // unpacked from the sorted keys
             set_old(r, &r.full);
             r.full = std::move(C);
+            if (r.by1) advance_by1(r, Dv);
             if (!r.old_is_full && full_words) r.word_builds.emplace(static_cast<int>(kOld), std::move(full_words));
         }
         r.delta = std::move(Dv);
@@ -1896,6 +1941,12 @@ private:
     const double block_sparse_bytes_ = [] {
         const char* e = std::getenv("FVLOG_BLOCK_SPARSE_BYTES");
         return e ? std::atof(e) : kBlockSparseMinBytes;
+    }();
+    // FVLOG_BY1=0: column-1 indexes of FULL re-sorted per iteration instead
+    // of maintained by merge.
+    const bool by1_ = [] {
+        const char* e = std::getenv("FVLOG_BY1");
+        return !(e && std::string(e) == "0");
     }();
     // FVLOG_WORDS=0: no word sinks, word builds or word intermediates.
     const bool words_ = [] {

@@ -205,6 +205,12 @@ struct RelState {
     // whole words into it; with word_mode off its DELTA is expanded back to
     // tuples at finalize. word_mode implies word_sink.
     bool word_sink = false;
+    // FULL ordered by (col 1, col 0) with its column-1 join index (binary,
+    // sorted FULL, single GPU): built once when a join first probes FULL on
+    // column 1, then maintained by merging each sorted DELTA into it (no
+    // per-iteration re-sort of FULL).
+    std::unique_ptr<JoinIndex> by1;
+    std::unique_ptr<JoinIndex> old_by1;  // the same for FULL - DELTA (the FULL the last merge replaced)
     // Word forms of this relation's versions built for composition joins
     // (key: Which), invalidated with `indexes`.
     std::map<int, std::unique_ptr<WordBuild>> word_builds;
