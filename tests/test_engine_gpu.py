@@ -350,9 +350,10 @@ def test_keyset_growth_paths_match_reference(ctx, grow, monkeypatch):
     {"FVLOG_INTER_PROBE_ROWS": "2", "FVLOG_WORDS": "0"},      # ... by sort-unique
     {"FVLOG_REVERSE": "1"},                                   # word compositions always probe DELTA's words
     {"FVLOG_REVERSE": "0"},                                   # ... never
+    {"FVLOG_BY1": "0"},                                       # column-1 indexes of FULL re-sorted every iteration
 ], ids=["keyset", "blocks", "blocks-overflow", "blocks-convert", "blocks-no-tile-set", "no-words",
         "words-overflow", "words-leave", "words-no-combine", "dump-sort", "inter-words", "inter-sort",
-        "reverse-always", "reverse-never"])
+        "reverse-always", "reverse-never", "by1-resort"])
 def test_dedup_sets_match_reference(ctx, setmode, monkeypatch):
     # FULL's dedup structure for binary/unary IDB relations: a BlockSet
     # (blocked bitmap, default) or a KeySet; every path must give the
