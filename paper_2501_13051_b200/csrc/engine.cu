@@ -431,7 +431,7 @@ public:
             idx.owned = std::move(sorted);
             idx.rows = &idx.owned;
         }
-        engine_build_runs(c_, idx.rows->cols[col].get(), idx.rows->n, idx);
+        engine_build_runs(c_, idx.rows->cols[col].get(), idx.rows->n, idx, st_.key_shift);
     }
 
     RowFilter source_filter(const PlanSource& s, const DevVersion& v) {
@@ -462,11 +462,18 @@ public:
     // All-to-all of routed rows. `route` has filled send buffers grouped by
     // destination with cnt/off; returns the received row count and fills
     // `recv` buffers (allocated here) for each column.
+    // d_cnt: the route kernel's per-destination counts, on the device; the
+    // count exchange gathers them there and returns send and receive counts
+    // with one host round trip.
     template <typename T>
-    u64 exchange(const std::vector<DBuf<T>>& send, const std::vector<u64>& cnt, const std::vector<u64>& off,
-                 std::vector<DBuf<T>>& recv) {
-        std::vector<u64> rcnt(world_), roff(world_);
-        c_->tx->exchange_counts(c_, cnt.data(), rcnt.data());
+    u64 exchange(const std::vector<DBuf<T>>& send, const u64* d_cnt, std::vector<DBuf<T>>& recv) {
+        std::vector<u64> cnt(world_), off(world_), rcnt(world_), roff(world_);
+        c_->tx->exchange_counts_dev(c_, d_cnt, cnt.data(), rcnt.data());
+        u64 run = 0;
+        for (u32 p = 0; p < world_; ++p) {
+            off[p] = run;
+            run += cnt[p];
+        }
         u64 total = 0;
         for (u32 p = 0; p < world_; ++p) {
             roff[p] = total;
@@ -499,9 +506,10 @@ public:
         std::vector<u64> cnt(world_), off(world_);
         RouteKey rk;
         rk.col = cur.cols.at(key);
-        engine_route(c_, cur.n, rk, world_, in, outp, {}, {}, cnt.data(), off.data());
+        DBuf<u64> d_cnt(c_, world_);
+        engine_route(c_, cur.n, rk, world_, in, outp, {}, {}, cnt.data(), off.data(), d_cnt.get());
         Inter next;
-        next.n = exchange(send, cnt, off, next.owned);
+        next.n = exchange(send, d_cnt.get(), next.owned);
         for (size_t j = 0; j < refs.size(); ++j) next.cols[refs[j]] = next.owned[j].get();
         return next;
     }
@@ -528,9 +536,10 @@ public:
         if (pool.arity >= 2 && home == 1) rk.mask = (u64(1) << st_.key_shift) - 1;
         rk.oshift = oshift;
         std::vector<u64> cnt(world_), off(world_);
-        engine_route(c_, pool.n, rk, world_, {}, {}, in, outp, cnt.data(), off.data());
+        DBuf<u64> d_cnt(c_, world_);
+        engine_route(c_, pool.n, rk, world_, {}, {}, in, outp, cnt.data(), off.data(), d_cnt.get());
         std::vector<DBuf<u64>> recv;
-        pool.n = exchange(send, cnt, off, recv);
+        pool.n = exchange(send, d_cnt.get(), recv);
         pool.words = std::move(recv);
         pool.cap = pool.n;
     }
@@ -589,7 +598,7 @@ public:
                                                 wb->words.cols[2].get(), std::max<u64>(n, 1));
             wb->words.lex_sorted = true;
             wb->idx.rows = &wb->words;
-            engine_build_runs(c_, wb->words.cols[0].get(), wb->words.n, wb->idx);
+            engine_build_runs(c_, wb->words.cols[0].get(), wb->words.n, wb->idx, st_.key_shift);
             if (trace_)
                 std::fprintf(stderr, "[fvlog]   word build of %s (full, from the bitmaps): %llu rows -> %llu words\n",
                              r.name.c_str(), static_cast<unsigned long long>(n),
@@ -620,7 +629,7 @@ public:
                         : 0;
         wb->words.lex_sorted = true;
         wb->idx.rows = &wb->words;
-        engine_build_runs(c_, wb->words.cols[0].get(), wb->words.n, wb->idx);
+        engine_build_runs(c_, wb->words.cols[0].get(), wb->words.n, wb->idx, st_.key_shift);
         if (trace_)
             std::fprintf(stderr, "[fvlog]   word build of %s (%s): %llu rows -> %llu words\n", r.name.c_str(),
                          which == kDelta ? "delta" : (which == kOld ? "old" : "full"),
@@ -1288,9 +1297,10 @@ public:
             RouteKey rk;
             rk.col = r.delta.cols[kc].get();
             std::vector<u64> cnt(world_), off(world_);
-            engine_route(c_, r.delta.n, rk, world_, in, outp, {}, {}, cnt.data(), off.data());
+            DBuf<u64> d_cnt(c_, world_);
+            engine_route(c_, r.delta.n, rk, world_, in, outp, {}, {}, cnt.data(), off.data(), d_cnt.get());
             std::vector<DBuf<u32>> recv;
-            const u64 n = exchange(send, cnt, off, recv);
+            const u64 n = exchange(send, d_cnt.get(), recv);
             CandPool pool;
             pool.arity = r.arity;
             pool.reserve(c_, n);
@@ -1689,10 +1699,18 @@ public:
         // is read (and cleared) from the DELTA bitmap.
         s.bits = DBuf<u32>(c_, nw);
         const bool idx_ok = s.gen0 == r.blocks.generation && r.blocks.capacity() <= (u64(1) << 27);
-        engine_blockset_collect(c_, s.keys.get(), idx_ok ? s.widx.get() : nullptr, nw, block_args(r), s.bits.get());
         auto delta_index = std::make_unique<JoinIndex>();
-        const bool grouped = engine_group_keys(c_, s.keys, nw, st_.key_shift, delta_index.get(), Dv.cols[0].get(),
-                                               Dv.cols[1].get(), s.bits.get(), Dv.cols[2].get());
+        // With valid recorded word indices the grouping scatter reads the
+        // masks from the DELTA bitmap itself (no collect pass).
+        bool grouped = idx_ok && engine_group_keys(c_, s.keys, nw, st_.key_shift, delta_index.get(), Dv.cols[0].get(),
+                                                   Dv.cols[1].get(), nullptr, Dv.cols[2].get(), s.widx.get(),
+                                                   r.blocks.dbits.get());
+        if (!grouped) {
+            engine_blockset_collect(c_, s.keys.get(), idx_ok ? s.widx.get() : nullptr, nw, block_args(r),
+                                    s.bits.get());
+            grouped = engine_group_keys(c_, s.keys, nw, st_.key_shift, delta_index.get(), Dv.cols[0].get(),
+                                        Dv.cols[1].get(), s.bits.get(), Dv.cols[2].get());
+        }
         if (!grouped) {
             // Domain too large for the counting sort: unpack, then order the
             // entries by x (stable LSD pass over column 0) and gather.
@@ -1798,7 +1816,7 @@ public:
         auto ni = std::make_unique<JoinIndex>();
         ni->owned = std::move(C);
         ni->rows = &ni->owned;
-        engine_build_runs(c_, ni->owned.cols[1].get(), ni->owned.n, *ni);
+        engine_build_runs(c_, ni->owned.cols[1].get(), ni->owned.n, *ni, st_.key_shift);
         // the replaced copy is FULL - DELTA's (exactly-once variants probe it)
         r.old_by1 = r.keep_old && !r.old_is_full ? std::move(r.by1) : nullptr;
         r.by1 = std::move(ni);

@@ -431,8 +431,11 @@ u64 engine_unique_unpack(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, u32
 // With col0/col1, the grouped rows are written as SoA columns instead
 // (keys left as they were). pay_in/pay_out: a u32 payload per key moved
 // along (word masks).
+// gather_idx / gather_src: the payload is gather_src[gather_idx[i]] instead
+// (cleared after the read) — the word masks straight from the DELTA bitmap.
 bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs = nullptr, u32* col0 = nullptr,
-                       u32* col1 = nullptr, const u32* pay_in = nullptr, u32* pay_out = nullptr);
+                       u32* col1 = nullptr, const u32* pay_in = nullptr, u32* pay_out = nullptr,
+                       const u32* gather_idx = nullptr, u32* gather_src = nullptr);
 // Word-form block-set insert (RelState::word_mode): n word keys with masks
 // `bits`, or packed binary tuple keys (bits null) as one-bit words. New bits
 // are OR-ed into FULL and into the DELTA bitmap (s.dbits); a word's first
@@ -493,7 +496,9 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
 // Single-source projection of n rows (side 0 only) into `spec`.
 void engine_project(Ctx* c, u64 n, const OutSpec& spec);
 // RLE of a sorted key column into (ukeys, ustart, ucount) + hash table.
-void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx);
+// key_bits (the key domain's bit width, when <= 24): a direct-address index
+// instead of runs + hash (no host readback).
+void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u32 key_bits = 0);
 // Pack SoA columns into W key words.
 void engine_pack_keys(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 shift, u64* const* words);
 // Merge sorted distinct A (SoA, arity) with sorted B keys (W words, dups
@@ -517,9 +522,11 @@ struct RouteKey {
 // Group n rows by destination rank: u32 columns `c32` and u64 columns `c64`
 // are scattered into the matching *_out buffers (capacity n) so that rows for
 // rank p occupy [off[p], off[p] + cnt[p]) (order inside a bucket unspecified).
+// d_counts_out (device, world entries): the counts stay on the device there
+// and cnt/off are not filled (no host round trip; the exchange reads them).
 void engine_route(Ctx* c, u64 n, const RouteKey& key, u32 world, const std::vector<const u32*>& c32,
                   const std::vector<u32*>& c32_out, const std::vector<const u64*>& c64,
-                  const std::vector<u64*>& c64_out, u64* cnt, u64* off);
+                  const std::vector<u64*>& c64_out, u64* cnt, u64* off, u64* d_counts_out = nullptr);
 // Sort W-word keys in place (LSD over words with a permutation payload).
 // Sort packed row keys lexicographically. group_only (one-word keys only):
 // order by the first column alone (rows grouped for a column-0 join index;

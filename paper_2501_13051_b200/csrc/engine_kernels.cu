@@ -882,6 +882,22 @@ struct RunsOp {
     }
 };
 
+// Direct-address run index of sorted keys: the first row of each run stores
+// its position at the run's value, the last row its length.
+__global__ void direct_start_kernel(const u32* __restrict__ keys, u64 n, u32* __restrict__ dstart) {
+    GRID_STRIDE(i, n) {
+        const u32 k = keys[i];
+        if (i == 0 || keys[i - 1] != k) dstart[k] = static_cast<u32>(i);
+    }
+}
+__global__ void direct_count_kernel(const u32* __restrict__ keys, u64 n, const u32* __restrict__ dstart,
+                                    u32* __restrict__ dcount) {
+    GRID_STRIDE(i, n) {
+        const u32 k = keys[i];
+        if (i + 1 == n || keys[i + 1] != k) dcount[k] = static_cast<u32>(i + 1 - dstart[k]);
+    }
+}
+
 __global__ void runs_count_kernel(const u32* __restrict__ ustart, u32* __restrict__ ucount, u64 nu, u64 n) {
     GRID_STRIDE(i, nu) {
         const u64 end = i + 1 < nu ? ustart[i + 1] : n;
@@ -1777,7 +1793,8 @@ __global__ void group_count_kernel(const u64* __restrict__ keys, u64 n, u32 shif
 __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 shift, const u64* __restrict__ base,
                                      u32* __restrict__ cursor, u64* __restrict__ out, u32* __restrict__ c0,
                                      u32* __restrict__ c1, const u32* __restrict__ pay_in,
-                                     u32* __restrict__ pay_out) {
+                                     u32* __restrict__ pay_out, const u32* __restrict__ gather_idx,
+                                     u32* __restrict__ gather_src) {
     const u64 n_round = ceil_div(n, 32) * 32;
     const u32 lane = lane_id();
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n_round; i += u64(gridDim.x) * blockDim.x) {
@@ -1803,7 +1820,15 @@ __global__ void group_scatter_kernel(const u64* __restrict__ keys, u64 n, u32 sh
 #endif
         }
         if (valid) {
-            if (pay_out) pay_out[pos] = pay_in[i];  // word masks travel with their keys
+            if (pay_out) {  // word masks travel with their keys
+                if (gather_idx) {  // read (and clear) from the DELTA bitmap: no separate collect pass
+                    const u32 w = gather_idx[i];
+                    pay_out[pos] = gather_src[w];
+                    gather_src[w] = 0;
+                } else {
+                    pay_out[pos] = pay_in[i];
+                }
+            }
             if (c0) {  // unpacked straight into SoA columns
                 c0[pos] = g;
                 c1[pos] = static_cast<u32>(key & ((u64(1) << shift) - 1));
@@ -1890,6 +1915,14 @@ __device__ __forceinline__ u32 route_dest(const RouteKey& k, u64 i, u32 world) {
     if (k.col) v = k.col[i];
     else v = static_cast<u32>(k.hi ? (k.word[i] >> k.shift) : (k.word[i] & k.mask));
     return static_cast<u32>((static_cast<u64>(hash32(v >> k.oshift)) * world) >> 32);
+}
+
+__global__ void route_cursor_kernel(const u64* counts, u64* cursors, u32 world) {
+    u64 run = 0;
+    for (u32 p = 0; p < world; ++p) {
+        cursors[p] = run;
+        run += counts[p];
+    }
 }
 
 __global__ void route_count_kernel(RouteKey key, u64 n, u32 world, unsigned long long* counts) {
@@ -2205,7 +2238,7 @@ bool engine_hash_grow(Ctx* c, const KeySet& from, KeySet& to) {
 static void build_run_hash(Ctx* c, JoinIndex& idx);
 
 bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs, u32* col0, u32* col1,
-                       const u32* pay_in, u32* pay_out) {
+                       const u32* pay_in, u32* pay_out, const u32* gather_idx, u32* gather_src) {
     // Small domains with thousands of keys per value serialize on the
     // counters (C1: 2.6 K keys per value, 2.2 -> 5.1 ms); radix there.
     if (shift > kGroupMaxBits || n > (u64(kGroupMaxPerValue) << shift)) return false;
@@ -2221,7 +2254,8 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
         FV_CUDA(cudaGetLastError());
         tile_scan(c, GroupBaseOp{cnt.get(), base.get(), runs ? base32.get() : nullptr}, domain, nullptr);
         group_scatter_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys.get(), n, shift, base.get(), cursor.get(),
-                                                                  out.get(), col0, col1, pay_in, pay_out);
+                                                                  out.get(), col0, col1, pay_in, pay_out,
+                                                                  gather_idx, gather_src);
         FV_CUDA(cudaGetLastError());
         c->count_launch(2);
     }
@@ -2457,9 +2491,31 @@ void engine_project(Ctx* c, u64 n, const OutSpec& spec) {
     c->count_launch();
 }
 
-void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx) {
+void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u32 key_bits) {
     idx.n_unique = 0;
+    idx.domain = 0;
     if (n == 0) return;
+    // (only where the domain is not much larger than the rows: the arrays
+    // and their clearing scale with the domain)
+    if (key_bits && key_bits <= kGroupMaxBits && (u64(1) << key_bits) <= 16 * n) {
+        // Direct-address index over the value domain: run starts and lengths
+        // at their values (two light passes, no compaction, no hash table,
+        // no host readback of the run count).
+        const u64 domain = u64(1) << key_bits;
+        idx.domain = domain;
+        idx.n_unique = n;  // not counted; non-zero marks a non-empty index
+        idx.ustart = DBuf<u32>(c, domain);
+        idx.ucount = DBuf<u32>(c, domain);
+        idx.ukeys = DBuf<u32>();
+        idx.ht = HashIndex();
+        FV_CUDA(cudaMemsetAsync(idx.ucount.get(), 0, 4 * domain, c->stream));
+        ProfScope prof(c, "direct_index", 8.0 * double(n));
+        direct_start_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get());
+        direct_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), idx.ucount.get());
+        FV_CUDA(cudaGetLastError());
+        c->count_launch(2);
+        return;
+    }
     DBuf<u32> uk(c, n), us(c, n);
     u64* d = c->d_scalars + 16;
     tile_scan(c, RunsOp{sorted_keys, uk.get(), us.get()}, n, d);
@@ -2562,7 +2618,7 @@ void engine_merge(Ctx* c, const std::vector<const u32*>& a_cols, u64 n_a, u64* c
 
 void engine_route(Ctx* c, u64 n, const RouteKey& key, u32 world, const std::vector<const u32*>& c32,
                   const std::vector<u32*>& c32_out, const std::vector<const u64*>& c64,
-                  const std::vector<u64*>& c64_out, u64* cnt, u64* off) {
+                  const std::vector<u64*>& c64_out, u64* cnt, u64* off, u64* d_counts_out) {
     if (world > static_cast<u32>(kMaxRanks)) fail(FV_ERR_INVALID, "more than 64 ranks");
     if (c32.size() > FV_MAX_ARITY || c64.size() > 4) fail(FV_ERR_INVALID, "route: too many columns");
     DBuf<u64> d(c, 2 * world);
@@ -2574,14 +2630,23 @@ void engine_route(Ctx* c, u64 n, const RouteKey& key, u32 world, const std::vect
         FV_CUDA(cudaGetLastError());
         c->count_launch();
     }
-    d.download(cnt, world);
-    u64 run = 0;
-    for (u32 p = 0; p < world; ++p) {
-        off[p] = run;
-        run += cnt[p];
+    if (d_counts_out) {
+        // Counts stay on the device (the exchange gathers them there);
+        // the bucket cursors are their exclusive prefix, computed in place.
+        FV_CUDA(cudaMemcpyAsync(d_counts_out, d.get(), 8 * world, cudaMemcpyDeviceToDevice, c->stream));
+        route_cursor_kernel<<<1, 1, 0, c->stream>>>(d.get(), d.get() + world, world);
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+    } else {
+        d.download(cnt, world);
+        u64 run = 0;
+        for (u32 p = 0; p < world; ++p) {
+            off[p] = run;
+            run += cnt[p];
+        }
+        if (n) d.upload(off, world, world);  // cursors start at the bucket offsets
     }
     if (!n) return;
-    d.upload(off, world, world);  // cursors start at the bucket offsets
     Cols8 i32{};
     OutCols8 o32{};
     Words4 i64{}, o64{};

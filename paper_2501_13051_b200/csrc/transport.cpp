@@ -9,6 +9,13 @@
 
 namespace fv {
 
+void Transport::exchange_counts_dev(Ctx* c, const u64* d_send, u64* send_counts, u64* recv_counts) {
+    FV_CUDA(cudaMemcpyAsync(send_counts, d_send, sizeof(u64) * world(), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    exchange_counts(c, send_counts, recv_counts);
+}
+
+
 // ---- NCCL (resolved at run time) ---------------------------------------------
 
 namespace {
@@ -87,6 +94,17 @@ public:
         std::vector<u64> h(u64(world_) * world_);
         all.download(h.data(), h.size());
         for (int p = 0; p < world_; ++p) recv_counts[p] = h[u64(p) * world_ + rank_];
+    }
+
+    void exchange_counts_dev(Ctx* c, const u64* d_send, u64* send_counts, u64* recv_counts) override {
+        DBuf<u64> all(c, u64(world_) * world_);
+        nccl_check(nccl().AllGather(d_send, all.get(), world_, kNcclUint64, comm_, c->stream), "AllGather");
+        std::vector<u64> h(u64(world_) * world_);
+        all.download(h.data(), h.size());  // the one host round trip of the exchange
+        for (int p = 0; p < world_; ++p) {
+            send_counts[p] = h[u64(rank_) * world_ + p];
+            recv_counts[p] = h[u64(p) * world_ + rank_];
+        }
     }
 
     void exchange_rows(Ctx* c, const std::vector<ExchangeCol>& cols, const u64* scnt, const u64* soff,

@@ -31,6 +31,10 @@ public:
     virtual int world() const = 0;
     // send_counts[p] rows go to peer p; recv_counts[p] rows arrive from p.
     virtual void exchange_counts(Ctx* c, const u64* send_counts, u64* recv_counts) = 0;
+    // The same from send counts already on the device (written by the route
+    // kernel): fills both host arrays with one host round trip where the
+    // transport can (NCCL: an all-gather of the device counts, then one read).
+    virtual void exchange_counts_dev(Ctx* c, const u64* d_send_counts, u64* send_counts, u64* recv_counts);
     // Move every column's per-peer segments (offsets/counts in rows).
     virtual void exchange_rows(Ctx* c, const std::vector<ExchangeCol>& cols, const u64* scnt, const u64* soff,
                                const u64* rcnt, const u64* roff) = 0;
