@@ -104,12 +104,12 @@ struct Ctx {
     void reserve(size_t bytes);  // pre-map pool memory (fv_ctx_reserve)
     void release(void* p);
     void activate() const;  // cudaSetDevice
-    void sync();
+    void sync(const char* who = __builtin_FUNCTION());
     // Reserve `words` look-back status words and a fresh epoch; returns the
     // epoch to pass to the kernel. Also hands out a zeroed tile counter.
     u32 lookback_epoch(u64 words, u32** tile_counter);
     // Copy n u64 device scalars to host (one synchronisation).
-    void read_scalars(const u64* d, u64* h, int n);
+    void read_scalars(const u64* d, u64* h, int n, const char* who = __builtin_FUNCTION());
     void count_launch(int n = 1) { launches += n; }
 };
 
@@ -190,10 +190,10 @@ public:
     void upload(const T* h, u64 n, u64 offset = 0) {
         if (n) FV_CUDA(cudaMemcpyAsync(p_ + offset, h, sizeof(T) * n, cudaMemcpyHostToDevice, ctx_->stream));
     }
-    void download(T* h, u64 n, u64 offset = 0) const {
+    void download(T* h, u64 n, u64 offset = 0, const char* who = __builtin_FUNCTION()) const {
         if (n) {
             FV_CUDA(cudaMemcpyAsync(h, p_ + offset, sizeof(T) * n, cudaMemcpyDeviceToHost, ctx_->stream));
-            FV_CUDA(cudaStreamSynchronize(ctx_->stream));
+            ctx_->sync(who);  // counted as a host round trip
         }
     }
 

@@ -57,8 +57,14 @@ void Ctx::release(void* p) {
     if (p) cudaFreeAsync(p, stream);
 }
 
-void Ctx::sync() {
+namespace {
+// FVLOG_TRACE_SYNCS=1: name the function behind every host round trip.
+const bool g_trace_syncs = std::getenv("FVLOG_TRACE_SYNCS") != nullptr;
+}  // namespace
+
+void Ctx::sync(const char* who) {
     ++syncs;
+    if (g_trace_syncs) std::fprintf(stderr, "[sync] %s\n", who);
     FV_CUDA(cudaStreamSynchronize(stream));
     if (!prof_pending.empty()) prof_flush();
 }
@@ -130,8 +136,9 @@ u32 Ctx::lookback_epoch(u64 words, u32** tile_counter) {
     return lb.epoch;
 }
 
-void Ctx::read_scalars(const u64* d, u64* h, int n) {
+void Ctx::read_scalars(const u64* d, u64* h, int n, const char* who) {
     ++syncs;
+    if (g_trace_syncs) std::fprintf(stderr, "[sync] %s\n", who);
     FV_CUDA(cudaMemcpyAsync(pinned, d, sizeof(u64) * n, cudaMemcpyDeviceToHost, stream));
     FV_CUDA(cudaStreamSynchronize(stream));
     std::memcpy(h, pinned, sizeof(u64) * n);
