@@ -271,6 +271,38 @@ __device__ __forceinline__ u64 lookback_thread(const u64* status, u32 tile, u32 
     return excl;
 }
 
+// lookback_thread with Q predecessors' words loaded per round (independent
+// loads; with slot = the thread's lane-contiguous index each round is one
+// coalesced row per warp), consumed newest first up to the first inclusive.
+template <int Q>
+__device__ __forceinline__ u64 lookback_thread_deep(const u64* status, u32 tile, u32 stride, u32 slot,
+                                                    u32 epoch) {
+    u64 excl = 0;
+    long long t = static_cast<long long>(tile) - 1;
+    while (t >= 0) {
+        u64 w[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            w[q] = t - q >= 0 ? ld_relaxed_u64(status + u64(t - q) * stride + slot) : lb_pack(epoch, kLbFlagInclusive, 0);
+        bool done = false;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (done) break;
+            while (!lb_valid(w[q], epoch)) {
+#ifdef FV_LB_SLEEP
+                __nanosleep(FV_LB_SLEEP);
+#endif
+                w[q] = ld_relaxed_u64(status + u64(t - q) * stride + slot);
+            }
+            excl += lb_value(w[q]);
+            done = lb_flag(w[q]) == kLbFlagInclusive;
+        }
+        if (done) break;
+        t -= Q;
+    }
+    return excl;
+}
+
 // Warp-cooperative look-back (lane-parallel window of 32 predecessors);
 // call from all lanes of one warp; returns the exclusive prefix in every lane.
 __device__ __forceinline__ u64 lookback_warp(const u64* status, u32 tile, u32 epoch) {

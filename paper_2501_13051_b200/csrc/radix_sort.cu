@@ -20,6 +20,8 @@
 // HBM roofline per pass: n * 2 * (sizeof(K) + sizeof(payload)) bytes.
 #include "radix_sort.h"
 
+#include <type_traits>
+
 namespace fv {
 
 namespace {
@@ -175,11 +177,36 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 phase) {
 #ifndef FV_SORT_BULK
 #define FV_SORT_BULK 1
 #endif
+// Resident CTAs per SM the register budget is cut for (smem carveout at
+// its maximum so 4 tiles fit): u64 keys + payload keep 3 (less spilling).
+#ifndef FV_SORT_MINB
+#define FV_SORT_MINB 4
+#endif
+template <typename K, bool HAS_VAL>
+constexpr int sort_min_blocks() { return sizeof(K) == 8 && HAS_VAL ? 3 : FV_SORT_MINB; }
+// Early counts: the tile's digit counts come from a shared-atomic histogram
+// right after the load and are published before the ranking, so a
+// successor's look-back no longer waits for this tile's ranking.
+#ifndef FV_SORT_EARLY
+#define FV_SORT_EARLY 1
+#endif
+// Peer masks from match.any (1) instead of one ballot per digit bit (0).
+#ifndef FV_SORT_MATCH
+#define FV_SORT_MATCH 0
+#endif
+// Look-back depth: predecessors' status words loaded per round (one
+// coalesced row of a warp's 32 digits each).
+#ifndef FV_SORT_LBQ
+#define FV_SORT_LBQ 4
+#endif
+#ifndef FV_SORT_CARVE
+#define FV_SORT_CARVE 100
+#endif
 
 // ---- onesweep pass ------------------------------------------------------------
 
 template <typename K, bool HAS_VAL>
-__global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
+__global__ void __launch_bounds__(kSortBlock, (sort_min_blocks<K, HAS_VAL>())) onesweep_kernel(
     const K* __restrict__ keys_in, K* __restrict__ keys_out, const u32* __restrict__ vals_in,
     u32* __restrict__ vals_out, u64 n, u32 shift, u32 mask, const u64* __restrict__ bins,
     u64* __restrict__ status, u32 epoch, u32* __restrict__ tile_counter) {
@@ -192,6 +219,7 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
     u32* s_vals = reinterpret_cast<u32*>(s_raw + sizeof(K) * TILE);
     __shared__ u32 s_whist[kSortWarps][kRadix];
     __shared__ u32 s_block_excl[kRadix];
+    __shared__ u32 s_count[kRadix];
     __shared__ u64 s_global[kRadix];
     __shared__ u32 s_tile;
     __shared__ u32 s_warp_sums[kSortWarps];
@@ -203,15 +231,15 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
         if (FV_SORT_BULK) mbar_init(&s_bar, 1);
     }
     for (u32 i = tid; i < kSortWarps * kRadix; i += kSortBlock) (&s_whist[0][0])[i] = 0;
+    if (FV_SORT_EARLY) s_count[tid] = 0;
     __syncthreads();
     const u32 tile = s_tile;
     const u64 tile_base = u64(tile) * TILE;
-    const u64 warp_base = tile_base + u64(warp) * WARP_TILE;
 
-    K key[ITEMS];
-    u32 val[ITEMS];
-    u32 rank[ITEMS];
     u32 dig[ITEMS];
+    // The tile is staged in shared memory and only the digits stay in
+    // registers through ranking and look-back (the keys are re-read for the
+    // exchange), which keeps 4 CTAs per SM without spilling the key array.
     // Full tiles of 16-byte aligned arrays arrive by one TMA bulk copy per
     // array; the partial last tile (and unaligned inputs) load directly.
     const bool bulk = FV_SORT_BULK && tile_base + TILE <= n &&
@@ -225,69 +253,91 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
             if (HAS_VAL) bulk_load(s_vals, vals_in + tile_base, vb, &s_bar);
         }
         mbar_wait(&s_bar, 0);
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-            const u32 li = warp * WARP_TILE + k * 32 + lane;
-            key[k] = s_keys[li];
-            if (HAS_VAL) val[k] = s_vals[li];
-            dig[k] = digit_of(key[k], shift, mask);
-        }
     } else {
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
-            const u64 i = warp_base + u64(k) * 32 + lane;
-            const bool valid = i < n;
-            key[k] = valid ? keys_in[i] : K(0);
-            if (HAS_VAL) val[k] = valid ? vals_in[i] : 0u;
-            dig[k] = valid ? digit_of(key[k], shift, mask) : 0xffffu;
+            const u32 li = warp * WARP_TILE + k * 32 + lane;
+            const u64 i = tile_base + li;
+            if (i < n) {
+                s_keys[li] = keys_in[i];
+                if (HAS_VAL) s_vals[li] = vals_in[i];
+            }
         }
+        __syncwarp();  // each warp reads back only its own slice
     }
-    // Warp-level stable ranking, item-major (k outer, lane inner) = input order.
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
-        const u32 d = dig[k];
-        // Lanes with the same digit, from one ballot per digit bit (cheaper
-        // than match.any); out-of-range lanes only match each other.
-        const bool valid_item = d != 0xffffu;
-        u32 peers = __ballot_sync(0xffffffffu, valid_item);
-        if (!valid_item) peers = ~peers;
-#pragma unroll
-        for (int b = 0; b < kRadixBits; ++b) {
-            if (!((mask >> b) & 1u)) break;
-            const u32 x = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            peers &= ((d >> b) & 1u) ? x : ~x;
-        }
-        const u32 leader = __ffs(peers) - 1;
-        u32 b = 0;
-        if (d != 0xffffu && lane == leader) {
-            b = s_whist[warp][d];
-            s_whist[warp][d] = b + __popc(peers);
-        }
-        b = __shfl_sync(0xffffffffu, b, leader);
-        rank[k] = b + __popc(peers & lanemask_lt());
-        // The next item's leader for this digit may be another lane: order
-        // this lane's counter update before its read (compute-sanitizer
-        // racecheck flagged the pair without it).
-        __syncwarp();
+        const u32 li = warp * WARP_TILE + k * 32 + lane;
+        dig[k] = tile_base + li < n ? digit_of(s_keys[li], shift, mask) : 0xffffu;
     }
+    u64* my_status = status + u64(tile) * kRadix + tid;
+    if (FV_SORT_EARLY) {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k)
+            if (dig[k] != 0xffffu) atomicAdd(&s_count[dig[k]], 1u);
+        __syncthreads();
+        st_relaxed_u64(my_status, lb_pack(epoch, tile == 0 ? kLbFlagInclusive : kLbFlagAggregate, s_count[tid]));
+    }
+    // Warp-level stable ranking, item-major (k outer, lane inner) = input order.
+    // Lanes with the same digit come from one ballot per digit bit (cheaper
+    // than match.any): peers &= ~(ballot ^ (bit ? ~0 : 0)). A full tile with
+    // a full 8-bit digit (every pass but a short last one) runs the
+    // straight-line form; out-of-range lanes of the last tile only match
+    // each other.
+    auto rank_items = [&](auto partial_tag, auto full_digit_tag) {
+        constexpr bool PARTIAL = decltype(partial_tag)::value;
+        constexpr bool FULL_DIGIT = decltype(full_digit_tag)::value;
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const u32 d = dig[k];
+            u32 peers = ~0u;
+            if (FV_SORT_MATCH) {
+                peers = __match_any_sync(0xffffffffu, d);
+            } else if (PARTIAL) {
+                const bool valid_item = d != 0xffffu;
+                peers = __ballot_sync(0xffffffffu, valid_item);
+                if (!valid_item) peers = ~peers;
+            }
+#pragma unroll
+            for (int b = 0; b < (FV_SORT_MATCH ? 0 : kRadixBits); ++b) {
+                if (!FULL_DIGIT && !((mask >> b) & 1u)) break;
+                const u32 bit = (d >> b) & 1u;
+                const u32 x = __ballot_sync(0xffffffffu, bit);
+                peers &= ~(x ^ (0u - bit));
+            }
+            const u32 leader = __ffs(peers) - 1;
+            u32 b = 0;
+            if ((!PARTIAL || d != 0xffffu) && lane == leader) {
+                b = s_whist[warp][d];
+                s_whist[warp][d] = b + __popc(peers);
+            }
+            b = __shfl_sync(0xffffffffu, b, leader);
+            dig[k] = d | ((b + __popc(peers & lanemask_lt())) << 16);  // digit | rank << 16
+            // The next item's leader for this digit may be another lane: order
+            // this lane's counter update before its read (compute-sanitizer
+            // racecheck flagged the pair without it).
+            __syncwarp();
+        }
+    };
+    using True = std::integral_constant<bool, true>;
+    using False = std::integral_constant<bool, false>;
+    const bool partial_tile = tile_base + TILE > n;
+    if (partial_tile) rank_items(True{}, False{});
+    else if (mask == 0xffu) rank_items(False{}, True{});
+    else rank_items(False{}, False{});
     __syncthreads();
 
     // Thread d owns digit d: exclusive scan across warps, tile count.
     const u32 d = tid;
+    u32 wcount[kSortWarps];
     u32 count = 0;
 #pragma unroll
     for (int w = 0; w < kSortWarps; ++w) {
-        const u32 t = s_whist[w][d];
-        s_whist[w][d] = count;
-        count += t;
+        wcount[w] = s_whist[w][d];
+        count += wcount[w];
     }
-    // Publish early so successors are not held up by our own look-back.
-    u64* my_status = status + u64(tile) * kRadix + d;
-    if (tile == 0) {
-        st_relaxed_u64(my_status, lb_pack(epoch, kLbFlagInclusive, count));
-    } else {
-        st_relaxed_u64(my_status, lb_pack(epoch, kLbFlagAggregate, count));
-    }
+    // Publish before the look-back so successors are not held up by it.
+    if (!FV_SORT_EARLY) st_relaxed_u64(my_status, lb_pack(epoch, tile == 0 ? kLbFlagInclusive : kLbFlagAggregate, count));
     // Block exclusive scan of counts across digits (for the smem exchange).
     {
         u32 x = count;
@@ -306,21 +356,40 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
             }
         }
         __syncthreads();
-        s_block_excl[d] = s_warp_sums[warp] + x - count;
+        const u32 block_excl = s_warp_sums[warp] + x - count;
+        s_block_excl[d] = block_excl;
+        // s_whist[w][d] := tile slot of warp w's first item of digit d
+        u32 run = block_excl;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) {
+            s_whist[w][d] = run;
+            run += wcount[w];
+        }
     }
     u64 excl = 0;
     if (tile > 0) {
-        excl = lookback_thread(status, tile, kRadix, d, epoch);
+        excl = lookback_thread_deep<FV_SORT_LBQ>(status, tile, kRadix, d, epoch);
         st_relaxed_u64(my_status, lb_pack(epoch, kLbFlagInclusive, excl + count));
     }
-    s_global[d] = bins[d] + excl;
+    // Output position of tile slot i of digit dd: s_global[dd] + i.
+    s_global[d] = bins[d] + excl - s_block_excl[d];
     __syncthreads();
 
     // Exchange into digit order within the tile.
+    K key[ITEMS];
+    u32 val[ITEMS];
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
-        if (dig[k] != 0xffffu) {
-            const u32 lp = s_block_excl[dig[k]] + s_whist[warp][dig[k]] + rank[k];
+        const u32 li = warp * WARP_TILE + k * 32 + lane;
+        key[k] = s_keys[li];
+        if (HAS_VAL) val[k] = s_vals[li];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u32 dk = dig[k] & 0xffffu;
+        if (dk != 0xffffu) {
+            const u32 lp = s_whist[warp][dk] + (dig[k] >> 16);
             s_keys[lp] = key[k];
             if (HAS_VAL) s_vals[lp] = val[k];
         }
@@ -331,7 +400,7 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_kernel(
     for (u32 i = tid; i < valid_count; i += kSortBlock) {
         const K kk = s_keys[i];
         const u32 dd = digit_of(kk, shift, mask);
-        const u64 pos = s_global[dd] + (i - s_block_excl[dd]);
+        const u64 pos = s_global[dd] + i;
         keys_out[pos] = kk;
         if (HAS_VAL) vals_out[pos] = s_vals[i];
     }
@@ -349,6 +418,9 @@ void onesweep_pass(Ctx* c, const K* kin, K* kout, const u32* vin, u32* vout, u64
     static const bool smem_ok = [&] {
         FV_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, HAS_VAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
+        if (FV_SORT_CARVE >= 0)
+            FV_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, HAS_VAL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         FV_SORT_CARVE));
         return true;
     }();
     (void)smem_ok;
