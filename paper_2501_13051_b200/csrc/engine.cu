@@ -623,9 +623,13 @@ public:
             src = &sorted;
         }
         for (int j = 0; j < 3; ++j) wb->words.cols.emplace_back(c_, std::max<u64>(n, 1));
+        // Sized by the row count (rows past the words carry x = 0xffffffff,
+        // which no index holds) unless that could be a value (32-bit keys)
+        // or the trace wants the word count.
+        const bool exact = st_.key_shift >= 32 || trace_;
         wb->words.n = n ? engine_tuples_to_words(c_, src->cols[0].get(), src->cols[1].get(), n,
                                                  wb->words.cols[0].get(), wb->words.cols[1].get(),
-                                                 wb->words.cols[2].get())
+                                                 wb->words.cols[2].get(), exact)
                         : 0;
         wb->words.lex_sorted = true;
         wb->idx.rows = &wb->words;
@@ -956,7 +960,7 @@ public:
         }
         if (inter_word) {
             Inter next = word_intermediate(*idx, offsets.get(), n, T, starts.get(), slot_of(inter_refs[0]),
-                                           inter_refs);
+                                           inter_refs, temp_ratio_[std::make_tuple(&plan, k, delta_source)]);
             if (!D && next.n == 0) return;
             join_step(v, k + 1, std::move(next));
             return;
@@ -975,8 +979,8 @@ public:
             if (other.size() == 1 && need.size() == 3 && spec.n_filters == 0) {
                 const ColRef refs3[3] = {other[0], yb, ym};
                 const SlotRef zb = slot_of(yb), wm = slot_of(ym);
-                Inter next = word_intermediate(*idx, offsets.get(), n, T, starts.get(), slot_of(other[0]), refs3, &zb,
-                                               &wm);
+                Inter next = word_intermediate(*idx, offsets.get(), n, T, starts.get(), slot_of(other[0]), refs3,
+                                               temp_ratio_[std::make_tuple(&plan, k, delta_source)], &zb, &wm);
                 if (next.n == 0) return;
                 join_step(v, k + 1, std::move(next));
                 return;
@@ -1057,9 +1061,13 @@ public:
     // (x, z window) with the masks of all its derivations OR-ed — and keeps
     // carrying it (refs[1] = {0,1}, refs[2] = {0,2}).
     Inter word_intermediate(JoinIndex& idx, const u64* offsets, u64 n, u64 T, const u32* starts, const SlotRef& left,
-                            const ColRef* refs, const SlotRef* zb = nullptr, const SlotRef* wbits = nullptr) {
+                            const ColRef* refs, double& block_ratio, const SlotRef* zb = nullptr,
+                            const SlotRef* wbits = nullptr) {
         const bool carried = zb != nullptr;
         RelState tmp;
+        // new blocks per output measured at this call site last time: the
+        // directory is sized for it up front (no overflow-list rounds)
+        tmp.blocks.ratio = block_ratio;
         tmp.name = "(intermediate)";
         tmp.arity = 2;
         tmp.hash_mode = tmp.block_mode = tmp.levels_mode = tmp.word_sink = true;
@@ -1092,6 +1100,7 @@ public:
         CandPool none;
         none.arity = 2;
         const u64 nd = T ? hash_finalize(tmp, sk, none) : 0;
+        if (T) block_ratio = tmp.blocks.ratio;
         if (trace_)
             std::fprintf(stderr, "[fvlog]   word intermediate: %llu word outputs -> %llu rows\n",
                          static_cast<unsigned long long>(T), static_cast<unsigned long long>(nd));
@@ -1119,6 +1128,8 @@ public:
     // re-measured whenever its intermediates grow 4x past the last
     // measurement (early iterations often have no repeats yet).
     using InterKey = std::tuple<const Plan*, size_t, long>;
+    // Word intermediates' new-blocks-per-output ratio, per plan step.
+    std::map<std::tuple<const Plan*, size_t, long>, double> temp_ratio_;
     struct InterPolicy {
         bool on = false;
         u64 measured = 0;  // size of the last measured intermediate (0: never)
@@ -1179,48 +1190,106 @@ public:
     }
 
     // Sort candidates and fold them into (full, delta); returns |DELTA|.
-    u64 dedup_merge(DevVersion& full, DevVersion& delta, IndexMap& indexes, u32 arity, CandPool& cand,
-                    RelState* home = nullptr) {
-        if (cand.n == 0) {
-            delta = DevVersion();
-            delta.n = 0;
-            delta.cols.resize(arity);
-            indexes.clear();
-            if (home) home->word_builds.clear();
-            if (home) set_old(*home, nullptr);
-            return 0;
-        }
-        engine_sort_keys(c_, cand.words, cand.n, arity, st_.key_shift);
+    // Sort-merge dedup in two halves so that several relations' merges share
+    // one host round trip for their new-row counts: merge_launch enqueues the
+    // sort and the merge-path merge (new count to a device slot), then
+    // merge_complete installs FULL and DELTA once the count is on the host.
+    struct PendingMerge {
+        DevVersion* full = nullptr;
+        DevVersion* delta = nullptr;
+        IndexMap* indexes = nullptr;
+        RelState* home = nullptr;
+        u32 arity = 0;
         DevVersion C, Dv;
+        u64 cand_n = 0;
+        DBuf<u64> d_new;
+    };
+
+    PendingMerge merge_launch(DevVersion& full, DevVersion& delta, IndexMap& indexes, u32 arity, CandPool& cand,
+                              RelState* home) {
+        PendingMerge pm;
+        pm.full = &full;
+        pm.delta = &delta;
+        pm.indexes = &indexes;
+        pm.home = home;
+        pm.arity = arity;
+        pm.cand_n = cand.n;
+        if (cand.n == 0) return pm;
+        engine_sort_keys(c_, cand.words, cand.n, arity, st_.key_shift);
         for (u32 j = 0; j < arity; ++j) {
-            C.cols.emplace_back(c_, full.n + cand.n);
-            Dv.cols.emplace_back(c_, cand.n);
+            pm.C.cols.emplace_back(c_, full.n + cand.n);
+            pm.Dv.cols.emplace_back(c_, cand.n);
         }
         std::vector<u64*> bw;
         for (auto& w : cand.words) bw.push_back(w.get());
         std::vector<u32*> cc, dc;
         for (u32 j = 0; j < arity; ++j) {
-            cc.push_back(C.cols[j].get());
-            dc.push_back(Dv.cols[j].get());
+            cc.push_back(pm.C.cols[j].get());
+            dc.push_back(pm.Dv.cols[j].get());
         }
-        u64* d_new = c_->d_scalars + 21;
-        engine_merge(c_, full.ptrs(), full.n, bw.data(), cand.n, arity, st_.key_shift, cc, dc, d_new);
-        u64 nd = 0;
-        c_->read_scalars(d_new, &nd, 1);
-        c_->prof_add_bytes("merge_dedup", 8.0 * double(nd) * arity);
-        C.n = full.n + nd;
-        Dv.n = nd;
-        C.lex_sorted = Dv.lex_sorted = true;  // merge-path output of sorted inputs
+        pm.d_new = DBuf<u64>(c_, 1);
+        engine_merge(c_, full.ptrs(), full.n, bw.data(), cand.n, arity, st_.key_shift, cc, dc, pm.d_new.get());
+        return pm;
+    }
+
+    u64 merge_complete(PendingMerge& pm, u64 nd) {
+        DevVersion& full = *pm.full;
+        DevVersion& delta = *pm.delta;
+        RelState* home = pm.home;
+        if (pm.cand_n == 0) {
+            delta = DevVersion();
+            delta.n = 0;
+            delta.cols.resize(pm.arity);
+            pm.indexes->clear();
+            if (home) home->word_builds.clear();
+            if (home) set_old(*home, nullptr);
+            return 0;
+        }
+        c_->prof_add_bytes("merge_dedup", 8.0 * double(nd) * pm.arity);
+        pm.C.n = full.n + nd;
+        pm.Dv.n = nd;
+        pm.C.lex_sorted = pm.Dv.lex_sorted = true;  // merge-path output of sorted inputs
         if (home) home->word_builds.clear();
         if (home && nd) {
             set_old(*home, &full);
         } else if (home) {
             set_old(*home, nullptr);
         }
-        full = std::move(C);
-        delta = std::move(Dv);
-        indexes.clear();
+        full = std::move(pm.C);
+        delta = std::move(pm.Dv);
+        pm.indexes->clear();
         return nd;
+    }
+
+    // Complete several pending merges with one read of their counts.
+    std::vector<u64> merge_complete_all(std::vector<PendingMerge>& pms) {
+        std::vector<u64> nds(pms.size(), 0);
+        size_t live = 0;
+        for (auto& pm : pms) live += pm.cand_n ? 1 : 0;
+        if (live) {
+            if (batch_pinned_cap_ < live) {
+                if (batch_pinned_) cudaFreeHost(batch_pinned_);
+                batch_pinned_cap_ = std::max<size_t>(256, 2 * live);
+                FV_CUDA(cudaMallocHost(&batch_pinned_, sizeof(u64) * batch_pinned_cap_));
+            }
+            size_t q = 0;
+            for (auto& pm : pms)
+                if (pm.cand_n)
+                    FV_CUDA(cudaMemcpyAsync(batch_pinned_ + q++, pm.d_new.get(), 8, cudaMemcpyDeviceToHost, c_->stream));
+            c_->sync();
+            q = 0;
+            for (size_t i = 0; i < pms.size(); ++i)
+                if (pms[i].cand_n) nds[i] = batch_pinned_[q++];
+        }
+        for (size_t i = 0; i < pms.size(); ++i) nds[i] = merge_complete(pms[i], nds[i]);
+        return nds;
+    }
+
+    u64 dedup_merge(DevVersion& full, DevVersion& delta, IndexMap& indexes, u32 arity, CandPool& cand,
+                    RelState* home = nullptr) {
+        std::vector<PendingMerge> one;
+        one.push_back(merge_launch(full, delta, indexes, arity, cand, home));
+        return merge_complete_all(one)[0];
     }
 
     // A relation's versions changed: its join indexes and word builds go.
@@ -1246,14 +1315,21 @@ public:
 
     // Seed one copy of a relation from raw EDB rows (owner-filtered on kc
     // when partitioned).
-    void seed_copy(RelState& r, const DevVersion& v, u32 kc) {
+    // Sort-merged copies are only launched (pend): the caller completes
+    // every relation's seed merge with one read of the counts.
+    void seed_copy(RelState& r, const DevVersion& v, u32 kc, std::vector<PendingMerge>& pend) {
         CandPool pool = seed_pool(r, v, kc);
         if (kc == r.home && r.hash_mode) {
             HeadSink sink;
             hash_finalize(r, sink, pool);
             return;
         }
-        dedup_merge(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool, kc == r.home ? &r : nullptr);
+        pend.push_back(
+            merge_launch(vfull(r, kc), vdelta(r, kc), vindexes(r, kc), r.arity, pool, kc == r.home ? &r : nullptr));
+    }
+
+    PendingMerge merge_launch_home(RelState& r, CandPool& cand) {
+        return merge_launch(r.full, r.delta, r.indexes, r.arity, cand, &r);
     }
 
     CandPool seed_pool(RelState& r, const DevVersion& v, u32 kc) {
@@ -1498,10 +1574,14 @@ public:
 
     void block_reserve(RelState& r, HeadSink& s, u64 extra) {
         u64 nw = 0, ov = 0;
+        // No directory yet: the sink's count is the prefetched (or fresh,
+        // zero) value when there is one, not another round trip.
+        const bool pre_known = s.pre;
+        const u64 pre_nw = s.pre_vals[0];
         if (r.blocks.capacity()) read_block_counters(r, s, &nw, &ov);
         else s.pre = false;
         if (s.bound + extra > s.cap) {
-            const u64 have = r.blocks.capacity() ? nw : sink_count(s);
+            const u64 have = r.blocks.capacity() ? nw : pre_known ? pre_nw : sink_count(s);
             const u64 nc = std::max<u64>(have + extra, 2 * s.cap);
             DBuf<u64> nk(c_, nc);
             if (have) FV_CUDA(cudaMemcpyAsync(nk.get(), s.keys.get(), 8 * have, cudaMemcpyDeviceToDevice, c_->stream));
@@ -1608,6 +1688,27 @@ public:
         r.blocks.ratio = double(nb) / double(pool.n);
     }
 
+    // estimate_blocks for several heads' pools with one read of the counts.
+    void estimate_blocks_all(const std::vector<std::pair<RelState*, HeadSink*>>& heads,
+                             std::map<std::string, CandPool>& pooled) {
+        std::vector<RelState*> need;
+        for (auto& [r, s] : heads) {
+            const CandPool& pool = pooled.at(r->name);
+            if (r->hash_mode && r->block_mode && r->blocks.ratio <= 0 && pool.n >= (u64(1) << 16) && block_ratio_ < 0)
+                need.push_back(r);
+        }
+        if (need.size() < 2) return;  // (a single one reads its count in estimate_blocks)
+        DBuf<u64> d(c_, need.size());
+        for (size_t q = 0; q < need.size(); ++q) {
+            const CandPool& pool = pooled.at(need[q]->name);
+            engine_count_blocks_async(c_, pool.words[0].get(), pool.n, st_.key_shift, need[q]->arity, d.get() + q);
+        }
+        std::vector<u64> nb(need.size());
+        d.download(nb.data(), need.size());
+        for (size_t q = 0; q < need.size(); ++q)
+            need[q]->blocks.ratio = double(nb[q]) / double(pooled.at(need[q]->name).n);
+    }
+
     // Insert a head's pooled candidates (copies, unfused joins) into its set;
     // the new keys join the ones the fused joins appended.
     void insert_pool(RelState& r, HeadSink& s, CandPool& pool) {
@@ -1702,7 +1803,7 @@ public:
         auto delta_index = std::make_unique<JoinIndex>();
         // With valid recorded word indices the grouping scatter reads the
         // masks from the DELTA bitmap itself (no collect pass).
-        bool grouped = idx_ok && engine_group_keys(c_, s.keys, nw, st_.key_shift, delta_index.get(), Dv.cols[0].get(),
+        bool grouped = idx_ok && scatter_gather_ && engine_group_keys(c_, s.keys, nw, st_.key_shift, delta_index.get(), Dv.cols[0].get(),
                                                    Dv.cols[1].get(), nullptr, Dv.cols[2].get(), s.widx.get(),
                                                    r.blocks.dbits.get());
         if (!grouped) {
@@ -1975,6 +2076,13 @@ private:
     const u32 word_combine_ = [] {
         const char* e = std::getenv("FVLOG_WORD_COMBINE");
         return e ? static_cast<u32>(std::atoi(e) != 0) : 1u;
+    }();
+    // FVLOG_SCATTER_GATHER=1: the grouping scatter reads a word-form DELTA's
+    // masks from the DELTA bitmap itself instead of a separate collect pass
+    // (C2: 25.2 vs 24.85 ms per fixpoint with the collect pass, so off).
+    const bool scatter_gather_ = [] {
+        const char* e = std::getenv("FVLOG_SCATTER_GATHER");
+        return e && std::string(e) == "1";
     }();
     // FVLOG_BLOCK_TILE_SET=0: no tile-local dedup before the block-set probe.
     const u32 block_tile_set_ = [] {
@@ -2352,13 +2460,17 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     if (trace) tr("setup", t0, 0);
     // ---- seed: FULL = DELTA = dedup(EDB) (engine.cpp:148-161) ---------------
     const auto ts = Clock::now();
-    for (auto& [name, vp] : raw) {
-        RelState& r = *st->relations[name];
-        if (eng.partitioned(r)) {
-            for (u32 kc : r.keyset) eng.seed_copy(r, *vp, kc);
-        } else {
-            eng.seed_copy(r, *vp, 0);  // FULL empty: C = D = distinct rows
+    {
+        std::vector<Engine::PendingMerge> pend;
+        for (auto& [name, vp] : raw) {
+            RelState& r = *st->relations[name];
+            if (eng.partitioned(r)) {
+                for (u32 kc : r.keyset) eng.seed_copy(r, *vp, kc, pend);
+            } else {
+                eng.seed_copy(r, *vp, 0, pend);  // FULL empty: C = D = distinct rows
+            }
         }
+        eng.merge_complete_all(pend);
     }
     raw.clear();
     concat.clear();
@@ -2408,16 +2520,35 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
         bool any_pool = false;
         for (auto& [r, s] : set_heads) any_pool = any_pool || pooled.at(r->name).n > 0;
         if (any_pool) {
+            eng.estimate_blocks_all(set_heads, pooled);
             eng.prefetch_counters(set_heads);
             for (auto& [r, s] : set_heads) eng.insert_pool(*r, *s, pooled.at(r->name));
         }
         eng.prefetch_counters(set_heads);
-        for (auto& [name, pool] : pooled) {
-            RelState& r = *st->relations.at(name);
-            const u64 nd = r.hash_mode ? eng.hash_finalize(r, sinks[name], pool) : eng.dedup_merge_home(r, pool);
-            if (eng.dist()) eng.forward_delta(r);
-            counts.push_back(nd);
-            counts.push_back(r.rows());
+        {
+            // Sort-merged heads (single GPU) complete together: one read of
+            // their new-row counts.
+            std::vector<Engine::PendingMerge> pend;
+            std::vector<std::pair<size_t, RelState*>> pend_at;
+            for (auto& [name, pool] : pooled) {
+                RelState& r = *st->relations.at(name);
+                if (!r.hash_mode && !eng.dist()) {
+                    pend_at.emplace_back(counts.size(), &r);
+                    pend.push_back(eng.merge_launch_home(r, pool));
+                    counts.push_back(0);
+                    counts.push_back(0);
+                    continue;
+                }
+                const u64 nd = r.hash_mode ? eng.hash_finalize(r, sinks[name], pool) : eng.dedup_merge_home(r, pool);
+                if (eng.dist()) eng.forward_delta(r);
+                counts.push_back(nd);
+                counts.push_back(r.rows());
+            }
+            const std::vector<u64> nds = eng.merge_complete_all(pend);
+            for (size_t i = 0; i < pend.size(); ++i) {
+                counts[pend_at[i].first] = nds[i];
+                counts[pend_at[i].first + 1] = pend_at[i].second->rows();
+            }
         }
         eng.allreduce(counts);
         tr("finalize", tf, iteration);

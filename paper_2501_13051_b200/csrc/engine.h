@@ -453,12 +453,15 @@ void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, co
 u64 engine_blockset_fingerprint(Ctx* c, const BlockSet& s, u32 arity);
 // Distinct block ids among n packed keys (directory sizing).
 u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity);
+// The same count left in *d_out on the device (no host round trip).
+void engine_count_blocks_async(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity, u64* d_out);
 // Packed tuple keys of n word entries (word key, mask) into out, sized by
 // the caller to the sum of the masks' popcounts (no host readback).
 void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out);
 // Word form (x, z base, mask) of a lexicographically sorted binary version
 // of n rows; outputs sized n; returns the word count.
-u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits);
+u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits,
+                            bool exact = true);
 // The non-empty words of a binary block set in row-major (x, z) order —
 // FULL's word form straight from its bitmaps; outputs hold cap_out entries.
 u64 engine_blockset_words(Ctx* c, const BlockSet& s, u32* x, u32* zb, u32* bits, u64 cap_out);

@@ -884,21 +884,26 @@ struct RunsOp {
 
 // Direct-address run index of sorted keys: the first row of each run stores
 // its position at the run's value, the last row its length.
-__global__ void direct_start_kernel(const u32* __restrict__ keys, u64 n, u32* __restrict__ dstart) {
+// (keys >= domain: the 0xffffffff tail of a word build sized by its bound,
+// not indexed)
+__global__ void direct_start_kernel(const u32* __restrict__ keys, u64 n, u32* __restrict__ dstart, u64 domain) {
     GRID_STRIDE(i, n) {
         const u32 k = keys[i];
-        if (i == 0 || keys[i - 1] != k) dstart[k] = static_cast<u32>(i);
+        if (k < domain && (i == 0 || keys[i - 1] != k)) dstart[k] = static_cast<u32>(i);
     }
 }
 __global__ void direct_count_kernel(const u32* __restrict__ keys, u64 n, const u32* __restrict__ dstart,
-                                    u32* __restrict__ dcount) {
+                                    u32* __restrict__ dcount, u64 domain) {
     GRID_STRIDE(i, n) {
         const u32 k = keys[i];
-        if (i + 1 == n || keys[i + 1] != k) dcount[k] = static_cast<u32>(i + 1 - dstart[k]);
+        if (k < domain && (i + 1 == n || keys[i + 1] != k)) dcount[k] = static_cast<u32>(i + 1 - dstart[k]);
     }
 }
 
-__global__ void runs_count_kernel(const u32* __restrict__ ustart, u32* __restrict__ ucount, u64 nu, u64 n) {
+// d_nu (optional): the run count on the device; nu is then only its bound.
+__global__ void runs_count_kernel(const u32* __restrict__ ustart, u32* __restrict__ ucount, u64 nu, u64 n,
+                                  const u64* __restrict__ d_nu) {
+    if (d_nu) nu = *d_nu;
     GRID_STRIDE(i, nu) {
         const u64 end = i + 1 < nu ? ustart[i + 1] : n;
         ucount[i] = static_cast<u32>(end - ustart[i]);
@@ -906,7 +911,8 @@ __global__ void runs_count_kernel(const u32* __restrict__ ustart, u32* __restric
 }
 
 __global__ void hash_build_kernel(const u32* __restrict__ ukeys, u64 nu, unsigned long long* __restrict__ slots,
-                                  u32 mask) {
+                                  u32 mask, const u64* __restrict__ d_nu) {
+    if (d_nu) nu = *d_nu;
     GRID_STRIDE(i, nu) {
         const u32 key = ukeys[i];
         const unsigned long long packed = (static_cast<unsigned long long>(key) << 32) | u32(i);
@@ -1909,6 +1915,9 @@ struct UniqueUnpackOp {
 constexpr int kMaxRanks = 64;
 constexpr u32 kGroupMaxBits = 24;       // engine_group_keys: counter arrays of <= 16 M entries
 constexpr u32 kGroupMaxPerValue = 512;  // ... and at most this many keys per value on average
+// engine_build_runs: builds of at most this many rows size their run arrays
+// and hash table by the rows (no host read of the run count).
+constexpr u64 kRunsBoundRows = u64(1) << 20;
 
 __device__ __forceinline__ u32 route_dest(const RouteKey& k, u64 i, u32 world) {
     u32 v;
@@ -2057,13 +2066,18 @@ void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u6
     c->count_launch();
 }
 
-u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits) {
+u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits, bool exact) {
     if (!n) return 0;
     u64* d = c->d_scalars + 45;
+    // Not exact: the n rows past the words keep x = 0xffffffff (outside
+    // every value domain below 2^32: no index holds them, no probe meets
+    // them) and the bound n is returned without a host round trip.
+    if (!exact) FV_CUDA(cudaMemsetAsync(x, 0xff, 4 * n, c->stream));
     {
         ProfScope prof(c, "tuples_to_words", 8.0 * double(n));
         tile_scan(c, TuplesToWordsOp{c0, c1, n, x, zb, bits}, n, d);
     }
+    if (!exact) return n;
     u64 total = 0;
     c->read_scalars(d, &total, 1);
     return total;
@@ -2083,6 +2097,18 @@ u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u6
 
 u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity) {
     if (!n) return 0;
+    u64* d = c->d_scalars + 42;
+    engine_count_blocks_async(c, keys, n, shift, arity, d);
+    u64 m = 0;
+    c->read_scalars(d, &m, 1);
+    return m;
+}
+
+void engine_count_blocks_async(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity, u64* d_out) {
+    if (!n) {
+        FV_CUDA(cudaMemsetAsync(d_out, 0, 8, c->stream));
+        return;
+    }
     DBuf<u64> ids(c, n), alt(c, n);
     {
         ProfScope prof(c, "count_blocks", 16.0 * double(n));
@@ -2091,11 +2117,7 @@ u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity) {
         c->count_launch();
     }
     if (radix_sort_keys_u64(c, ids.get(), alt.get(), n, 0, 54)) ids.swap(alt);
-    u64* d = c->d_scalars + 42;
-    tile_scan(c, DistinctOp{ids.get()}, n, d);
-    u64 m = 0;
-    c->read_scalars(d, &m, 1);
-    return m;
+    tile_scan(c, DistinctOp{ids.get()}, n, d_out);
 }
 
 namespace {
@@ -2235,7 +2257,7 @@ bool engine_hash_grow(Ctx* c, const KeySet& from, KeySet& to) {
     return true;
 }
 
-static void build_run_hash(Ctx* c, JoinIndex& idx);
+static void build_run_hash(Ctx* c, JoinIndex& idx, const u64* d_nu = nullptr);
 
 bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* runs, u32* col0, u32* col1,
                        const u32* pay_in, u32* pay_out, const u32* gather_idx, u32* gather_src) {
@@ -2510,8 +2532,9 @@ void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u3
         idx.ht = HashIndex();
         FV_CUDA(cudaMemsetAsync(idx.ucount.get(), 0, 4 * domain, c->stream));
         ProfScope prof(c, "direct_index", 8.0 * double(n));
-        direct_start_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get());
-        direct_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), idx.ucount.get());
+        direct_start_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), domain);
+        direct_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), idx.ucount.get(),
+                                                                 domain);
         FV_CUDA(cudaGetLastError());
         c->count_launch(2);
         return;
@@ -2519,6 +2542,21 @@ void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u3
     DBuf<u32> uk(c, n), us(c, n);
     u64* d = c->d_scalars + 16;
     tile_scan(c, RunsOp{sorted_keys, uk.get(), us.get()}, n, d);
+    if (n <= kRunsBoundRows) {
+        // Small builds: sized by the row count (the run count stays on the
+        // device, read by the kernels) instead of a host round trip.
+        DBuf<u64> d_nu(c, 1);
+        FV_CUDA(cudaMemcpyAsync(d_nu.get(), d, 8, cudaMemcpyDeviceToDevice, c->stream));
+        idx.n_unique = n;  // a bound; non-zero marks a non-empty index
+        idx.ukeys = std::move(uk);
+        idx.ustart = std::move(us);
+        idx.ucount = DBuf<u32>(c, n);
+        runs_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(idx.ustart.get(), idx.ucount.get(), n, n, d_nu.get());
+        FV_CUDA(cudaGetLastError());
+        c->count_launch();
+        build_run_hash(c, idx, d_nu.get());
+        return;
+    }
     c->read_scalars(d, &idx.n_unique, 1);
     const u64 nu = idx.n_unique;
     idx.ukeys = DBuf<u32>(c, nu);
@@ -2526,14 +2564,15 @@ void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u3
     idx.ucount = DBuf<u32>(c, nu);
     FV_CUDA(cudaMemcpyAsync(idx.ukeys.get(), uk.get(), 4 * nu, cudaMemcpyDeviceToDevice, c->stream));
     FV_CUDA(cudaMemcpyAsync(idx.ustart.get(), us.get(), 4 * nu, cudaMemcpyDeviceToDevice, c->stream));
-    runs_count_kernel<<<grid_for(nu), 256, 0, c->stream>>>(idx.ustart.get(), idx.ucount.get(), nu, n);
+    runs_count_kernel<<<grid_for(nu), 256, 0, c->stream>>>(idx.ustart.get(), idx.ucount.get(), nu, n, nullptr);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
     build_run_hash(c, idx);
 }
 
-// Hash table over the unique keys of idx (key -> run number).
-static void build_run_hash(Ctx* c, JoinIndex& idx) {
+// Hash table over the unique keys of idx (key -> run number); d_nu: their
+// count on the device, idx.n_unique then a bound.
+static void build_run_hash(Ctx* c, JoinIndex& idx, const u64* d_nu) {
     const u64 nu = idx.n_unique;
     u64 cap = 64;
     while (cap < 2 * nu) cap <<= 1;
@@ -2542,7 +2581,7 @@ static void build_run_hash(Ctx* c, JoinIndex& idx) {
     FV_CUDA(cudaMemsetAsync(idx.ht.slots.get(), 0xff, 8 * cap, c->stream));
     if (!nu) return;
     hash_build_kernel<<<grid_for(nu), 256, 0, c->stream>>>(
-        idx.ukeys.get(), nu, reinterpret_cast<unsigned long long*>(idx.ht.slots.get()), idx.ht.mask);
+        idx.ukeys.get(), nu, reinterpret_cast<unsigned long long*>(idx.ht.slots.get()), idx.ht.mask, d_nu);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }
