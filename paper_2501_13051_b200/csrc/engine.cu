@@ -675,22 +675,40 @@ public:
         // its column 1 is only the head's column 1, so the mask rides along
         // as ColRef {0, 2} and the last step emits one word per row.
         bool carry = false;
+        // Step 0's probe counts and output offsets computed ahead, together
+        // with other variants' (one host round trip for all their sizes).
+        struct Pre {
+            bool valid = false;
+            DBuf<u32> starts;
+            DBuf<u64> offsets;
+            u64 T = 0;
+        } pre;
+        Inter cur;  // step 0's input (prepared variants)
     };
 
     // `old_src[s]`: source s reads FULL - DELTA instead of FULL (exactly-once
     // variants; empty = every non-DELTA source reads FULL, the reference).
     void exec_variant(const Plan& plan, const DistPlan& dp, long delta_source, const std::vector<u8>& old_src,
                       CandPool& out, HeadSink* sink) {
+        std::unique_ptr<VarRun> v = prepare_variant(plan, dp, delta_source, old_src, out, sink);
+        if (v) run_variant(*v);
+    }
+
+    // A variant's versions and step-0 input; null when a source is empty.
+    std::unique_ptr<VarRun> prepare_variant(const Plan& plan, const DistPlan& dp, long delta_source,
+                                            const std::vector<u8>& old_src, CandPool& out, HeadSink* sink) {
         const u32 ns = static_cast<u32>(plan.sources.size());
-        VarRun v{plan, dp, delta_source, std::vector<const DevVersion*>(ns), std::vector<Which>(ns, kFull),
-                 {}, (plan.head_arity + 1) / 2, plan.sources[0].constrained(), dist(), out, sink};
+        auto vp = std::unique_ptr<VarRun>(new VarRun{plan, dp, delta_source, std::vector<const DevVersion*>(ns),
+                                                     std::vector<Which>(ns, kFull), {}, (plan.head_arity + 1) / 2,
+                                                     plan.sources[0].constrained(), dist(), out, sink});
+        VarRun& v = *vp;
         for (u32 s = 0; s < ns; ++s) {
             RelState& r = rel(plan.sources[s].relation);
             const u32 kc = partitioned(r) ? dp.src_copy[s] : 0;
             if (static_cast<long>(s) == delta_source) v.which[s] = kDelta;
             else if (!old_src.empty() && old_src[s]) v.which[s] = kOld;
             v.ver[s] = &version(r, kc, v.which[s]);
-            if (!v.D && v.ver[s]->n == 0) return;  // engine.cpp:76-78
+            if (!v.D && v.ver[s]->n == 0) return nullptr;  // engine.cpp:76-78
         }
         // (partitioned runs: only a DELTA that is already words — the word
         // builds are single-GPU)
@@ -700,9 +718,9 @@ public:
             // the probe side as words (cached word build of that version)
             WordBuild& wb = word_build(rel(plan.sources[0].relation), v.which[0]);
             v.ver[0] = &wb.words;
-            if (v.ver[0]->n == 0) return;
+            if (v.ver[0]->n == 0) return nullptr;
         }
-        Inter cur;
+        Inter& cur = v.cur;
         cur.n = v.ver[0]->n;
         for (u32 j = 0; j < plan.sources[0].arity; ++j) cur.cols[ColRef{0, j}] = v.ver[0]->cols[j].get();
         if (v.carry) cur.cols[ColRef{0, 2}] = v.ver[0]->cols[2].get();
@@ -717,7 +735,15 @@ public:
             for (auto& r : plan.output_cols) s.insert(r);
             if (v.carry) s.insert(ColRef{0, 2});
         }
-        if (nj) {
+        return vp;
+    }
+
+    void run_variant(VarRun& v) {
+        const Plan& plan = v.plan;
+        const DistPlan& dp = v.dp;
+        CandPool& out = v.out;
+        Inter cur = std::move(v.cur);
+        if (!plan.joins.empty()) {
             join_step(v, 0, std::move(cur));
             return;
         }
@@ -751,6 +777,92 @@ public:
         out.n += produced;
     }
 
+    // The build-side index of join step k (tmp owns a constrained source's
+    // one-off index); *inter_word: the step's intermediate goes through a
+    // word sink (inter_refs its columns).
+    JoinIndex* step_index(VarRun& v, size_t k, std::unique_ptr<JoinIndex>& tmp, ColRef (&inter_refs)[2],
+                          bool* inter_word) {
+        const Plan& plan = v.plan;
+        const PlanJoin& jn = plan.joins[k];
+        const u32 R = jn.right_source;
+        const size_t nj = plan.joins.size();
+        RelState& rr = rel(plan.sources[R].relation);
+        const bool word_step = k + 1 == nj && !v.D && word_step_ok(plan, k);
+        // A deduplicated binary intermediate (x, z) of a composition step is
+        // produced through a temporary word sink instead of rows + sort-unique.
+        *inter_word = !v.D && words_ && k + 1 < nj && inter_word_ok(v, k, inter_refs);
+        if (plan.sources[R].constrained()) {
+            tmp = std::make_unique<JoinIndex>();
+            build_index_on(*v.ver[R], jn.right_col, *tmp, &plan.sources[R]);
+            return tmp.get();
+        }
+        if ((word_step && rel(plan.head).word_sink && v.ver[R]->cols.size() == 2) || *inter_word) {
+            // Composition into a word sink: probe the word form of the build
+            // version (x, z base, mask), one output per word.
+            return &word_build(rr, v.which[R]).idx;
+        }
+        return &index(rr, partitioned(rr) ? v.dp.src_copy[R] : 0, v.which[R], jn.right_col);
+    }
+
+    // Probe counts of step k -> per-row output offsets (offsets[n] = T).
+    void count_step(VarRun& v, size_t k, const Inter& cur, JoinIndex& idx, u32* starts, u64* offsets) {
+        const u64 n = cur.n;
+        DBuf<u32> counts(c_, n);
+        RowFilter pred;
+        if (k == 0 && v.src0_pending) pred = source_filter(v.plan.sources[0], *v.ver[0]);
+        engine_probe_count(c_, cur.cols.at(v.plan.joins[k].left), n, idx, pred, starts, counts.get());
+        exclusive_scan_counts(c_, counts.get(), offsets, n);
+    }
+
+    // Step 0 of several prepared variants counted with one host round trip
+    // for all their output sizes. Left to join_step (which reads its size
+    // with the head's set counters): partitioned runs, constrained build
+    // sides, and a last step into a head an earlier variant of the batch
+    // already feeds (its set counters are read on that step's sync).
+    void precount_variants(std::vector<std::unique_ptr<VarRun>>& vs) {
+        if (dist()) return;
+        std::vector<VarRun*> todo;
+        std::set<std::string> heads;
+        for (auto& vp : vs) {
+            if (!vp) continue;
+            VarRun& v = *vp;
+            const Plan& plan = v.plan;
+            if (plan.joins.empty()) continue;
+            const bool last = plan.joins.size() == 1;
+            const bool taken = last && v.sink && (heads.count(plan.head) || v.sink->counter.get());
+            if (v.sink) heads.insert(plan.head);
+            if (taken || plan.sources[plan.joins[0].right_source].constrained()) continue;
+            todo.push_back(&v);
+        }
+        if (todo.size() < 2) return;
+        if (batch_pinned_cap_ < todo.size()) {
+            if (batch_pinned_) cudaFreeHost(batch_pinned_);
+            batch_pinned_cap_ = std::max<size_t>(256, 2 * todo.size());
+            FV_CUDA(cudaMallocHost(&batch_pinned_, sizeof(u64) * batch_pinned_cap_));
+        }
+        for (size_t q = 0; q < todo.size(); ++q) {
+            VarRun& v = *todo[q];
+            std::unique_ptr<JoinIndex> tmp;
+            ColRef refs[2];
+            bool iw = false;
+            JoinIndex* idx = step_index(v, 0, tmp, refs, &iw);
+            const u64 n = v.cur.n;
+            v.pre.starts = DBuf<u32>(c_, n);
+            v.pre.offsets = DBuf<u64>(c_, n + 1);
+            if (idx->rows->n == 0) {
+                FV_CUDA(cudaMemsetAsync(v.pre.offsets.get() + n, 0, 8, c_->stream));
+            } else {
+                count_step(v, 0, v.cur, *idx, v.pre.starts.get(), v.pre.offsets.get());
+            }
+            FV_CUDA(cudaMemcpyAsync(batch_pinned_ + q, v.pre.offsets.get() + n, 8, cudaMemcpyDeviceToHost, c_->stream));
+        }
+        c_->sync();
+        for (size_t q = 0; q < todo.size(); ++q) {
+            todo[q]->pre.T = batch_pinned_[q];
+            todo[q]->pre.valid = true;
+        }
+    }
+
     // Join step k of a variant on intermediate `cur`; recurses into step k+1.
     // An intermediate larger than inter_chunk_ rows is produced and carried
     // through the rest of the chain chunk by chunk (single GPU: every rank of
@@ -767,59 +879,53 @@ public:
         const size_t nj = plan.joins.size();
         const PlanJoin& jn = plan.joins[k];
         const u32 R = jn.right_source;
-        RelState& rr = rel(plan.sources[R].relation);
-        const bool rpart = partitioned(rr);
         if (D && dp.shuffle[k]) cur = shuffle(cur, jn.left);
         std::unique_ptr<JoinIndex> tmp;
-        JoinIndex* idx;
-        const bool word_step = k + 1 == nj && !D && word_step_ok(plan, k);
-        // A deduplicated binary intermediate (x, z) of a composition step is
-        // produced through a temporary word sink instead of rows + sort-unique.
         ColRef inter_refs[2];
-        const bool inter_word = !D && words_ && k + 1 < nj && inter_word_ok(v, k, inter_refs);
-        if (plan.sources[R].constrained()) {
-            tmp = std::make_unique<JoinIndex>();
-            build_index_on(*v.ver[R], jn.right_col, *tmp, &plan.sources[R]);
-            idx = tmp.get();
-        } else if ((word_step && rel(plan.head).word_sink && v.ver[R]->cols.size() == 2) || inter_word) {
-            // Composition into a word sink: probe the word form of the build
-            // version (x, z base, mask), one output per word.
-            idx = &word_build(rr, v.which[R]).idx;
-        } else {
-            idx = &index(rr, rpart ? dp.src_copy[R] : 0, v.which[R], jn.right_col);
-        }
-        if (!D && idx->rows->n == 0) return;
+        bool inter_word = false;
+        JoinIndex* idx = step_index(v, k, tmp, inter_refs, &inter_word);
+        const bool pre_ok = k == 0 && v.pre.valid;
+        if (!D && !pre_ok && idx->rows->n == 0) return;
         // The build side is in word form (x, z base, mask): a binary atom whose
         // version has three columns (a ternary atom's version also has three).
         const bool word_build_side = plan.sources[R].arity == 2 && idx->rows->cols.size() == 3;
         // Carried words: the last step's head column 1 is source 0's word.
         const bool word_probe_side = v.carry && k + 1 == nj;
         const u64 n = cur.n;
-        DBuf<u32> starts(c_, n), counts(c_, n);
-        RowFilter pred;
-        if (k == 0 && v.src0_pending) pred = source_filter(plan.sources[0], *v.ver[0]);
-        engine_probe_count(c_, cur.cols.at(jn.left), n, *idx, pred, starts.get(), counts.get());
-        DBuf<u64> offsets(c_, n + 1);
-        exclusive_scan_counts(c_, counts.get(), offsets.get(), n);
-        FV_CUDA(cudaMemcpyAsync(c_->pinned, offsets.get() + n, 8, cudaMemcpyDeviceToHost, c_->stream));
-        // The fused dedup's set counters ride on the same sync (its first
-        // chunk then needs no read of its own).
-        HeadSink* pre = nullptr;
-        if (k + 1 == nj && sink && sink->counter.get()) {
-            RelState& hr = rel(plan.head);
-            if (hr.block_mode && hr.blocks.capacity()) {
-                pre = sink;
-                FV_CUDA(cudaMemcpyAsync(c_->pinned + 8, sink->counter.get(), 24, cudaMemcpyDeviceToHost, c_->stream));
-                FV_CUDA(cudaMemcpyAsync(c_->pinned + 11, hr.blocks.count.get(), 8, cudaMemcpyDeviceToHost, c_->stream));
+        DBuf<u32> starts;
+        DBuf<u64> offsets;
+        u64 T = 0;
+        if (pre_ok) {
+            // counted ahead (precount_variants)
+            starts = std::move(v.pre.starts);
+            offsets = std::move(v.pre.offsets);
+            T = v.pre.T;
+            v.pre.valid = false;
+        } else {
+            starts = DBuf<u32>(c_, n);
+            offsets = DBuf<u64>(c_, n + 1);
+            count_step(v, k, cur, *idx, starts.get(), offsets.get());
+            FV_CUDA(cudaMemcpyAsync(c_->pinned, offsets.get() + n, 8, cudaMemcpyDeviceToHost, c_->stream));
+            // The fused dedup's set counters ride on the same sync (its first
+            // chunk then needs no read of its own).
+            HeadSink* pre = nullptr;
+            if (k + 1 == nj && sink && sink->counter.get()) {
+                RelState& hr = rel(plan.head);
+                if (hr.block_mode && hr.blocks.capacity()) {
+                    pre = sink;
+                    FV_CUDA(cudaMemcpyAsync(c_->pinned + 8, sink->counter.get(), 24, cudaMemcpyDeviceToHost,
+                                            c_->stream));
+                    FV_CUDA(cudaMemcpyAsync(c_->pinned + 11, hr.blocks.count.get(), 8, cudaMemcpyDeviceToHost,
+                                            c_->stream));
+                }
+            }
+            c_->sync();
+            T = c_->pinned[0];
+            if (pre && T) {  // consumed by the first chunk's hash_reserve below
+                pre->pre = true;
+                for (int q = 0; q < 4; ++q) pre->pre_vals[q] = c_->pinned[8 + q];
             }
         }
-        c_->sync();
-        const u64 T = c_->pinned[0];
-        if (pre && T) {  // consumed by the first chunk's hash_reserve below
-            pre->pre = true;
-            for (int q = 0; q < 4; ++q) pre->pre_vals[q] = c_->pinned[8 + q];
-        }
-        counts.reset();
         if (trace_)
             std::fprintf(stderr, "[fvlog]   %s join %zu/%zu delta@%ld probe=%llu outputs=%llu\n", plan.head.c_str(), k, nj,
                          delta_source, static_cast<unsigned long long>(n), static_cast<unsigned long long>(T));
@@ -2446,6 +2552,9 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     const char* rev_env = std::getenv("FVLOG_REVERSE");
     const bool reverse_env = !(rev_env && std::string(rev_env) == "0");
     const bool reverse_always = rev_env && std::string(rev_env) == "1";
+    // FVLOG_PRECOUNT=0: every join step reads its own output size.
+    const char* pc_env = std::getenv("FVLOG_PRECOUNT");
+    const bool precount_env = !(pc_env && std::string(pc_env) == "0");
     u64 syncs_seen = c->syncs;
     auto tr = [&](const char* what, Clock::time_point t, u64 it) {
         if (trace) {
@@ -2489,22 +2598,32 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
                 if (v.delta_source >= 0 || iteration == 0) active.emplace_back(v.plan, v.delta_source);
             eng.prepare_full_words(active);
         }
-        for (auto& v : variants) {
-            if (v.delta_source < 0 && iteration != 0) continue;
-            RelState& hr = *st->relations.at(v.plan->head);
-            HeadSink* sink = hr.hash_mode ? &sinks[v.plan->head] : nullptr;
-            if (v.alt && hr.word_sink && reverse_env) {
-                // DELTA's rows (words when it is word form) against the other
-                // atom's rows: probe the smaller side.
-                const RelState& dr = *st->relations.at(v.plan->sources[1].relation);
-                const RelState& pr = *st->relations.at(v.plan->sources[0].relation);
-                const u64 other = v.old_src.empty() || !v.old_src[0] || pr.old_is_full ? pr.rows() : pr.full_old.n;
-                if (reverse_always || (eng.dist() && dr.word_mode) || (!eng.dist() && 2 * dr.delta.n < other)) {
-                    eng.exec_variant(*v.alt, dplans[v.alt_index], 0, v.alt_old, pooled[v.plan->head], sink);
-                    continue;
+        {
+            // Every variant is prepared first so that their step-0 output
+            // sizes come back in one host round trip (precount_variants).
+            std::vector<std::unique_ptr<Engine::VarRun>> runs;
+            for (auto& v : variants) {
+                if (v.delta_source < 0 && iteration != 0) continue;
+                RelState& hr = *st->relations.at(v.plan->head);
+                HeadSink* sink = hr.hash_mode ? &sinks[v.plan->head] : nullptr;
+                if (v.alt && hr.word_sink && reverse_env) {
+                    // DELTA's rows (words when it is word form) against the other
+                    // atom's rows: probe the smaller side.
+                    const RelState& dr = *st->relations.at(v.plan->sources[1].relation);
+                    const RelState& pr = *st->relations.at(v.plan->sources[0].relation);
+                    const u64 other = v.old_src.empty() || !v.old_src[0] || pr.old_is_full ? pr.rows() : pr.full_old.n;
+                    if (reverse_always || (eng.dist() && dr.word_mode) || (!eng.dist() && 2 * dr.delta.n < other)) {
+                        runs.push_back(
+                            eng.prepare_variant(*v.alt, dplans[v.alt_index], 0, v.alt_old, pooled[v.plan->head], sink));
+                        continue;
+                    }
                 }
+                runs.push_back(eng.prepare_variant(*v.plan, dplans[v.plan_index], v.delta_source, v.old_src,
+                                                   pooled[v.plan->head], sink));
             }
-            eng.exec_variant(*v.plan, dplans[v.plan_index], v.delta_source, v.old_src, pooled[v.plan->head], sink);
+            if (precount_env) eng.precount_variants(runs);
+            for (auto& r : runs)
+                if (r) eng.run_variant(*r);
         }
         tr("variants", ti, iteration);
         const auto tf = Clock::now();
