@@ -1206,7 +1206,9 @@ public:
         CandPool none;
         none.arity = 2;
         const u64 nd = T ? hash_finalize(tmp, sk, none) : 0;
-        if (T) block_ratio = tmp.blocks.ratio;
+        // (from the final block count: an overflowed first insert counts
+        // only the blocks that fit before its drain)
+        if (T) block_ratio = std::max(tmp.blocks.ratio, double(tmp.blocks.blocks) / double(T));
         if (trace_)
             std::fprintf(stderr, "[fvlog]   word intermediate: %llu word outputs -> %llu rows\n",
                          static_cast<unsigned long long>(T), static_cast<unsigned long long>(nd));
