@@ -1315,29 +1315,68 @@ public:
 
     PendingMerge merge_launch(DevVersion& full, DevVersion& delta, IndexMap& indexes, u32 arity, CandPool& cand,
                               RelState* home) {
+        if (cand.n) engine_sort_keys(c_, cand.words, cand.n, arity, st_.key_shift);
+        std::vector<u64*> bw;
+        for (auto& w : cand.words) bw.push_back(w.get());
+        return merge_launch_sorted(full, delta, indexes, arity, bw, cand.n, home);
+    }
+
+    // merge_launch of n candidate keys already sorted (bw: their words).
+    PendingMerge merge_launch_sorted(DevVersion& full, DevVersion& delta, IndexMap& indexes, u32 arity,
+                                     std::vector<u64*>& bw, u64 n, RelState* home) {
         PendingMerge pm;
         pm.full = &full;
         pm.delta = &delta;
         pm.indexes = &indexes;
         pm.home = home;
         pm.arity = arity;
-        pm.cand_n = cand.n;
-        if (cand.n == 0) return pm;
-        engine_sort_keys(c_, cand.words, cand.n, arity, st_.key_shift);
+        pm.cand_n = n;
+        if (n == 0) return pm;
         for (u32 j = 0; j < arity; ++j) {
-            pm.C.cols.emplace_back(c_, full.n + cand.n);
-            pm.Dv.cols.emplace_back(c_, cand.n);
+            pm.C.cols.emplace_back(c_, full.n + n);
+            pm.Dv.cols.emplace_back(c_, n);
         }
-        std::vector<u64*> bw;
-        for (auto& w : cand.words) bw.push_back(w.get());
         std::vector<u32*> cc, dc;
         for (u32 j = 0; j < arity; ++j) {
             cc.push_back(pm.C.cols[j].get());
             dc.push_back(pm.Dv.cols[j].get());
         }
         pm.d_new = DBuf<u64>(c_, 1);
-        engine_merge(c_, full.ptrs(), full.n, bw.data(), cand.n, arity, st_.key_shift, cc, dc, pm.d_new.get());
+        engine_merge(c_, full.ptrs(), full.n, bw.data(), n, arity, st_.key_shift, cc, dc, pm.d_new.get());
         return pm;
+    }
+
+    // Seeds of several sort-merged (EDB) relations share one radix sort:
+    // their packed keys are tagged with the relation's number above the
+    // key bits, sorted together, untagged, and each relation's slice is
+    // merged (deduplicated) on its own. False (nothing done) when fewer
+    // than two relations qualify or the tags do not fit in 64 bits.
+    bool seed_batch(const std::vector<std::pair<RelState*, const DevVersion*>>& rels, std::vector<PendingMerge>& pend) {
+        if (rels.size() < 2) return false;
+        const u32 base = 2 * st_.key_shift;
+        u32 tag_bits = 1;
+        while ((u64(1) << tag_bits) < rels.size()) ++tag_bits;
+        if (base + tag_bits > 64) return false;
+        u64 total = 0;
+        for (auto& [r, v] : rels) total += v->n;
+        DBuf<u64> all(c_, std::max<u64>(total, 1)), alt(c_, std::max<u64>(total, 1));
+        u64 off = 0;
+        for (size_t i = 0; i < rels.size(); ++i) {
+            const DevVersion& v = *rels[i].second;
+            u64* wp = all.get() + off;
+            engine_pack_keys(c_, v.ptrs(), v.n, st_.key_shift, &wp);
+            engine_mask_u64(c_, wp, v.n, ~u64(0), u64(i) << base);
+            off += v.n;
+        }
+        if (total > 1 && radix_sort_keys_u64(c_, all.get(), alt.get(), total, 0, base + tag_bits)) all.swap(alt);
+        engine_mask_u64(c_, all.get(), total, base >= 64 ? ~u64(0) : (u64(1) << base) - 1, 0);
+        off = 0;
+        for (auto& [r, v] : rels) {
+            std::vector<u64*> bw{all.get() + off};
+            pend.push_back(merge_launch_sorted(r->full, r->delta, r->indexes, r->arity, bw, v->n, r));
+            off += v->n;
+        }
+        return true;
     }
 
     u64 merge_complete(PendingMerge& pm, u64 nd) {
@@ -2554,6 +2593,9 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     const char* rev_env = std::getenv("FVLOG_REVERSE");
     const bool reverse_env = !(rev_env && std::string(rev_env) == "0");
     const bool reverse_always = rev_env && std::string(rev_env) == "1";
+    // FVLOG_SEED_BATCH=0: every sort-merged relation's seed sorts on its own.
+    const char* sb_env = std::getenv("FVLOG_SEED_BATCH");
+    const bool seed_batch_env = !(sb_env && std::string(sb_env) == "0");
     // FVLOG_PRECOUNT=0: every join step reads its own output size.
     const char* pc_env = std::getenv("FVLOG_PRECOUNT");
     const bool precount_env = !(pc_env && std::string(pc_env) == "0");
@@ -2573,8 +2615,19 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
     const auto ts = Clock::now();
     {
         std::vector<Engine::PendingMerge> pend;
+        // sort-merged single-GPU relations of arity <= 2: one shared sort
+        std::vector<std::pair<RelState*, const DevVersion*>> batch;
         for (auto& [name, vp] : raw) {
             RelState& r = *st->relations[name];
+            if (seed_batch_env && !eng.partitioned(r) && !r.hash_mode && r.arity <= 2 && vp->n)
+                batch.emplace_back(&r, vp);
+        }
+        const bool batched = eng.seed_batch(batch, pend);
+        for (auto& [name, vp] : raw) {
+            RelState& r = *st->relations[name];
+            if (batched && std::find_if(batch.begin(), batch.end(), [&](const auto& b) { return b.first == &r; }) !=
+                               batch.end())
+                continue;
             if (eng.partitioned(r)) {
                 for (u32 kc : r.keyset) eng.seed_copy(r, *vp, kc, pend);
             } else {

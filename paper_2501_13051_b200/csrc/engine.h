@@ -504,6 +504,8 @@ void engine_project(Ctx* c, u64 n, const OutSpec& spec);
 void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u32 key_bits = 0);
 // Pack SoA columns into W key words.
 void engine_pack_keys(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 shift, u64* const* words);
+// p[i] = (p[i] & and_mask) | or_bits (tagging / untagging packed keys).
+void engine_mask_u64(Ctx* c, u64* p, u64 n, u64 and_mask, u64 or_bits);
 // Merge sorted distinct A (SoA, arity) with sorted B keys (W words, dups
 // allowed): C = A u B (SoA), D = B \ A distinct (SoA). Returns |D| (device
 // scalar written to *d_new; |C| = n_a + |D|).

@@ -1482,6 +1482,11 @@ struct ExpandWordsOp {
 
 __global__ void set_u64_kernel(u64* p, u64 v) { *p = v; }
 
+// p[i] = (p[i] & and_mask) | or_bits
+__global__ void mask_u64_kernel(u64* __restrict__ p, u64 n, u64 and_mask, u64 or_bits) {
+    GRID_STRIDE(i, n) p[i] = (p[i] & and_mask) | or_bits;
+}
+
 // Block ids of packed keys (the distinct count sizes a directory).
 __global__ void block_ids_kernel(const u64* __restrict__ keys, u64 n, u32 shift, u32 arity, u64* __restrict__ out) {
     GRID_STRIDE(i, n) {
@@ -2750,6 +2755,13 @@ void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u
         c->count_launch();
         words[w].swap(tmp);
     }
+}
+
+void engine_mask_u64(Ctx* c, u64* p, u64 n, u64 and_mask, u64 or_bits) {
+    if (!n) return;
+    mask_u64_kernel<<<grid_for(n), 256, 0, c->stream>>>(p, n, and_mask, or_bits);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
 }
 
 }  // namespace fv
