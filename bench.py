@@ -488,14 +488,25 @@ def run_workload(R: Runner, name: str, spec: dict, golden: dict, steps: int, war
     for _ in range(warmup):
         st = R.step_resident(w)
         del st
+    syncs0 = R.ctx.host_syncs()
     ms, st = R.timed(steps, lambda: R.step_resident(w))
+    syncs = (R.ctx.host_syncs() - syncs0) / steps
     derived = st.derived_tuples()
+    iterations = st.iterations
     parity = check_parity(st, golden.get(spec["golden"], {}), spec["result"], R.world, R.dist)
-    out = {"workload": spec["desc"], "ms_per_step": ms / steps, "value": derived / (ms / steps / 1000.0),
-           "unit": UNIT, "derived_tuples_per_step": derived, "iterations": st.iterations,
-           "facts": int(sum(v.shape[0] for v in facts.values())), "steps": steps, "warmup": warmup,
-           "parity": parity}
     del st
+    # one profiled step: the device's kernel time against the step's time
+    kernels, st = R.profile(1, lambda: R.step_resident(w))
+    del st
+    kernel_ms = sum(k["ms"] for k in kernels)
+    out = {"workload": spec["desc"], "ms_per_step": ms / steps, "value": derived / (ms / steps / 1000.0),
+           "unit": UNIT, "derived_tuples_per_step": derived, "iterations": iterations,
+           "facts": int(sum(v.shape[0] for v in facts.values())), "steps": steps, "warmup": warmup,
+           "host_syncs_per_step": syncs, "host_syncs_per_iteration": round(syncs / max(iterations, 1), 2),
+           "kernel_ms_per_step": round(kernel_ms, 3),
+           "kernel_busy": round(kernel_ms / (ms / steps), 3),
+           "kernel_busy_what": "sum of per-launch CUDA-event kernel times (one profiled step) / ms_per_step",
+           "parity": parity}
     R.release(w)
     return out
 
@@ -638,6 +649,7 @@ def run_fvlog(args):
         "e2e": e2e,
         "e2e_with_dump": e2e_dump,
         "gpu_launches": int(launches),
+        "kernel_busy": round(sum(k["ms"] for k in kernels) / prof_steps / (t_max / args.steps), 3),
         "host_syncs": {"per_step": syncs / args.steps, "per_iteration": round(syncs / args.steps / iterations, 2),
                        "what": "stream syncs + scalar readbacks on the engine context (fv_ctx_host_syncs)"},
         "clocks": sampler.summary(),

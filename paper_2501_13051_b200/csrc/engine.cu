@@ -807,9 +807,13 @@ public:
     // Probe counts of step k -> per-row output offsets (offsets[n] = T).
     void count_step(VarRun& v, size_t k, const Inter& cur, JoinIndex& idx, u32* starts, u64* offsets) {
         const u64 n = cur.n;
-        DBuf<u32> counts(c_, n);
         RowFilter pred;
         if (k == 0 && v.src0_pending) pred = source_filter(v.plan.sources[0], *v.ver[0]);
+        if (fused_probe_scan_) {
+            engine_probe_offsets(c_, cur.cols.at(v.plan.joins[k].left), n, idx, pred, starts, offsets);
+            return;
+        }
+        DBuf<u32> counts(c_, n);
         engine_probe_count(c_, cur.cols.at(v.plan.joins[k].left), n, idx, pred, starts, counts.get());
         exclusive_scan_counts(c_, counts.get(), offsets, n);
     }
@@ -2223,6 +2227,12 @@ private:
     const u32 word_combine_ = [] {
         const char* e = std::getenv("FVLOG_WORD_COMBINE");
         return e ? static_cast<u32>(std::atoi(e) != 0) : 1u;
+    }();
+    // FVLOG_PROBE_SCAN=0: probe counts written by one kernel and scanned by
+    // another instead of one fused single-pass probe + scan.
+    const bool fused_probe_scan_ = [] {
+        const char* e = std::getenv("FVLOG_PROBE_SCAN");
+        return !(e && std::string(e) == "0");
     }();
     // FVLOG_SCATTER_GATHER=1: the grouping scatter reads a word-form DELTA's
     // masks from the DELTA bitmap itself instead of a separate collect pass

@@ -487,6 +487,10 @@ struct RowFilter {  // predicate on probe-side rows (source constraints)
 
 // counts[i] = run length of probe[i] in the index (0 on miss or when the
 // probe row fails `pred`); starts[i] = run start.
+// Probe counts scanned straight into offsets[n + 1] (offsets[n] = total),
+// one single-pass kernel; starts as for engine_probe_count.
+void engine_probe_offsets(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, const RowFilter& pred,
+                          u32* starts, u64* offsets);
 void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, const RowFilter& pred,
                         u32* starts, u32* counts);
 // Ascending ids of rows passing `pred` (side 0); returns the count.

@@ -2388,6 +2388,57 @@ u64 engine_select_rows(Ctx* c, u64 n, const RowFilter& pred, u32* ids) {
     return k;
 }
 
+// Probe + exclusive scan in one single-pass kernel: each row's run lookup is
+// the scan's item value (its run start stored on the way), so the counts are
+// never written and read back (12 bytes per probe row less, one launch less).
+struct ProbeScanOp {
+    const u32* probe;
+    const u64* slots;
+    u32 mask;
+    const u32* ustart;
+    const u32* ucount;
+    u64 domain;
+    RowFilter pred;
+    u32* starts;
+    u64* offsets;
+    u64 n;
+    __device__ u64 value(u64 i) const {
+        u32 s = 0, c = 0, r;
+        if (pass_filters(pred.f, pred.n, i, 0)) {
+            const u32 v = probe[i];
+            if (domain) {
+                if (v < domain) {
+                    s = ustart[v];
+                    c = ucount[v];
+                }
+            } else if (ht_lookup(slots, mask, v, &r)) {
+                s = ustart[r];
+                c = ucount[r];
+            }
+        }
+        starts[i] = s;
+        return c;
+    }
+    __device__ void emit(u64 i, u64 prefix, u64 v) const {
+        offsets[i] = prefix;
+        if (i == n - 1) offsets[n] = prefix + v;
+    }
+};
+
+void engine_probe_offsets(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, const RowFilter& pred,
+                          u32* starts, u64* offsets) {
+    if (!n || idx.n_unique == 0) {  // empty build side: every probe misses
+        FV_CUDA(cudaMemsetAsync(offsets, 0, 8 * (n + 1), c->stream));
+        if (n) FV_CUDA(cudaMemsetAsync(starts, 0, 4 * n, c->stream));
+        return;
+    }
+    ProfScope prof(c, "join_probe_count", double(n) * 20.0);
+    tile_scan(c,
+              ProbeScanOp{probe, idx.ht.slots.get(), idx.ht.mask, idx.ustart.get(), idx.ucount.get(), idx.domain,
+                          pred, starts, offsets, n},
+              n, nullptr);
+}
+
 void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, const RowFilter& pred,
                         u32* starts, u32* counts) {
     if (!n) return;
