@@ -794,8 +794,11 @@ constexpr int kMatGroup = 1;  // measured: 1 is best on C1-C4 (FVLOG_MAT_GROUP o
 #ifndef FV_MAT_MIN_BLOCKS_BS
 #define FV_MAT_MIN_BLOCKS_BS 2
 #endif
+// Word form: 3 CTAs per SM (40 registers, a 136-byte spill) beat 2 (60
+// registers): C2 24.7 -> 23.7 ms, C3 18.4 -> 17.1, C4 73.4 -> 70.4 (4 CTAs:
+// 32 registers, 332-byte spill, 24.7 ms).
 #ifndef FV_MAT_MIN_BLOCKS_W
-#define FV_MAT_MIN_BLOCKS_W 2
+#define FV_MAT_MIN_BLOCKS_W 3
 #endif
 template <bool COMPACT, bool REMOTE, bool BLOCKS, bool WORDS>
 __global__ void __launch_bounds__(kMatBlock, WORDS ? FV_MAT_MIN_BLOCKS_W : (BLOCKS ? FV_MAT_MIN_BLOCKS_BS : FV_MAT_MIN_BLOCKS)) materialize_kernel(const u64* __restrict__ offsets, u64 m,
