@@ -461,13 +461,42 @@ __device__ __forceinline__ u32 block_excl_u32(u32 v, u32* s_warp, u32* total) {
 }
 
 // First and last source row of every output tile (parallel binary searches).
+// upper_bound by one warp: a 32-ary search (each round one load per lane,
+// log32(len) rounds instead of log2(len) dependent loads). All lanes call
+// it with the same x and get the same result.
+__device__ __forceinline__ u64 upper_bound_warp(const u64* __restrict__ a, u64 len, u64 x) {
+    const u32 lane = lane_id();
+    u64 lo = 0, hi = len;  // answer in [lo, hi]
+    while (hi - lo > 32) {
+        const u64 step = (hi - lo + 31) / 32;
+        const u64 idx = lo + u64(lane) * step;
+        const bool valid = idx < hi;
+        // probes with a[idx] <= x form a prefix of the valid ones
+        const u32 c = __popc(__ballot_sync(0xffffffffu, valid && a[idx] <= x));
+        const u32 nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+        const u64 nlo = c ? lo + u64(c - 1) * step + 1 : lo;
+        const u64 nhi = c < nvalid ? lo + u64(c) * step : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    const u64 idx = lo + lane;
+    const u32 m = __ballot_sync(0xffffffffu, idx < hi && a[idx] > x);
+    return m ? lo + __ffs(m) - 1 : hi;
+}
+
+// One warp per output tile: the rows holding its first and last output.
 __global__ void tile_rows_kernel(const u64* __restrict__ offsets, u64 m, u64 o_begin, u64 total, u64 tiles,
                                  u64* __restrict__ jlo, u64* __restrict__ jhi) {
-    GRID_STRIDE(b, tiles) {
+    const u64 warps = u64(gridDim.x) * (blockDim.x / 32);
+    for (u64 b = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / 32; b < tiles; b += warps) {
         const u64 o0 = o_begin + b * kMatTile;
         const u64 o_end = min(o0 + kMatTile, total);
-        jlo[b] = upper_bound_u64(offsets, m + 1, o0) - 1;
-        jhi[b] = upper_bound_u64(offsets, m + 1, o_end - 1) - 1;
+        const u64 lo = upper_bound_warp(offsets, m + 1, o0) - 1;
+        const u64 hi = upper_bound_warp(offsets, m + 1, o_end - 1) - 1;
+        if (lane_id() == 0) {
+            jlo[b] = lo;
+            jhi[b] = hi;
+        }
     }
 }
 
@@ -2486,8 +2515,8 @@ void engine_materialize(Ctx* c, const u64* offsets, u64 m, u64 total, const u32*
     const double out_bytes = fused_set(spec) ? 2.0 * row_bytes : row_bytes;
     const double frac = double(outs) / double(total);  // a chunk reads its share of the probe rows
     DBuf<u64> rows(c, 2 * tiles);
-    tile_rows_kernel<<<grid_for(tiles), 256, 0, c->stream>>>(offsets, m, o_begin, o_end, tiles, rows.get(),
-                                                             rows.get() + tiles);
+    tile_rows_kernel<<<grid_for(tiles * 32), 256, 0, c->stream>>>(offsets, m, o_begin, o_end, tiles, rows.get(),
+                                                                  rows.get() + tiles);
     FV_CUDA(cudaGetLastError());
     // The fused join + key-set dedup is profiled as "join_dedup". Word
     // outputs are charged per tuple candidate they stand for (SURVEY.md
