@@ -595,8 +595,8 @@ public:
         if (from_bitmap && which == kFull && r.block_mode && r.blocks.capacity() && r.arity == 2 && !dist()) {
             for (int j = 0; j < 3; ++j) wb->words.cols.emplace_back(c_, std::max<u64>(n, 1));
             wb->words.n = engine_blockset_words(c_, r.blocks, wb->words.cols[0].get(), wb->words.cols[1].get(),
-                                                wb->words.cols[2].get(), std::max<u64>(n, 1));
-            wb->words.lex_sorted = true;
+                                                wb->words.cols[2].get(), std::max<u64>(n, 1), st_.key_shift);
+            wb->words.lex_sorted = false;  // grouped by x (z windows in block order)
             wb->idx.rows = &wb->words;
             engine_build_runs(c_, wb->words.cols[0].get(), wb->words.n, wb->idx, st_.key_shift);
             if (trace_)

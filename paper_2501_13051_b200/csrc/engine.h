@@ -464,7 +464,7 @@ u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, 
                             bool exact = true);
 // The non-empty words of a binary block set in row-major (x, z) order —
 // FULL's word form straight from its bitmaps; outputs hold cap_out entries.
-u64 engine_blockset_words(Ctx* c, const BlockSet& s, u32* x, u32* zb, u32* bits, u64 cap_out);
+u64 engine_blockset_words(Ctx* c, const BlockSet& s, u32* x, u32* zb, u32* bits, u64 cap_out, u32 key_shift);
 // FULL of a block-set relation as lexicographically sorted SoA rows (c0, and
 // c1 for binary relations; null c0: count only), decoded from the bitmaps in
 // order — no sort of the tuples. Returns the row count.

@@ -1482,14 +1482,16 @@ struct TuplesToWordsOp {
     __device__ u64 value(u64 i) const {
         return (i == 0 || c0[i] != c0[i - 1] || (c1[i] >> 5) != (c1[i - 1] >> 5)) ? 1 : 0;
     }
+    // Every row ORs its bit into its word (p + v - 1: the word starts
+    // before it, this one included); bits[] is zeroed first. (A serial walk
+    // from each word start was latency-bound: 188 us for 7 M rows.)
     __device__ void emit(u64 i, u64 p, u64 v) const {
-        if (!v) return;
-        const u32 a = c0[i], w = c1[i] >> 5;
-        u32 m = 0;
-        for (u64 j = i; j < n && c0[j] == a && (c1[j] >> 5) == w; ++j) m |= 1u << (c1[j] & 31);
-        x[p] = a;
-        zb[p] = w << 5;
-        bits[p] = m;
+        const u32 z = c1[i];
+        if (v) {
+            x[p] = c0[i];
+            zb[p] = z & ~31u;
+        }
+        atomicOr(bits + (p + v - 1), 1u << (z & 31));
     }
 };
 
@@ -2114,6 +2116,7 @@ u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, 
     // every value domain below 2^32: no index holds them, no probe meets
     // them) and the bound n is returned without a host round trip.
     if (!exact) FV_CUDA(cudaMemsetAsync(x, 0xff, 4 * n, c->stream));
+    FV_CUDA(cudaMemsetAsync(bits, 0, 4 * n, c->stream));
     {
         ProfScope prof(c, "tuples_to_words", 8.0 * double(n));
         tile_scan(c, TuplesToWordsOp{c0, c1, n, x, zb, bits}, n, d);
@@ -2169,7 +2172,10 @@ struct SortedBlocks {
     u64 m = 0, rows = 0;
 };
 
-SortedBlocks sorted_blocks(Ctx* c, const BlockSet& s, u32 arity) {
+// x_bits > 0: only group the blocks by their row group (block id bits
+// [27, 27 + x_bits): x >> 5) instead of a full (x, z) order — enough for
+// consumers that need each x's words together but not z-ordered.
+SortedBlocks sorted_blocks(Ctx* c, const BlockSet& s, u32 arity, u32 x_bits = 0) {
     SortedBlocks b;
     const u64 cap = s.capacity();
     u64* d = c->d_scalars + 41;
@@ -2184,7 +2190,8 @@ SortedBlocks sorted_blocks(Ctx* c, const BlockSet& s, u32 arity) {
     c->read_scalars(d, &b.m, 1);
     if (!b.m) return b;
     // binary ids are (a >> 5) << 27 | (b >> 5): bits [0, 27) and [27, 54)
-    if (radix_sort_pairs_u64(c, b.bids.get(), bids_alt.get(), b.slots.get(), slots_alt.get(), b.m, 0, 54)) {
+    const u32 lo_bit = x_bits ? 27 : 0, hi_bit = x_bits ? std::min(54u, 27 + x_bits) : 54;
+    if (radix_sort_pairs_u64(c, b.bids.get(), bids_alt.get(), b.slots.get(), slots_alt.get(), b.m, lo_bit, hi_bit)) {
         b.bids.swap(bids_alt);
         b.slots.swap(slots_alt);
     }
@@ -2197,9 +2204,11 @@ SortedBlocks sorted_blocks(Ctx* c, const BlockSet& s, u32 arity) {
 }
 }  // namespace
 
-u64 engine_blockset_words(Ctx* c, const BlockSet& s, u32* x, u32* zb, u32* bits, u64 cap_out) {
+u64 engine_blockset_words(Ctx* c, const BlockSet& s, u32* x, u32* zb, u32* bits, u64 cap_out, u32 key_shift) {
     if (!s.capacity()) return 0;
-    SortedBlocks b = sorted_blocks(c, s, 2);
+    // words grouped by x (a join index on x needs no z order): the blocks
+    // are sorted on their row group only (3 radix passes instead of 7)
+    SortedBlocks b = sorted_blocks(c, s, 2, key_shift > 5 ? key_shift - 5 : 1);
     if (!b.m) return 0;
     const u64 items = b.m * 32;
     DBuf<u32> cnt(c, items);

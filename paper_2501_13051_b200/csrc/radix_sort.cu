@@ -20,6 +20,8 @@
 // HBM roofline per pass: n * 2 * (sizeof(K) + sizeof(payload)) bytes.
 #include "radix_sort.h"
 
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 namespace fv {
@@ -438,6 +440,10 @@ bool radix_sort_impl(Ctx* c, K* keys, K* keys_alt, u32* vals, u32* vals_alt, u64
                      u32 begin_bit, u32 end_bit) {
     if (n <= 1 || end_bit <= begin_bit) return false;
     const u32 npass = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
+    static const bool trace_sorts = std::getenv("FVLOG_TRACE_SORTS") != nullptr;
+    if (trace_sorts)
+        std::fprintf(stderr, "[sort] n=%llu key=%zu val=%d bits=%u..%u\n", static_cast<unsigned long long>(n),
+                     sizeof(K), HAS_VAL ? 1 : 0, begin_bit, end_bit);
     // hist (u64 x npass x 256) | bins (same) | trivial flags (npass)
     DBuf<u64> scratch(c, u64(npass) * kRadix * 2 + 8);
     unsigned long long* hist = reinterpret_cast<unsigned long long*>(scratch.get());
