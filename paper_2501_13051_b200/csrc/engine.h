@@ -99,6 +99,10 @@ struct JoinIndex {
     // domain > 0: direct-address index (from a counting-sort grouping):
     // ustart/ucount have `domain` entries indexed by value, no ukeys/ht.
     u64 domain = 0;
+    // direct index built from sorted keys: ucount holds each run's END
+    // (exclusive; 0 = no run, ustart then unset) — one pass, one cleared
+    // array (the counting-sort grouping's index keeps counts).
+    bool ends = false;
 };
 
 using IndexMap = std::map<std::pair<int, u32>, std::unique_ptr<JoinIndex>>;

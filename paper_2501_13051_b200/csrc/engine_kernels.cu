@@ -65,18 +65,32 @@ __device__ __forceinline__ bool ht_lookup(const u64* __restrict__ slots, u32 mas
     }
 }
 
+// Run (start, count) of value v in a direct-address index (ends: ucount
+// holds the run's end, 0 when there is none).
+__device__ __forceinline__ void direct_run(const u32* __restrict__ ustart, const u32* __restrict__ ucount, bool ends,
+                                           u32 v, u32* s, u32* c) {
+    const u32 e = ucount[v];
+    if (ends) {
+        if (e) {
+            *s = ustart[v];
+            *c = e - *s;
+        }
+    } else {
+        *s = ustart[v];
+        *c = e;
+    }
+}
+
 __global__ void probe_count_kernel(const u32* __restrict__ probe, u64 n, const u64* __restrict__ slots,
                                    u32 mask, const u32* __restrict__ ustart, const u32* __restrict__ ucount,
-                                   u64 domain, RowFilter pred, u32* __restrict__ starts, u32* __restrict__ counts) {
+                                   u64 domain, bool ends, RowFilter pred, u32* __restrict__ starts,
+                                   u32* __restrict__ counts) {
     GRID_STRIDE(i, n) {
         u32 s = 0, c = 0, r;
         if (pass_filters(pred.f, pred.n, i, 0)) {
             const u32 v = probe[i];
             if (domain) {  // direct-address index: run of value v at ustart[v], ucount[v]
-                if (v < domain) {
-                    s = ustart[v];
-                    c = ucount[v];
-                }
+                if (v < domain) direct_run(ustart, ucount, ends, v, &s, &c);
             } else if (ht_lookup(slots, mask, v, &r)) {
                 s = ustart[r];
                 c = ucount[r];
@@ -922,17 +936,13 @@ struct RunsOp {
 // its position at the run's value, the last row its length.
 // (keys >= domain: the 0xffffffff tail of a word build sized by its bound,
 // not indexed)
-__global__ void direct_start_kernel(const u32* __restrict__ keys, u64 n, u32* __restrict__ dstart, u64 domain) {
+__global__ void direct_runs_kernel(const u32* __restrict__ keys, u64 n, u32* __restrict__ dstart,
+                                   u32* __restrict__ dend, u64 domain) {
     GRID_STRIDE(i, n) {
         const u32 k = keys[i];
-        if (k < domain && (i == 0 || keys[i - 1] != k)) dstart[k] = static_cast<u32>(i);
-    }
-}
-__global__ void direct_count_kernel(const u32* __restrict__ keys, u64 n, const u32* __restrict__ dstart,
-                                    u32* __restrict__ dcount, u64 domain) {
-    GRID_STRIDE(i, n) {
-        const u32 k = keys[i];
-        if (k < domain && (i + 1 == n || keys[i + 1] != k)) dcount[k] = static_cast<u32>(i + 1 - dstart[k]);
+        if (k >= domain) continue;
+        if (i == 0 || keys[i - 1] != k) dstart[k] = static_cast<u32>(i);
+        if (i + 1 == n || keys[i + 1] != k) dend[k] = static_cast<u32>(i + 1);
     }
 }
 
@@ -2337,6 +2347,7 @@ bool engine_group_keys(Ctx* c, DBuf<u64>& keys, u64 n, u32 shift, JoinIndex* run
         // is (base32[v], cnt[v]) — no compaction, no hash table, no host
         // readback of the run count.
         runs->domain = domain;
+        runs->ends = false;  // counts
         runs->n_unique = n;  // not counted; non-zero marks a non-empty index
         runs->ustart = std::move(base32);
         runs->ucount = std::move(cnt);
@@ -2443,6 +2454,7 @@ struct ProbeScanOp {
     const u32* ustart;
     const u32* ucount;
     u64 domain;
+    bool ends;
     RowFilter pred;
     u32* starts;
     u64* offsets;
@@ -2452,10 +2464,7 @@ struct ProbeScanOp {
         if (pass_filters(pred.f, pred.n, i, 0)) {
             const u32 v = probe[i];
             if (domain) {
-                if (v < domain) {
-                    s = ustart[v];
-                    c = ucount[v];
-                }
+                if (v < domain) direct_run(ustart, ucount, ends, v, &s, &c);
             } else if (ht_lookup(slots, mask, v, &r)) {
                 s = ustart[r];
                 c = ucount[r];
@@ -2480,7 +2489,7 @@ void engine_probe_offsets(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx,
     ProfScope prof(c, "join_probe_count", double(n) * 20.0);
     tile_scan(c,
               ProbeScanOp{probe, idx.ht.slots.get(), idx.ht.mask, idx.ustart.get(), idx.ucount.get(), idx.domain,
-                          pred, starts, offsets, n},
+                          idx.ends, pred, starts, offsets, n},
               n, nullptr);
 }
 
@@ -2494,7 +2503,8 @@ void engine_probe_count(Ctx* c, const u32* probe, u64 n, const JoinIndex& idx, c
     }
     ProfScope prof(c, "join_probe_count", double(n) * 20.0);
     probe_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(probe, n, idx.ht.slots.get(), idx.ht.mask,
-                                                            idx.ustart.get(), idx.ucount.get(), idx.domain, pred,
+                                                            idx.ustart.get(), idx.ucount.get(), idx.domain,
+                                                            idx.ends, pred,
                                                             starts, counts);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
@@ -2617,27 +2627,28 @@ void engine_project(Ctx* c, u64 n, const OutSpec& spec) {
 void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u32 key_bits) {
     idx.n_unique = 0;
     idx.domain = 0;
+    idx.ends = false;
     if (n == 0) return;
     // (only where the domain is not much larger than the rows: the arrays
     // and their clearing scale with the domain)
     if (key_bits && key_bits <= kGroupMaxBits && (u64(1) << key_bits) <= 16 * n) {
-        // Direct-address index over the value domain: run starts and lengths
-        // at their values (two light passes, no compaction, no hash table,
-        // no host readback of the run count).
+        // Direct-address index over the value domain: run starts and ends
+        // at their values (one light pass, only the ends cleared; no
+        // compaction, no hash table, no host readback of the run count).
         const u64 domain = u64(1) << key_bits;
         idx.domain = domain;
+        idx.ends = true;
         idx.n_unique = n;  // not counted; non-zero marks a non-empty index
         idx.ustart = DBuf<u32>(c, domain);
         idx.ucount = DBuf<u32>(c, domain);
         idx.ukeys = DBuf<u32>();
         idx.ht = HashIndex();
         FV_CUDA(cudaMemsetAsync(idx.ucount.get(), 0, 4 * domain, c->stream));
-        ProfScope prof(c, "direct_index", 8.0 * double(n));
-        direct_start_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), domain);
-        direct_count_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), idx.ucount.get(),
-                                                                 domain);
+        ProfScope prof(c, "direct_index", 4.0 * double(n));
+        direct_runs_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), idx.ucount.get(),
+                                                                domain);
         FV_CUDA(cudaGetLastError());
-        c->count_launch(2);
+        c->count_launch();
         return;
     }
     DBuf<u32> uk(c, n), us(c, n);
