@@ -1919,15 +1919,30 @@ public:
         const u64 tuples = s.counter.get() ? s.tuples : 0;
         if (!r.word_mode) {
             // Word sink with a tuple DELTA: the merged words of the
-            // iteration expand to packed tuple keys, then the usual path.
-            DBuf<u64> tk(c_, std::max<u64>(tuples, 1));
+            // iteration become DELTA's tuples.
             if (nw) {
                 s.bits = DBuf<u32>(c_, nw);
                 const bool idx_ok = s.gen0 == r.blocks.generation && r.blocks.capacity() <= (u64(1) << 27);
                 engine_blockset_collect(c_, s.keys.get(), idx_ok ? s.widx.get() : nullptr, nw, block_args(r),
                                         s.bits.get());
-                engine_expand_word_keys(c_, s.keys.get(), s.bits.get(), nw, tk.get());
             }
+            if (nw && grouped_expand_ && r.levels_mode && r.arity == 2) {
+                // Group the word entries by x (counting sort over words, not
+                // tuples), then expand them: the tuples come out grouped by x
+                // with no tuple-level sort or scatter.
+                DBuf<u32> wb(c_, nw);
+                if (engine_group_keys(c_, s.keys, nw, st_.key_shift, nullptr, nullptr, nullptr, s.bits.get(),
+                                      wb.get())) {
+                    const u64 nd = install_word_delta(r, s.keys.get(), wb.get(), nw, tuples);
+                    s.keys = DBuf<u64>();
+                    s.cap = 0;
+                    if (r.word_sparse && !r.temp) leave_word_mode(r);
+                    return nd;
+                }
+            }
+            // ... else expand to packed tuple keys, then the usual path.
+            DBuf<u64> tk(c_, std::max<u64>(tuples, 1));
+            if (nw) engine_expand_word_keys(c_, s.keys.get(), s.bits.get(), nw, tk.get());
             s.keys = DBuf<u64>();
             s.cap = 0;
             const u64 nd = finish_delta(r, std::move(tk), tuples);
@@ -1988,6 +2003,26 @@ public:
         }
         if (r.word_sparse && !r.temp) leave_word_mode(r);
         return tuples;
+    }
+
+    // Levels-mode binary relation: DELTA = the tuples of nw word entries
+    // (word key, mask) already grouped by x (nd tuples in all), with its
+    // column-0 direct index; the previous DELTA becomes a level.
+    u64 install_word_delta(RelState& r, const u64* wkeys, const u32* wb, u64 nw, u64 nd) {
+        invalidate(r);
+        if (r.delta.n) r.levels.push_back(std::move(r.delta));
+        DevVersion Dv;
+        Dv.n = nd;
+        for (u32 j = 0; j < 2; ++j) Dv.cols.emplace_back(c_, std::max<u64>(nd, 1));
+        r.keys.count += nd;
+        r.level_rows += nd;
+        engine_expand_word_keys(c_, wkeys, wb, nw, nullptr, Dv.cols[0].get(), Dv.cols[1].get(), st_.key_shift);
+        auto di = std::make_unique<JoinIndex>();
+        engine_build_runs(c_, Dv.cols[0].get(), nd, *di, st_.key_shift, true);
+        r.delta = std::move(Dv);
+        di->rows = &r.delta;
+        r.indexes.emplace(std::make_pair(static_cast<int>(kDelta), 0u), std::move(di));
+        return nd;
     }
 
     // Word-form version -> tuple form (grouping by x is kept).
@@ -2232,6 +2267,13 @@ private:
     // another instead of one fused single-pass probe + scan.
     const bool fused_probe_scan_ = [] {
         const char* e = std::getenv("FVLOG_PROBE_SCAN");
+        return !(e && std::string(e) == "0");
+    }();
+    // FVLOG_GROUPED_EXPAND=0: a word sink's tuple DELTA is expanded to
+    // packed keys and grouped by a tuple-level counting sort instead of
+    // grouping the word entries and expanding them in place.
+    const bool grouped_expand_ = [] {
+        const char* e = std::getenv("FVLOG_GROUPED_EXPAND");
         return !(e && std::string(e) == "0");
     }();
     // FVLOG_SCATTER_GATHER=1: the grouping scatter reads a word-form DELTA's

@@ -461,7 +461,8 @@ u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity);
 void engine_count_blocks_async(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity, u64* d_out);
 // Packed tuple keys of n word entries (word key, mask) into out, sized by
 // the caller to the sum of the masks' popcounts (no host readback).
-void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out);
+void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out, u32* out_x = nullptr,
+                             u32* out_z = nullptr, u32 shift = 0);
 // Word form (x, z base, mask) of a lexicographically sorted binary version
 // of n rows; outputs sized n; returns the word count.
 u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits,
@@ -476,7 +477,9 @@ u64 engine_blockset_dump(Ctx* c, const BlockSet& s, u32 arity, u32* c0, u32* c1)
 // Tuples (x, z) of n word entries (x, z base, mask), entry order kept (so
 // entries grouped by x give tuples grouped by x); returns the tuple count.
 // out_x null: count only.
-u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u64 n, u32* out_x, u32* out_z);
+// count false: no readback (the caller knows the total), returns 0.
+u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u64 n, u32* out_x, u32* out_z,
+                        bool count = true);
 // Distinct rows of sorted packed keys into fresh word buffers; returns the count.
 u64 engine_unique_words(Ctx* c, const std::vector<DBuf<u64>>& words, u64 n, std::vector<DBuf<u64>>& out);
 // SoA columns -> row-major rows out[i * arity + j] (device buffer).
@@ -509,7 +512,10 @@ void engine_project(Ctx* c, u64 n, const OutSpec& spec);
 // RLE of a sorted key column into (ukeys, ustart, ucount) + hash table.
 // key_bits (the key domain's bit width, when <= 24): a direct-address index
 // instead of runs + hash (no host readback).
-void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u32 key_bits = 0);
+// force_direct: a direct-address index whenever key_bits allows one (the
+// caller accepts the 2^key_bits arrays however few the rows).
+void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u32 key_bits = 0,
+                       bool force_direct = false);
 // Pack SoA columns into W key words.
 void engine_pack_keys(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 shift, u64* const* words);
 // p[i] = (p[i] & and_mask) | or_bits (tagging / untagging packed keys).

@@ -1442,8 +1442,11 @@ struct PopcOffsetsOp {
 // lane finding its word by a shuffle search over the warp's offsets and its
 // bit with __fns, so the writes are coalesced (a thread-per-word loop writes
 // up to 32 scattered rows per thread).
+// out_x (optional): the tuples as SoA columns (x = key >> shift, z) instead
+// of packed keys.
 __global__ void expand_word_keys_kernel(const u64* __restrict__ keys, const u32* __restrict__ bits,
-                                        const u64* __restrict__ off, u64 n, u64* __restrict__ out) {
+                                        const u64* __restrict__ off, u64 n, u64* __restrict__ out,
+                                        u32* __restrict__ out_x, u32* __restrict__ out_z, u32 shift) {
     const u32 lane = lane_id();
     const u64 warps = (n + 31) / 32;
     for (u64 w = (u64(blockIdx.x) * blockDim.x + threadIdx.x) / 32; w < warps;
@@ -1474,7 +1477,12 @@ __global__ void expand_word_keys_kernel(const u64* __restrict__ keys, const u32*
             const u64 wk = __shfl_sync(0xffffffffu, k, lo);
             if (t < tot) {
                 const u32 b = __fns(wm, 0, t - wr + 1);
-                out[base + t] = wk + b;
+                if (out_x) {
+                    out_x[base + t] = static_cast<u32>(wk >> shift);
+                    out_z[base + t] = static_cast<u32>(wk & ((u64(1) << shift) - 1)) + b;
+                } else {
+                    out[base + t] = wk + b;
+                }
             }
         }
     }
@@ -2109,12 +2117,13 @@ void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, co
     c->count_launch();
 }
 
-void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out) {
+void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out, u32* out_x, u32* out_z,
+                             u32 shift) {
     if (!n) return;
     DBuf<u64> off(c, n);
     ProfScope prof(c, "expand_words", 12.0 * double(n));
     tile_scan(c, PopcOffsetsOp{bits, off.get()}, n, nullptr);
-    expand_word_keys_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, bits, off.get(), n, out);
+    expand_word_keys_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, bits, off.get(), n, out, out_x, out_z, shift);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }
@@ -2137,13 +2146,15 @@ u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, 
     return total;
 }
 
-u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u64 n, u32* out_x, u32* out_z) {
+u64 engine_expand_words(Ctx* c, const u32* x, const u32* zb, const u32* bits, u64 n, u32* out_x, u32* out_z,
+                        bool count) {
     if (!n) return 0;
     u64* d = c->d_scalars + 40;
     {
         ProfScope prof(c, "expand_words", 12.0 * double(n));
         tile_scan(c, ExpandWordsOp{x, zb, bits, out_x, out_z}, n, d);
     }
+    if (!count) return 0;
     u64 total = 0;
     c->read_scalars(d, &total, 1);
     return total;
@@ -2624,14 +2635,14 @@ void engine_project(Ctx* c, u64 n, const OutSpec& spec) {
     c->count_launch();
 }
 
-void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u32 key_bits) {
+void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u32 key_bits, bool force_direct) {
     idx.n_unique = 0;
     idx.domain = 0;
     idx.ends = false;
     if (n == 0) return;
     // (only where the domain is not much larger than the rows: the arrays
     // and their clearing scale with the domain)
-    if (key_bits && key_bits <= kGroupMaxBits && (u64(1) << key_bits) <= 16 * n) {
+    if (key_bits && key_bits <= kGroupMaxBits && (force_direct || (u64(1) << key_bits) <= 16 * n)) {
         // Direct-address index over the value domain: run starts and ends
         // at their values (one light pass, only the ends cleared; no
         // compaction, no hash table, no host readback of the run count).
