@@ -1397,7 +1397,15 @@ __global__ void blockset_word_insert_kernel(const u64* __restrict__ keys, const 
 // its block's DELTA bitmap word and clears it for the next iteration. With
 // widx (no directory growth since the entries were appended) the word index
 // recorded at append time is used; otherwise the block is looked up.
-constexpr int kCollectItems = 4;  // independent gathers in flight per thread
+// Read-and-clear of the DELTA words by atomicExch (one L2 request per
+// word) instead of a load and a store: C2 23.46 -> 21.77 ms.
+#ifndef FV_COLLECT_EXCH
+#define FV_COLLECT_EXCH 1
+#endif
+#ifndef FV_COLLECT_ITEMS
+#define FV_COLLECT_ITEMS 4
+#endif
+constexpr int kCollectItems = FV_COLLECT_ITEMS;  // independent gathers in flight per thread
 __global__ void blockset_collect_kernel(const u64* __restrict__ keys, const u32* __restrict__ widx, u64 n,
                                         BlockSetArgs s, u32* __restrict__ out) {
     const u64 base = u64(blockIdx.x) * blockDim.x * kCollectItems + threadIdx.x;
@@ -1418,6 +1426,15 @@ __global__ void blockset_collect_kernel(const u64* __restrict__ keys, const u32*
         }
     }
     u32 v[kCollectItems];
+#if FV_COLLECT_EXCH
+    // read-and-clear as one L2 atomic per word (one request instead of a
+    // load and a store: the kernel is bound by the random requests)
+#pragma unroll
+    for (int k = 0; k < kCollectItems; ++k) v[k] = w[k] != ~u64(0) ? atomicExch(s.dbits + w[k], 0u) : 0;
+#pragma unroll
+    for (int k = 0; k < kCollectItems; ++k)
+        if (w[k] != ~u64(0)) out[base + u64(k) * blockDim.x] = v[k];
+#else
 #pragma unroll
     for (int k = 0; k < kCollectItems; ++k) v[k] = w[k] != ~u64(0) ? __ldcg(s.dbits + w[k]) : 0;
 #pragma unroll
@@ -1426,6 +1443,7 @@ __global__ void blockset_collect_kernel(const u64* __restrict__ keys, const u32*
         out[base + u64(k) * blockDim.x] = v[k];
         s.dbits[w[k]] = 0;
     }
+#endif
 }
 
 
