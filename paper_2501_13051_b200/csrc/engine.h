@@ -99,9 +99,10 @@ struct JoinIndex {
     // domain > 0: direct-address index (from a counting-sort grouping):
     // ustart/ucount have `domain` entries indexed by value, no ukeys/ht.
     u64 domain = 0;
-    // direct index built from sorted keys: ucount holds each run's END
-    // (exclusive; 0 = no run, ustart then unset) — one pass, one cleared
-    // array (the counting-sort grouping's index keeps counts).
+    // direct index built from sorted keys: ustart holds interleaved
+    // (start, end) pairs per value (end exclusive; 0 = no run) and ucount is
+    // empty — one pass to build, one 8-byte load per probe (the
+    // counting-sort grouping's index keeps separate starts and counts).
     bool ends = false;
 };
 

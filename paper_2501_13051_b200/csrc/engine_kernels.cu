@@ -69,6 +69,14 @@ __device__ __forceinline__ bool ht_lookup(const u64* __restrict__ slots, u32 mas
 // holds the run's end, 0 when there is none).
 __device__ __forceinline__ void direct_run(const u32* __restrict__ ustart, const u32* __restrict__ ucount, bool ends,
                                            u32 v, u32* s, u32* c) {
+    if (!ucount) {  // interleaved (start, end) pairs: one 8-byte load
+        const uint2 p = reinterpret_cast<const uint2*>(ustart)[v];
+        if (p.y) {
+            *s = p.x;
+            *c = p.y - p.x;
+        }
+        return;
+    }
     const u32 e = ucount[v];
     if (ends) {
         if (e) {
@@ -936,13 +944,14 @@ struct RunsOp {
 // its position at the run's value, the last row its length.
 // (keys >= domain: the 0xffffffff tail of a word build sized by its bound,
 // not indexed)
-__global__ void direct_runs_kernel(const u32* __restrict__ keys, u64 n, u32* __restrict__ dstart,
-                                   u32* __restrict__ dend, u64 domain) {
+// Run (start, end) of every value into pair[2v], pair[2v + 1] (pair cleared:
+// end 0 = no run).
+__global__ void direct_runs_kernel(const u32* __restrict__ keys, u64 n, u32* __restrict__ pair, u64 domain) {
     GRID_STRIDE(i, n) {
         const u32 k = keys[i];
         if (k >= domain) continue;
-        if (i == 0 || keys[i - 1] != k) dstart[k] = static_cast<u32>(i);
-        if (i + 1 == n || keys[i + 1] != k) dend[k] = static_cast<u32>(i + 1);
+        if (i == 0 || keys[i - 1] != k) pair[2 * u64(k)] = static_cast<u32>(i);
+        if (i + 1 == n || keys[i + 1] != k) pair[2 * u64(k) + 1] = static_cast<u32>(i + 1);
     }
 }
 
@@ -2668,14 +2677,14 @@ void engine_build_runs(Ctx* c, const u32* sorted_keys, u64 n, JoinIndex& idx, u3
         idx.domain = domain;
         idx.ends = true;
         idx.n_unique = n;  // not counted; non-zero marks a non-empty index
-        idx.ustart = DBuf<u32>(c, domain);
-        idx.ucount = DBuf<u32>(c, domain);
+        // (start, end) interleaved: a probe is one 8-byte load (ucount empty)
+        idx.ustart = DBuf<u32>(c, 2 * domain);
+        idx.ucount = DBuf<u32>();
         idx.ukeys = DBuf<u32>();
         idx.ht = HashIndex();
-        FV_CUDA(cudaMemsetAsync(idx.ucount.get(), 0, 4 * domain, c->stream));
+        FV_CUDA(cudaMemsetAsync(idx.ustart.get(), 0, 8 * domain, c->stream));
         ProfScope prof(c, "direct_index", 4.0 * double(n));
-        direct_runs_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), idx.ucount.get(),
-                                                                domain);
+        direct_runs_kernel<<<grid_for(n), 256, 0, c->stream>>>(sorted_keys, n, idx.ustart.get(), domain);
         FV_CUDA(cudaGetLastError());
         c->count_launch();
         return;
