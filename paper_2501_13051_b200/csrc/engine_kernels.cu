@@ -305,6 +305,11 @@ __device__ __forceinline__ u64 word_key_of(u64 key, u32 shift, u32* bit) {
 // is flagged in *first (its key is appended once; the merged mask is read at
 // finalize). *ones = the new bits of this thread. Words whose block found no
 // directory slot are flagged in *ovf_mask.
+// A plain load of the FULL word before its atomicOr (repeats take no atomic):
+// measured without it C2 21.7 -> 23.9 ms, C4 64.9 -> 65.2.
+#ifndef FV_WORD_TEST_LOAD
+#define FV_WORD_TEST_LOAD 1
+#endif
 template <int N>
 __device__ __forceinline__ void blockset_word_items(const BlockSetArgs& s, u32 live, const u64 (&key)[N],
                                                     const u32 (&bits)[N], u32* first, u32* ones, u32* ovf_mask,
@@ -336,16 +341,22 @@ __device__ __forceinline__ void blockset_word_items(const BlockSetArgs& s, u32 l
         }
         slot[k] = f * 32 + wi[k];  // bitmap word index from here on
     }
+    u32 nb[N];
+#if FV_WORD_TEST_LOAD
+    // a plain load first: a word whose bits are all present takes no atomic
     u32 wv[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) wv[k] = ((live >> k) & 1u) ? __ldcg(s.bits + slot[k]) : ~0u;
-    u32 nb[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         nb[k] = 0;
         if (!((live >> k) & 1u) || (wv[k] & bits[k]) == bits[k]) continue;
         nb[k] = bits[k] & ~atomicOr(s.bits + slot[k], bits[k]);
     }
+#else
+#pragma unroll
+    for (int k = 0; k < N; ++k) nb[k] = ((live >> k) & 1u) ? bits[k] & ~atomicOr(s.bits + slot[k], bits[k]) : 0u;
+#endif
     u32 fm = 0, n1 = 0;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
