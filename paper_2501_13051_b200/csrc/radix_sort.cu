@@ -192,6 +192,9 @@ constexpr int sort_min_blocks() { return sizeof(K) == 8 && HAS_VAL ? 3 : FV_SORT
 #ifndef FV_SORT_EARLY
 #define FV_SORT_EARLY 1
 #endif
+#ifndef FV_SORT_RANK_GROUP
+#define FV_SORT_RANK_GROUP 1
+#endif
 // Peer masks from match.any (1) instead of one ballot per digit bit (0).
 #ifndef FV_SORT_MATCH
 #define FV_SORT_MATCH 0
@@ -289,36 +292,45 @@ __global__ void __launch_bounds__(kSortBlock, (sort_min_blocks<K, HAS_VAL>())) o
     auto rank_items = [&](auto partial_tag, auto full_digit_tag) {
         constexpr bool PARTIAL = decltype(partial_tag)::value;
         constexpr bool FULL_DIGIT = decltype(full_digit_tag)::value;
+        constexpr int G = FV_SORT_RANK_GROUP;  // items whose peer masks are formed together (ILP)
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-            const u32 d = dig[k];
-            u32 peers = ~0u;
-            if (FV_SORT_MATCH) {
-                peers = __match_any_sync(0xffffffffu, d);
-            } else if (PARTIAL) {
-                const bool valid_item = d != 0xffffu;
-                peers = __ballot_sync(0xffffffffu, valid_item);
-                if (!valid_item) peers = ~peers;
+        for (int k0 = 0; k0 < ITEMS; k0 += G) {
+            u32 peers[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const u32 d = dig[k0 + g];
+                peers[g] = ~0u;
+                if (FV_SORT_MATCH) {
+                    peers[g] = __match_any_sync(0xffffffffu, d);
+                } else if (PARTIAL) {
+                    const bool valid_item = d != 0xffffu;
+                    peers[g] = __ballot_sync(0xffffffffu, valid_item);
+                    if (!valid_item) peers[g] = ~peers[g];
+                }
+#pragma unroll
+                for (int b = 0; b < (FV_SORT_MATCH ? 0 : kRadixBits); ++b) {
+                    if (!FULL_DIGIT && !((mask >> b) & 1u)) break;
+                    const u32 bit = (d >> b) & 1u;
+                    const u32 x = __ballot_sync(0xffffffffu, bit);
+                    peers[g] &= ~(x ^ (0u - bit));
+                }
             }
 #pragma unroll
-            for (int b = 0; b < (FV_SORT_MATCH ? 0 : kRadixBits); ++b) {
-                if (!FULL_DIGIT && !((mask >> b) & 1u)) break;
-                const u32 bit = (d >> b) & 1u;
-                const u32 x = __ballot_sync(0xffffffffu, bit);
-                peers &= ~(x ^ (0u - bit));
+            for (int g = 0; g < G; ++g) {
+                const u32 d = dig[k0 + g];
+                const u32 leader = __ffs(peers[g]) - 1;
+                u32 b = 0;
+                if ((!PARTIAL || d != 0xffffu) && lane == leader) {
+                    b = s_whist[warp][d];
+                    s_whist[warp][d] = b + __popc(peers[g]);
+                }
+                b = __shfl_sync(0xffffffffu, b, leader);
+                dig[k0 + g] = d | ((b + __popc(peers[g] & lanemask_lt())) << 16);  // digit | rank << 16
+                // The next item's leader for this digit may be another lane:
+                // order this lane's counter update before its read
+                // (compute-sanitizer racecheck flagged the pair without it).
+                __syncwarp();
             }
-            const u32 leader = __ffs(peers) - 1;
-            u32 b = 0;
-            if ((!PARTIAL || d != 0xffffu) && lane == leader) {
-                b = s_whist[warp][d];
-                s_whist[warp][d] = b + __popc(peers);
-            }
-            b = __shfl_sync(0xffffffffu, b, leader);
-            dig[k] = d | ((b + __popc(peers & lanemask_lt())) << 16);  // digit | rank << 16
-            // The next item's leader for this digit may be another lane: order
-            // this lane's counter update before its read (compute-sanitizer
-            // racecheck flagged the pair without it).
-            __syncwarp();
         }
     };
     using True = std::integral_constant<bool, true>;
