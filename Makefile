@@ -18,7 +18,7 @@ CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 HDRS := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/fvlog.h
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP_SRCS))
 
-all: $(PKG)/libfvlog.so $(PKG)/fvlog tools/fvlog_membench tools/fvlog_sortbench
+all: $(PKG)/libfvlog.so $(PKG)/fvlog tools/fvlog_membench tools/fvlog_sortbench tools/fvlog_scanbench
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -39,10 +39,13 @@ tools/fvlog_membench: tools/membench.cu
 	$(NVCC) -O3 $(ARCH) -lineinfo -ccbin $(HOSTCXX) -o $@ $<
 
 SORTBENCH_OBJS := $(OBJ)/fv_ctx.o $(OBJ)/radix_sort.o $(OBJ)/prim.o
+tools/fvlog_scanbench: tools/scanbench.cu $(OBJ)/fv_ctx.o $(OBJ)/prim.o $(HDRS)
+	$(NVCC) $(NVFLAGS) -o $@ $< $(OBJ)/fv_ctx.o $(OBJ)/prim.o -cudart static -lpthread
+
 tools/fvlog_sortbench: tools/sortbench.cu $(SORTBENCH_OBJS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -o $@ $< $(SORTBENCH_OBJS) -cudart static -lpthread
 
 clean:
-	rm -rf build $(PKG)/libfvlog.so $(PKG)/fvlog tools/fvlog_membench tools/fvlog_sortbench
+	rm -rf build $(PKG)/libfvlog.so $(PKG)/fvlog tools/fvlog_membench tools/fvlog_sortbench tools/fvlog_scanbench
 
 .PHONY: all clean

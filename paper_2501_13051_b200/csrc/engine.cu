@@ -688,12 +688,6 @@ public:
 
     // `old_src[s]`: source s reads FULL - DELTA instead of FULL (exactly-once
     // variants; empty = every non-DELTA source reads FULL, the reference).
-    void exec_variant(const Plan& plan, const DistPlan& dp, long delta_source, const std::vector<u8>& old_src,
-                      CandPool& out, HeadSink* sink) {
-        std::unique_ptr<VarRun> v = prepare_variant(plan, dp, delta_source, old_src, out, sink);
-        if (v) run_variant(*v);
-    }
-
     // A variant's versions and step-0 input; null when a source is empty.
     std::unique_ptr<VarRun> prepare_variant(const Plan& plan, const DistPlan& dp, long delta_source,
                                             const std::vector<u8>& old_src, CandPool& out, HeadSink* sink) {

@@ -12,8 +12,14 @@
 
 namespace fv {
 
-constexpr int kScanBlock = 256;
-constexpr int kScanItems = 8;
+#ifndef FV_SCAN_BLOCK
+#define FV_SCAN_BLOCK 256
+#endif
+constexpr int kScanBlock = FV_SCAN_BLOCK;
+#ifndef FV_SCAN_ITEMS
+#define FV_SCAN_ITEMS 8
+#endif
+constexpr int kScanItems = FV_SCAN_ITEMS;
 constexpr int kScanTile = kScanBlock * kScanItems;
 
 // Block-wide exclusive scan of one u64 per thread; returns the thread's
@@ -48,29 +54,63 @@ __device__ __forceinline__ u64 block_exclusive_scan(u64 v, u64* s_warp, u64* tot
     return excl;
 }
 
+// Striped (default): value() and emit() are called in warp-striped order
+// (item k of lane l of warp w at k * BLOCK + l — every global access of the
+// ops coalesced), the values transposed through shared memory to a blocked
+// arrangement for the thread-sequential scan and the prefixes back.
+#ifndef FV_SCAN_STRIPED
+#define FV_SCAN_STRIPED 1
+#endif
+__device__ __forceinline__ u32 scan_pad(u32 j) { return j + (j >> 4); }  // u64 bank-conflict padding
+
 // Op contract:
 //   __device__ u64  value(u64 i) const;            // item weight (0/1 for select)
 //   __device__ void emit(u64 i, u64 prefix, u64 v) const;  // called for every i < n
 // The last tile stores the grand total to *d_total.
+// 8 CTAs per SM (32 registers): the warps of other tiles cover a tile's
+// look-back (tools/scanbench.cu, 10^8 counts: 1.55 -> 2.38 TB/s; with the
+// values kept in registers and 4 CTAs per SM most of the time went to the
+// barrier after warp 0's look-back).
+#ifndef FV_SCAN_MINB
+#define FV_SCAN_MINB 8
+#endif
 template <int BLOCK, int ITEMS, class Op>
-__global__ void __launch_bounds__(BLOCK) tile_scan_kernel(Op op, u64 n, u64* status, u32 epoch,
+__global__ void __launch_bounds__(BLOCK, FV_SCAN_MINB) tile_scan_kernel(Op op, u64 n, u64* status, u32 epoch,
                                                           u32* tile_counter, u64* d_total) {
     __shared__ u32 s_tile;
     __shared__ u64 s_warp[BLOCK / 32 + 1];
     __shared__ u64 s_prefix;
+#if FV_SCAN_STRIPED
+    __shared__ u64 s_x[BLOCK * ITEMS + (BLOCK * ITEMS) / 16 + 1];
+#endif
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const u32 tile = s_tile;
-    const u64 base = u64(tile) * (BLOCK * ITEMS) + u64(threadIdx.x) * ITEMS;
+    const u64 tile_base = u64(tile) * (BLOCK * ITEMS);
+    [[maybe_unused]] const u64 base = tile_base + u64(threadIdx.x) * ITEMS;
 
-    u64 v[ITEMS];
     u64 sum = 0;
+#if FV_SCAN_STRIPED
+    // (no per-item registers across the look-back: the values live in s_x,
+    // so more CTAs fit per SM to hide it)
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u32 li = k * BLOCK + threadIdx.x;
+        const u64 i = tile_base + li;
+        s_x[scan_pad(li)] = i < n ? op.value(i) : 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) sum += s_x[scan_pad(threadIdx.x * ITEMS + k)];
+#else
+    u64 v[ITEMS];
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         const u64 i = base + k;
         v[k] = i < n ? op.value(i) : 0;
         sum += v[k];
     }
+#endif
     u64 agg;
     const u64 excl = block_exclusive_scan<BLOCK>(sum, s_warp, &agg);
 
@@ -92,12 +132,34 @@ __global__ void __launch_bounds__(BLOCK) tile_scan_kernel(Op op, u64 n, u64* sta
     }
     __syncthreads();
     u64 run = s_prefix + excl;
+#if FV_SCAN_STRIPED
+    // values -> exclusive prefixes in place (block_exclusive_scan's last
+    // barrier ordered every read of s_x above); an item's value is then the
+    // next prefix minus its own (the tile's last: the tile total's end).
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u32 j = scan_pad(threadIdx.x * ITEMS + k);
+        const u64 x = s_x[j];
+        s_x[j] = run;
+        run += x;
+    }
+    if (threadIdx.x == BLOCK - 1) s_x[scan_pad(BLOCK * ITEMS)] = run;  // the slot past the tile
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u32 li = k * BLOCK + threadIdx.x;
+        const u64 i = tile_base + li;
+        const u64 p = s_x[scan_pad(li)];
+        if (i < n) op.emit(i, p, s_x[scan_pad(li + 1)] - p);
+    }
+#else
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         const u64 i = base + k;
         if (i < n) op.emit(i, run, v[k]);
         run += v[k];
     }
+#endif
 }
 
 // Launch helper. d_total may be null. n == 0 writes *d_total = 0.
