@@ -1696,7 +1696,7 @@ public:
             u64 need = std::max(r.blocks.blocks + std::max<u64>(4096, std::min(n, r.blocks.blocks)),
                                 r.blocks.capacity() / 2 + 1);
             if (n >= (u64(1) << 16))
-                need = std::max(need, r.blocks.blocks + engine_count_blocks(c_, tmp.get(), n, st_.key_shift, r.arity));
+                need = std::max(need, r.blocks.blocks + count_blocks(tmp.get(), n, r.arity));
             if (!block_grow(r, need, r.keys.count + s.bound + n)) {
                 // too sparse for blocks: the key set takes over, overflow keys included
                 convert_to_keyset(r, &s, tmp.get(), n);
@@ -1829,8 +1829,20 @@ public:
     // insert instead of by overflow rounds.
     void estimate_blocks(RelState& r, const CandPool& pool) {
         if (!r.block_mode || r.blocks.ratio > 0 || pool.n < (u64(1) << 16) || block_ratio_ >= 0) return;
-        const u64 nb = engine_count_blocks(c_, pool.words[0].get(), pool.n, st_.key_shift, r.arity);
+        const u64 nb = count_blocks(pool.words[0].get(), pool.n, r.arity);
         r.blocks.ratio = double(nb) / double(pool.n);
+    }
+
+    // Distinct blocks of n packed keys, to size a directory: the HyperLogLog
+    // sketch (one pass) unless FVLOG_EXACT_BLOCKS=1 (sort + count).
+    u64 count_blocks(const u64* keys, u64 n, u32 arity) {
+        if (exact_blocks_) return engine_count_blocks(c_, keys, n, st_.key_shift, arity);
+        if (!n) return 0;
+        DBuf<u32> regs(c_, kBlockSketchRegs);
+        engine_block_sketch(c_, keys, n, st_.key_shift, arity, regs.get());
+        std::vector<u32> h(kBlockSketchRegs);
+        regs.download(h.data(), kBlockSketchRegs);
+        return std::min<u64>(n, block_sketch_estimate(h.data()));
     }
 
     // estimate_blocks for several heads' pools with one read of the counts.
@@ -1843,13 +1855,26 @@ public:
                 need.push_back(r);
         }
         if (need.size() < 2) return;  // (a single one reads its count in estimate_blocks)
-        DBuf<u64> d(c_, need.size());
-        for (size_t q = 0; q < need.size(); ++q) {
-            const CandPool& pool = pooled.at(need[q]->name);
-            engine_count_blocks_async(c_, pool.words[0].get(), pool.n, st_.key_shift, need[q]->arity, d.get() + q);
-        }
         std::vector<u64> nb(need.size());
-        d.download(nb.data(), need.size());
+        if (exact_blocks_) {
+            DBuf<u64> d(c_, need.size());
+            for (size_t q = 0; q < need.size(); ++q) {
+                const CandPool& pool = pooled.at(need[q]->name);
+                engine_count_blocks_async(c_, pool.words[0].get(), pool.n, st_.key_shift, need[q]->arity, d.get() + q);
+            }
+            d.download(nb.data(), need.size());
+        } else {
+            DBuf<u32> regs(c_, kBlockSketchRegs * need.size());
+            for (size_t q = 0; q < need.size(); ++q) {
+                const CandPool& pool = pooled.at(need[q]->name);
+                engine_block_sketch(c_, pool.words[0].get(), pool.n, st_.key_shift, need[q]->arity,
+                                    regs.get() + kBlockSketchRegs * q);
+            }
+            std::vector<u32> h(kBlockSketchRegs * need.size());
+            regs.download(h.data(), h.size());
+            for (size_t q = 0; q < need.size(); ++q)
+                nb[q] = std::min<u64>(pooled.at(need[q]->name).n, block_sketch_estimate(h.data() + kBlockSketchRegs * q));
+        }
         for (size_t q = 0; q < need.size(); ++q)
             need[q]->blocks.ratio = double(nb[q]) / double(pooled.at(need[q]->name).n);
     }
@@ -2256,6 +2281,12 @@ private:
     const u32 word_combine_ = [] {
         const char* e = std::getenv("FVLOG_WORD_COMBINE");
         return e ? static_cast<u32>(std::atoi(e) != 0) : 1u;
+    }();
+    // FVLOG_EXACT_BLOCKS=1: directory sizes from an exact distinct-block
+    // count (54-bit radix sort) instead of the HyperLogLog sketch.
+    const bool exact_blocks_ = [] {
+        const char* e = std::getenv("FVLOG_EXACT_BLOCKS");
+        return e && std::string(e) == "1";
     }();
     // FVLOG_PROBE_SCAN=0: probe counts written by one kernel and scanned by
     // another instead of one fused single-pass probe + scan.

@@ -12,6 +12,7 @@
 //   merge         dedup_rows + deduplicate + difference + merge_delta
 //                 (relation.cpp:71-108, kernels.cpp:210-268) as ONE
 //                 merge-path pass over sorted FULL and sorted candidates.
+#include <cmath>
 #include <optional>
 #include <cstdlib>
 
@@ -1589,6 +1590,28 @@ __global__ void block_ids_kernel(const u64* __restrict__ keys, u64 n, u32 shift,
     }
 }
 
+// HyperLogLog sketch of the distinct block ids of n packed keys (2^12
+// registers, ~1.6 % standard error): one pass, shared-memory registers per
+// CTA merged with one atomicMax each. Sizes block-set directories, where a
+// few percent do not matter and the exact count's 54-bit radix sort does.
+constexpr int kHllBits = 12;
+constexpr int kHllRegs = 1 << kHllBits;
+__global__ void block_sketch_kernel(const u64* __restrict__ keys, u64 n, u32 shift, u32 arity, u32* __restrict__ regs) {
+    __shared__ u32 s[kHllRegs];
+    for (u32 i = threadIdx.x; i < kHllRegs; i += blockDim.x) s[i] = 0;
+    __syncthreads();
+    GRID_STRIDE(i, n) {
+        u32 bp;
+        const u64 h = mix64(block_of(keys[i], shift, arity, &bp));
+        const u32 idx = static_cast<u32>(h >> (64 - kHllBits));
+        const u32 rho = static_cast<u32>(__clzll((h << kHllBits) | (u64(1) << (kHllBits - 1)))) + 1;
+        atomicMax(s + idx, rho);
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < kHllRegs; i += blockDim.x)
+        if (s[i]) atomicMax(regs + i, s[i]);
+}
+
 struct DistinctOp {
     const u64* v;
     __device__ u64 value(u64 i) const { return (i == 0 || v[i] != v[i - 1]) ? 1 : 0; }
@@ -2918,6 +2941,30 @@ void engine_mask_u64(Ctx* c, u64* p, u64 n, u64 and_mask, u64 or_bits) {
     mask_u64_kernel<<<grid_for(n), 256, 0, c->stream>>>(p, n, and_mask, or_bits);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
+}
+
+void engine_block_sketch(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity, u32* regs) {
+    FV_CUDA(cudaMemsetAsync(regs, 0, 4 * kHllRegs, c->stream));
+    if (!n) return;
+    const u64 want = ceil_div(n, 256 * 16);
+    const unsigned grid = static_cast<unsigned>(std::max<u64>(1, std::min<u64>(want, u64(kNumSMs) * 2)));
+    ProfScope prof(c, "count_blocks", 8.0 * double(n));
+    block_sketch_kernel<<<grid, 256, 0, c->stream>>>(keys, n, shift, arity, regs);
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+u64 block_sketch_estimate(const u32* regs) {
+    const double m = kHllRegs;
+    double sum = 0;
+    u64 zeros = 0;
+    for (int i = 0; i < kHllRegs; ++i) {
+        sum += std::ldexp(1.0, -static_cast<int>(regs[i]));
+        zeros += regs[i] == 0;
+    }
+    double e = (0.7213 / (1.0 + 1.079 / m)) * m * m / sum;
+    if (e <= 2.5 * m && zeros) e = m * std::log(m / double(zeros));  // small range: linear counting
+    return static_cast<u64>(std::ceil(e));
 }
 
 }  // namespace fv
