@@ -112,7 +112,8 @@ void version_reconstruct(const Version& v, u32* rows_out);
 
 // Lexicographic (row, id) ordering permutation of a version's rows via
 // stable LSD passes over the columns (last column first).
-DBuf<u32> lexicographic_order(Ctx* c, const u32* const* cols, u32 arity, u64 n);
+DBuf<u32> lexicographic_order(Ctx* c, const u32* const* cols, u32 arity, u64 n,
+                              const char* who = __builtin_FUNCTION());
 
 // Process-wide gather counter (P/src/column.cpp:10-15).
 void add_gather_volume(u64 n);

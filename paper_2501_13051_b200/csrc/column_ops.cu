@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // Column-store operators on sm_100a: the device implementations behind the
 // operator-level C ABI (P/src/column.cpp, P/src/relation.cpp,
 // P/src/kernels.cpp). Orders reproduce the reference wherever its tests pin
@@ -562,7 +564,10 @@ std::unique_ptr<Version> project(Ctx* c, const Version& v, const u32* ids, u64 n
     return version_from_device(c, std::move(cols), n);
 }
 
-DBuf<u32> lexicographic_order(Ctx* c, const u32* const* cols, u32 arity, u64 n) {
+DBuf<u32> lexicographic_order(Ctx* c, const u32* const* cols, u32 arity, u64 n, const char* who) {
+    static const bool trace_sorts = std::getenv("FVLOG_TRACE_SORTS") != nullptr;
+    if (trace_sorts) std::fprintf(stderr, "[sort-call] lexicographic_order from %s n=%llu arity=%u\n", who,
+                                  static_cast<unsigned long long>(n), arity);
     DBuf<u32> perm(c, n), perm_alt(c, n), keys(c, n), keys_alt(c, n);
     iota_u32(c, perm.get(), n);
     for (int j = static_cast<int>(arity) - 1; j >= 0; --j) {

@@ -557,6 +557,7 @@ void engine_route(Ctx* c, u64 n, const RouteKey& key, u32 world, const std::vect
 // Sort packed row keys lexicographically. group_only (one-word keys only):
 // order by the first column alone (rows grouped for a column-0 join index;
 // within a group the order is unspecified) — skips the low-column passes.
-void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift, bool group_only = false);
+void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift, bool group_only = false,
+                      const char* who = __builtin_FUNCTION());
 
 }  // namespace fv

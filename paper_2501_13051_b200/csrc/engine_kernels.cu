@@ -13,6 +13,7 @@
 //                 (relation.cpp:71-108, kernels.cpp:210-268) as ONE
 //                 merge-path pass over sorted FULL and sorted candidates.
 #include <cmath>
+#include <cstdio>
 #include <optional>
 #include <cstdlib>
 
@@ -2903,7 +2904,11 @@ u64 engine_fingerprint(Ctx* c, const std::vector<const u32*>& cols, u64 n, u32 a
     return h;
 }
 
-void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift, bool group_only) {
+void engine_sort_keys(Ctx* c, std::vector<DBuf<u64>>& words, u64 n, u32 arity, u32 shift, bool group_only,
+                      const char* who) {
+    static const bool trace_sorts = std::getenv("FVLOG_TRACE_SORTS") != nullptr;
+    if (trace_sorts) std::fprintf(stderr, "[sort-call] engine_sort_keys from %s n=%llu arity=%u\n", who,
+                                  static_cast<unsigned long long>(n), arity);
     if (n <= 1) return;
     const u32 W = static_cast<u32>(words.size());
     auto word_bits = [&](u32 w) -> u32 {
