@@ -1385,6 +1385,9 @@ __global__ void blockset_insert_kernel(const u64* __restrict__ keys, u64 n, Bloc
 // words. Words first written to DELTA this iteration are appended to
 // new_keys (new bits counted in *new_tuples), entries without a directory
 // slot go to the overflow list with their full mask.
+#ifndef FV_INSERT_WARP_COMBINE
+#define FV_INSERT_WARP_COMBINE 1
+#endif
 __global__ void blockset_word_insert_kernel(const u64* __restrict__ keys, const u32* __restrict__ bits_in, u64 n,
                                             BlockSetArgs s, u64* __restrict__ new_keys, u32* __restrict__ new_widx,
                                             u64* new_count, u64* new_tuples, u64* __restrict__ ovf,
@@ -1409,6 +1412,22 @@ __global__ void blockset_word_insert_kernel(const u64* __restrict__ keys, const 
             live |= 1u << k;
         }
     }
+#if FV_INSERT_WARP_COMBINE
+    // Lanes holding the same word (sorted inputs: a seed or a copy of a
+    // sorted version — consecutive keys share words and blocks) OR their
+    // masks first; only one of them goes to the set.
+    const u32 lane = lane_id();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const u64 wk = ((live >> k) & 1u) ? key[k] : ~u64(lane);  // out-of-range lanes: unique
+        const u32 peers = __match_any_sync(0xffffffffu, wk);
+        const u32 m = __reduce_or_sync(peers, b[k]);
+        if ((live >> k) & 1u) {
+            if (lane == static_cast<u32>(__ffs(peers) - 1)) b[k] = m;
+            else live &= ~(1u << k);
+        }
+    }
+#endif
     u32 om, first, ones, widx[ITEMS];
     blockset_word_items(s, live, key, b, &first, &ones, &om, widx);
     append_words(new_keys, new_widx, new_count, new_tuples, ones, first, key, widx);
