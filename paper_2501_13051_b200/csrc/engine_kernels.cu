@@ -220,7 +220,13 @@ __device__ __forceinline__ u64 block_home(u64 bid, u64 mask) { return mix64(bid)
 // claims an empty slot for a new block. ~0: no slot (overflow).
 // (Arguments by value: a reference into the kernel's parameter block would
 // force the whole OutSpec into local memory.)
-__device__ __forceinline__ u64 blockset_find(u64* dir, u64 mask, u64* count, u64 limit, u64 bid, u64 h, u64 v) {
+// *inserted counts this thread's new blocks; the caller adds a warp's total
+// to the block count with one atomic (a single hot counter otherwise takes
+// one atomic per new block). The limit check reads a count that may lag by
+// the warps in flight — the load limit is 3/4 of capacity, and a full probe
+// window still falls back to the overflow list.
+__device__ __forceinline__ u64 blockset_find(u64* dir, u64 mask, u64* count, u64 limit, u64 bid, u64 h, u64 v,
+                                             u32* inserted) {
     for (int probe = 0; probe < kBlockMaxProbes; ++probe) {
         if (v == bid) return h;
         if (v == kEmptySlot) {
@@ -228,7 +234,7 @@ __device__ __forceinline__ u64 blockset_find(u64* dir, u64 mask, u64* count, u64
             const u64 prev = atomicCAS(reinterpret_cast<unsigned long long*>(dir + h), ~0ull,
                                        static_cast<unsigned long long>(bid));
             if (prev == ~0ull) {
-                atomicAdd(reinterpret_cast<unsigned long long*>(count), 1ull);
+                ++*inserted;
                 return h;
             }
             if (prev == bid) return h;
@@ -237,6 +243,12 @@ __device__ __forceinline__ u64 blockset_find(u64* dir, u64 mask, u64* count, u64
         v = __ldcg(dir + h);
     }
     return ~u64(0);
+}
+
+// One atomic per warp for its lanes' new blocks (call from all 32 lanes).
+__device__ __forceinline__ void add_block_count(u64* count, u32 inserted) {
+    const u32 t = __reduce_add_sync(0xffffffffu, inserted);
+    if (lane_id() == 0 && t) atomicAdd(reinterpret_cast<unsigned long long*>(count), static_cast<unsigned long long>(t));
 }
 
 // Set-insert of N keys (bit k of `live`: key[k] is a candidate). All
@@ -257,18 +269,19 @@ __device__ __forceinline__ u32 blockset_insert_items(const BlockSetArgs& s, u32 
     u64 dv[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) dv[k] = ((live >> k) & 1u) ? __ldcg(s.dir + block_home(slot[k], s.mask)) : 0;
-    u32 om = 0;
+    u32 om = 0, inserted = 0;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         if (!((live >> k) & 1u)) continue;
         const u64 bid = slot[k], h = block_home(bid, s.mask);
-        const u64 f = dv[k] == bid ? h : blockset_find(s.dir, s.mask, s.count, s.limit, bid, h, dv[k]);
+        const u64 f = dv[k] == bid ? h : blockset_find(s.dir, s.mask, s.count, s.limit, bid, h, dv[k], &inserted);
         if (f == ~u64(0)) {
             om |= 1u << k;
             live &= ~(1u << k);
         }
         slot[k] = f;
     }
+    add_block_count(s.count, inserted);
     u32 wv[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) wv[k] = ((live >> k) & 1u) ? __ldcg(s.bits + slot[k] * 32 + (bp[k] >> 5)) : 0;
@@ -331,18 +344,19 @@ __device__ __forceinline__ void blockset_word_items(const BlockSetArgs& s, u32 l
     u64 dv[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) dv[k] = ((live >> k) & 1u) ? __ldcg(s.dir + block_home(slot[k], s.mask)) : 0;
-    u32 om = 0;
+    u32 om = 0, inserted = 0;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         if (!((live >> k) & 1u)) continue;
         const u64 bid = slot[k], h = block_home(bid, s.mask);
-        const u64 f = dv[k] == bid ? h : blockset_find(s.dir, s.mask, s.count, s.limit, bid, h, dv[k]);
+        const u64 f = dv[k] == bid ? h : blockset_find(s.dir, s.mask, s.count, s.limit, bid, h, dv[k], &inserted);
         if (f == ~u64(0)) {
             om |= 1u << k;
             live &= ~(1u << k);
         }
         slot[k] = f * 32 + wi[k];  // bitmap word index from here on
     }
+    add_block_count(s.count, inserted);
     u32 nb[N];
 #if FV_WORD_TEST_LOAD
     // a plain load first: a word whose bits are all present takes no atomic
