@@ -1950,9 +1950,10 @@ public:
                 // tuples), then expand them: the tuples come out grouped by x
                 // with no tuple-level sort or scatter.
                 DBuf<u32> wb(c_, nw);
-                if (engine_group_keys(c_, s.keys, nw, st_.key_shift, nullptr, nullptr, nullptr, s.bits.get(),
+                JoinIndex word_runs;
+                if (engine_group_keys(c_, s.keys, nw, st_.key_shift, &word_runs, nullptr, nullptr, s.bits.get(),
                                       wb.get())) {
-                    const u64 nd = install_word_delta(r, s.keys.get(), wb.get(), nw, tuples);
+                    const u64 nd = install_word_delta(r, s.keys.get(), wb.get(), nw, tuples, &word_runs);
                     s.keys = DBuf<u64>();
                     s.cap = 0;
                     if (r.word_sparse && !r.temp) leave_word_mode(r);
@@ -2027,7 +2028,8 @@ public:
     // Levels-mode binary relation: DELTA = the tuples of nw word entries
     // (word key, mask) already grouped by x (nd tuples in all), with its
     // column-0 direct index; the previous DELTA becomes a level.
-    u64 install_word_delta(RelState& r, const u64* wkeys, const u32* wb, u64 nw, u64 nd) {
+    u64 install_word_delta(RelState& r, const u64* wkeys, const u32* wb, u64 nw, u64 nd,
+                           const JoinIndex* word_runs = nullptr) {
         invalidate(r);
         if (r.delta.n) r.levels.push_back(std::move(r.delta));
         DevVersion Dv;
@@ -2035,9 +2037,16 @@ public:
         for (u32 j = 0; j < 2; ++j) Dv.cols.emplace_back(c_, std::max<u64>(nd, 1));
         r.keys.count += nd;
         r.level_rows += nd;
-        engine_expand_word_keys(c_, wkeys, wb, nw, nullptr, Dv.cols[0].get(), Dv.cols[1].get(), st_.key_shift);
+        DBuf<u64> off(c_, nw + 1);
+        engine_expand_word_keys(c_, wkeys, wb, nw, nullptr, Dv.cols[0].get(), Dv.cols[1].get(), st_.key_shift,
+                                off.get());
         auto di = std::make_unique<JoinIndex>();
-        engine_build_runs(c_, Dv.cols[0].get(), nd, *di, st_.key_shift, true);
+        // DELTA's column-0 index from the words' runs (one pass over the
+        // value domain) instead of a pass over the expanded tuples
+        if (word_runs && word_runs->domain && word_runs->ucount.get())
+            engine_word_index_to_tuples(c_, *word_runs, off.get(), *di);
+        else
+            engine_build_runs(c_, Dv.cols[0].get(), nd, *di, st_.key_shift, true);
         r.delta = std::move(Dv);
         di->rows = &r.delta;
         r.indexes.emplace(std::make_pair(static_cast<int>(kDelta), 0u), std::move(di));

@@ -468,8 +468,14 @@ void engine_block_sketch(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity, u
 u64 block_sketch_estimate(const u32* regs);
 // Packed tuple keys of n word entries (word key, mask) into out, sized by
 // the caller to the sum of the masks' popcounts (no host readback).
+// off_out (optional, n + 1 entries): each entry's first tuple (and the
+// total at [n]) kept for the caller.
 void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out, u32* out_x = nullptr,
-                             u32* out_z = nullptr, u32 shift = 0);
+                             u32* out_z = nullptr, u32 shift = 0, u64* off_out = nullptr);
+// A direct index over word entries grouped by x (counting-sort runs: word
+// start + word count per value) -> the direct index of their expanded tuples
+// (interleaved (start, end) pairs), from the entries' tuple offsets.
+void engine_word_index_to_tuples(Ctx* c, const JoinIndex& words, const u64* off, JoinIndex& out);
 // Word form (x, z base, mask) of a lexicographically sorted binary version
 // of n rows; outputs sized n; returns the word count.
 u64 engine_tuples_to_words(Ctx* c, const u32* c0, const u32* c1, u64 n, u32* x, u32* zb, u32* bits,

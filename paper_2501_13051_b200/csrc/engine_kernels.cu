@@ -1505,9 +1505,13 @@ __global__ void blockset_collect_kernel(const u64* __restrict__ keys, const u32*
 // Exclusive prefix of the masks' popcounts (the tuples' output offsets).
 struct PopcOffsetsOp {
     const u32* bits;
-    u64* off;
+    u64* off;  // n + 1 entries: off[n] = the total
+    u64 n;
     __device__ u64 value(u64 i) const { return __popc(bits[i]); }
-    __device__ void emit(u64 i, u64 p, u64) const { off[i] = p; }
+    __device__ void emit(u64 i, u64 p, u64 v) const {
+        off[i] = p;
+        if (i == n - 1) off[n] = p + v;
+    }
 };
 
 // Warp-cooperative expansion of word entries into packed tuple keys: a warp
@@ -2213,12 +2217,17 @@ void engine_blockset_collect(Ctx* c, const u64* keys, const u32* widx, u64 n, co
 }
 
 void engine_expand_word_keys(Ctx* c, const u64* keys, const u32* bits, u64 n, u64* out, u32* out_x, u32* out_z,
-                             u32 shift) {
+                             u32 shift, u64* off_out) {
     if (!n) return;
-    DBuf<u64> off(c, n);
+    DBuf<u64> off_own;
+    u64* off = off_out;
+    if (!off) {
+        off_own = DBuf<u64>(c, n + 1);
+        off = off_own.get();
+    }
     ProfScope prof(c, "expand_words", 12.0 * double(n));
-    tile_scan(c, PopcOffsetsOp{bits, off.get()}, n, nullptr);
-    expand_word_keys_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, bits, off.get(), n, out, out_x, out_z, shift);
+    tile_scan(c, PopcOffsetsOp{bits, off, n}, n, nullptr);
+    expand_word_keys_kernel<<<grid_for(n), 256, 0, c->stream>>>(keys, bits, off, n, out, out_x, out_z, shift);
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }
@@ -3003,6 +3012,38 @@ u64 block_sketch_estimate(const u32* regs) {
     double e = (0.7213 / (1.0 + 1.079 / m)) * m * m / sum;
     if (e <= 2.5 * m && zeros) e = m * std::log(m / double(zeros));  // small range: linear counting
     return static_cast<u64>(std::ceil(e));
+}
+
+// Tuple-space (start, end) pairs of a direct index over word entries: value
+// v's words [wstart[v], wstart[v] + wcount[v]) hold tuples
+// [off[wstart[v]], off[wstart[v] + wcount[v]]) (off[n] = the tuple total).
+__global__ void word_runs_to_tuples_kernel(const u32* __restrict__ wstart, const u32* __restrict__ wcount,
+                                           const u64* __restrict__ off, u64 domain, u32* __restrict__ pair) {
+    GRID_STRIDE(v, domain) {
+        const u32 cnt = wcount[v];
+        u32 s = 0, e = 0;
+        if (cnt) {
+            s = static_cast<u32>(off[wstart[v]]);
+            e = static_cast<u32>(off[u64(wstart[v]) + cnt]);
+        }
+        pair[2 * v] = s;
+        pair[2 * v + 1] = e;
+    }
+}
+
+void engine_word_index_to_tuples(Ctx* c, const JoinIndex& words, const u64* off, JoinIndex& out) {
+    out.domain = words.domain;
+    out.ends = true;
+    out.n_unique = words.n_unique;
+    out.ukeys = DBuf<u32>();
+    out.ucount = DBuf<u32>();
+    out.ht = HashIndex();
+    out.ustart = DBuf<u32>(c, 2 * words.domain);
+    ProfScope prof(c, "direct_index", 16.0 * double(words.domain));
+    word_runs_to_tuples_kernel<<<grid_for(words.domain), 256, 0, c->stream>>>(words.ustart.get(), words.ucount.get(),
+                                                                              off, words.domain, out.ustart.get());
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
 }
 
 }  // namespace fv
