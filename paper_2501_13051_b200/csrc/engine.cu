@@ -1259,6 +1259,22 @@ public:
             wp.push_back(words.back().get());
         }
         engine_pack_keys(c_, cols, x.n, st_.key_shift, wp.data());
+        if (measure && W == 1 && !exact_blocks_) {
+            // Measure with a sketch of the distinct keys (one pass) and only
+            // sort-unique when it shows enough repeats (SG's intermediates
+            // have none: three measuring sorts of up to 2.8e7 rows).
+            DBuf<u32> regs(c_, kBlockSketchRegs);
+            engine_block_sketch(c_, words[0].get(), x.n, st_.key_shift, 0, regs.get());
+            std::vector<u32> h(kBlockSketchRegs);
+            regs.download(h.data(), kBlockSketchRegs);
+            const u64 est = std::min<u64>(x.n, block_sketch_estimate(h.data()));
+            policy.measured = x.n;
+            if (trace_)
+                std::fprintf(stderr, "[fvlog]   intermediate sketch %llu -> ~%llu distinct\n",
+                             static_cast<unsigned long long>(x.n), static_cast<unsigned long long>(est));
+            if (4 * est > 3 * x.n) return;  // < 1/4 repeats: leave it
+            policy.on = true;
+        }
         engine_sort_keys(c_, words, x.n, a, st_.key_shift);
         std::vector<DBuf<u32>> out;
         std::vector<u32*> op;
@@ -1270,7 +1286,7 @@ public:
         if (trace_)
             std::fprintf(stderr, "[fvlog]   intermediate dedup %llu -> %llu (%s)\n", static_cast<unsigned long long>(x.n),
                          static_cast<unsigned long long>(k), policy.on ? "on" : "measured");
-        if (measure) {
+        if (measure && !policy.on) {
             policy.measured = x.n;
             policy.on = 4 * k <= 3 * x.n;
         }

@@ -461,8 +461,9 @@ u64 engine_count_blocks(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity);
 // The same count left in *d_out on the device (no host round trip).
 void engine_count_blocks_async(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity, u64* d_out);
 // HyperLogLog sketch of the distinct block ids (kBlockSketchRegs u32
-// registers at regs, zeroed by the call); block_sketch_estimate turns the
-// downloaded registers into a count (~1.6 % standard error).
+// registers at regs, zeroed by the call; arity 0: of the distinct keys);
+// block_sketch_estimate turns the downloaded registers into a count (~1.6 %
+// standard error).
 constexpr int kBlockSketchRegs = 4096;
 void engine_block_sketch(Ctx* c, const u64* keys, u64 n, u32 shift, u32 arity, u32* regs);
 u64 block_sketch_estimate(const u32* regs);

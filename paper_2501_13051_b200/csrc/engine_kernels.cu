@@ -1640,7 +1640,8 @@ __global__ void block_sketch_kernel(const u64* __restrict__ keys, u64 n, u32 shi
     __syncthreads();
     GRID_STRIDE(i, n) {
         u32 bp;
-        const u64 h = mix64(block_of(keys[i], shift, arity, &bp));
+        // arity 0: the distinct keys themselves (not their blocks)
+        const u64 h = mix64(arity ? block_of(keys[i], shift, arity, &bp) : keys[i]);
         const u32 idx = static_cast<u32>(h >> (64 - kHllBits));
         const u32 rho = static_cast<u32>(__clzll((h << kHllBits) | (u64(1) << (kHllBits - 1)))) + 1;
         atomicMax(s + idx, rho);
