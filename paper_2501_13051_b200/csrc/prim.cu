@@ -16,12 +16,19 @@ __global__ void gather_kernel(const u32* __restrict__ src, const u32* __restrict
         out[i] = src[idx[i]];
 }
 
+// One global atomicMax per CTA (a per-warp atomic on the single output word
+// serialised ~20 K atomics per launch).
 __global__ void reduce_max_kernel(const u32* __restrict__ in, u64 n, unsigned long long* out) {
+    __shared__ u32 s_max;
+    if (threadIdx.x == 0) s_max = 0;
+    __syncthreads();
     u32 m = 0;
     for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
         m = max(m, in[i]);
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane_id() == 0) atomicMax(out, static_cast<unsigned long long>(m));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane_id() == 0 && m) atomicMax(&s_max, m);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_max) atomicMax(out, static_cast<unsigned long long>(s_max));
 }
 
 unsigned grid_for(u64 n, int block = 256) {
@@ -44,7 +51,9 @@ void exclusive_scan_counts(Ctx* c, const u32* counts, u64* offsets, u64 n) {
 void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out, bool accumulate) {
     if (!accumulate) FV_CUDA(cudaMemsetAsync(d_out, 0, sizeof(u64), c->stream));
     if (n == 0) return;
-    reduce_max_kernel<<<grid_for(n), 256, 0, c->stream>>>(in, n,
+    const u64 want = ceil_div(n, u64(256) * 16);  // >= 16 items per thread
+    const unsigned grid = static_cast<unsigned>(want < u64(kNumSMs) * 4 ? (want ? want : 1) : u64(kNumSMs) * 4);
+    reduce_max_kernel<<<grid, 256, 0, c->stream>>>(in, n,
                                                          reinterpret_cast<unsigned long long*>(d_out));
     FV_CUDA(cudaGetLastError());
     c->count_launch();
