@@ -357,9 +357,10 @@ def test_keyset_growth_paths_match_reference(ctx, grow, monkeypatch):
     {"FVLOG_PROBE_SCAN": "0"},                                # join counts written, then scanned by a second kernel
     {"FVLOG_GROUPED_EXPAND": "0"},                            # tuple DELTA of a word sink via a tuple-level counting sort
     {"FVLOG_EXACT_BLOCKS": "1"},                              # directories sized by exact block counts, not the sketch
+    {"FVLOG_BLOCK_HEADROOM": "2"},                            # directories grown to 2x their blocks (more growth passes)
 ], ids=["keyset", "blocks", "blocks-overflow", "blocks-convert", "blocks-no-tile-set", "no-words",
         "words-overflow", "words-leave", "words-no-combine", "dump-sort", "inter-words", "inter-sort",
-        "reverse-always", "reverse-never", "by1-resort", "scatter-gather", "no-precount", "no-seed-batch", "no-probe-scan", "no-grouped-expand", "exact-blocks"])
+        "reverse-always", "reverse-never", "by1-resort", "scatter-gather", "no-precount", "no-seed-batch", "no-probe-scan", "no-grouped-expand", "exact-blocks", "headroom-2"])
 def test_dedup_sets_match_reference(ctx, setmode, monkeypatch):
     # FULL's dedup structure for binary/unary IDB relations: a BlockSet
     # (blocked bitmap, default) or a KeySet; every path must give the
