@@ -2497,8 +2497,13 @@ std::unique_ptr<EvalState> evaluate_device(Ctx* c, const std::vector<RelationDec
             for (auto& cs : s.const_selects) vmax = std::max<u64>(vmax, cs.second);
     u64* dmax = c->d_scalars + 22;  // one max over every EDB column, one readback
     FV_CUDA(cudaMemsetAsync(dmax, 0, sizeof(u64), c->stream));
-    for (auto& [name, vp] : raw)
-        for (auto& col : vp->cols) reduce_max_u32(c, col.get(), vp->n, dmax, true);
+    {
+        std::vector<std::pair<const u32*, u64>> cols;  // every EDB column, one launch
+        for (auto& [name, vp] : raw)
+            for (auto& col : vp->cols)
+                if (vp->n) cols.emplace_back(col.get(), vp->n);
+        reduce_max_u32_multi(c, cols, dmax);
+    }
     {
         u64 m = 0;
         c->read_scalars(dmax, &m, 1);

@@ -1,6 +1,10 @@
 // Small device helpers shared by the operator kernels.
 #include "prim.cuh"
 
+#include <algorithm>
+#include <utility>
+#include <vector>
+
 namespace fv {
 
 namespace {
@@ -55,6 +59,45 @@ void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out, bool accumulate) {
     const unsigned grid = static_cast<unsigned>(want < u64(kNumSMs) * 4 ? (want ? want : 1) : u64(kNumSMs) * 4);
     reduce_max_kernel<<<grid, 256, 0, c->stream>>>(in, n,
                                                          reinterpret_cast<unsigned long long*>(d_out));
+    FV_CUDA(cudaGetLastError());
+    c->count_launch();
+}
+
+namespace {
+struct ColSpan {
+    const u32* p;
+    u64 n;
+};
+// blockIdx.y: the column; one global atomic per CTA.
+__global__ void reduce_max_multi_kernel(const ColSpan* __restrict__ cols, unsigned long long* out) {
+    __shared__ u32 s_max;
+    if (threadIdx.x == 0) s_max = 0;
+    __syncthreads();
+    const ColSpan cs = cols[blockIdx.y];
+    u32 m = 0;
+    for (u64 i = u64(blockIdx.x) * blockDim.x + threadIdx.x; i < cs.n; i += u64(gridDim.x) * blockDim.x)
+        m = max(m, cs.p[i]);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane_id() == 0 && m) atomicMax(&s_max, m);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_max) atomicMax(out, static_cast<unsigned long long>(s_max));
+}
+}  // namespace
+
+void reduce_max_u32_multi(Ctx* c, const std::vector<std::pair<const u32*, u64>>& cols, u64* d_out) {
+    if (cols.empty()) return;
+    std::vector<ColSpan> h;
+    u64 longest = 0;
+    for (auto& [p, n] : cols) {
+        h.push_back({p, n});
+        longest = std::max(longest, n);
+    }
+    DBuf<ColSpan> d(c, h.size());
+    d.upload(h.data(), h.size());
+    const u64 want = ceil_div(longest, u64(256) * 16);
+    const unsigned gx = static_cast<unsigned>(std::max<u64>(1, std::min<u64>(want, u64(kNumSMs) * 4)));
+    reduce_max_multi_kernel<<<dim3(gx, static_cast<unsigned>(h.size())), 256, 0, c->stream>>>(
+        d.get(), reinterpret_cast<unsigned long long*>(d_out));
     FV_CUDA(cudaGetLastError());
     c->count_launch();
 }

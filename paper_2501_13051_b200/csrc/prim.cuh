@@ -10,6 +10,9 @@
 
 #include "fv_common.cuh"
 
+#include <utility>
+#include <vector>
+
 namespace fv {
 
 #ifndef FV_SCAN_BLOCK
@@ -209,6 +212,8 @@ void exclusive_scan_counts(Ctx* c, const u32* counts, u64* offsets, u64 n);
 // Device reductions returning to a device scalar.
 // accumulate: fold into the existing *d_out (max) instead of resetting it.
 void reduce_max_u32(Ctx* c, const u32* in, u64 n, u64* d_out, bool accumulate = false);
+// max over several columns into *d_out (accumulates: atomicMax), one launch.
+void reduce_max_u32_multi(Ctx* c, const std::vector<std::pair<const u32*, u64>>& cols, u64* d_out);
 
 // Fill / iota helpers.
 void iota_u32(Ctx* c, u32* out, u64 n);
